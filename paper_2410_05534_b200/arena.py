@@ -1,0 +1,167 @@
+"""SoA e-graph arena: the layout shared by the host, the CPU oracle and the device.
+
+One *leaf* is one e-graph state in the form the reference's rebuild consumes
+(egraph.py:203-226): the insertion-ordered hashcons list ``(node, class id)``
+plus the union-find arrays. Order is semantic (rebuild scans hashcons in
+insertion order and the survivor of a congruent pair is the first entry,
+SURVEY Appendix A.2), so it is kept verbatim.
+
+Per leaf (all little-endian, dense):
+    hc_sym   u32[n]     interned symbol of hashcons entry i (symtab.py)
+    hc_koff  u32[n+1]   CSR offsets into hc_kids (arity = hc_koff[i+1]-hc_koff[i])
+    hc_kids  u32[K]     child class ids as stored in the key (may be stale)
+    hc_cid   u32[n]     class id value of the entry
+    hc_cost  f64[n]     operator cost of the node (cost_model.py), carried by rebuild
+    uf_parent u32[U]    union-find parents, U = ids ever created (egraph.py:87-91)
+    uf_rank   u8[U]     union-by-rank ranks (egraph.py:103-115)
+    root      u32       raw root id (0xFFFFFFFF = none)
+
+A *batch* concatenates leaves; per-leaf base offsets index every array.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+NONE = 0xFFFFFFFF
+
+
+@dataclass
+class LeafState:
+    hc_sym: np.ndarray
+    hc_koff: np.ndarray
+    hc_kids: np.ndarray
+    hc_cid: np.ndarray
+    hc_cost: np.ndarray
+    uf_parent: np.ndarray
+    uf_rank: np.ndarray
+    root: int = NONE
+
+    @property
+    def n(self) -> int:
+        return int(self.hc_sym.shape[0])
+
+    @property
+    def n_ids(self) -> int:
+        return int(self.uf_parent.shape[0])
+
+    @property
+    def n_kids(self) -> int:
+        return int(self.hc_kids.shape[0])
+
+    def to_json(self) -> dict:
+        return {
+            "hc_sym": self.hc_sym.tolist(),
+            "hc_koff": self.hc_koff.tolist(),
+            "hc_kids": self.hc_kids.tolist(),
+            "hc_cid": self.hc_cid.tolist(),
+            "hc_cost": [float(x).hex() for x in self.hc_cost],
+            "uf_parent": self.uf_parent.tolist(),
+            "uf_rank": self.uf_rank.tolist(),
+            "root": int(self.root),
+        }
+
+    @classmethod
+    def from_json(cls, d: dict) -> "LeafState":
+        return cls(
+            np.array(d["hc_sym"], np.uint32),
+            np.array(d["hc_koff"], np.uint32),
+            np.array(d["hc_kids"], np.uint32),
+            np.array(d["hc_cid"], np.uint32),
+            np.array([float.fromhex(x) for x in d["hc_cost"]], np.float64),
+            np.array(d["uf_parent"], np.uint32),
+            np.array(d["uf_rank"], np.uint8),
+            int(d["root"]),
+        )
+
+
+def _class_shape(egraph, cid):
+    cls = egraph.classes.get(egraph.find(cid))
+    if cls is None:
+        return None
+    for node in cls.nodes:
+        payload = node.symbol.payload
+        return payload[1] if isinstance(payload, tuple) and len(payload) == 2 else None
+    return None
+
+
+def export_state(egraph, symtab, cost_config=None, costs: dict | None = None) -> LeafState:
+    """Snapshot an e-graph (reference ``EGraph`` or ours, duck-typed) as a leaf.
+
+    Node costs come from ``costs`` (canonical ENode -> float) when given, else
+    from ``cost_config`` through cost_model.node_cost on the child class shapes.
+    """
+    from .cost_model import node_cost
+
+    language = egraph.language
+    items = list(egraph.hashcons.items())
+    n = len(items)
+    sym = np.empty(n, np.uint32)
+    koff = np.zeros(n + 1, np.uint32)
+    cid = np.empty(n, np.uint32)
+    cost = np.zeros(n, np.float64)
+    kids: list[int] = []
+    shape_cache: dict = {}
+    for i, (node, c) in enumerate(items):
+        sym[i] = symtab.intern(node.symbol, language)
+        kids.extend(node.children)
+        koff[i + 1] = len(kids)
+        cid[i] = c
+        if costs is not None:
+            cost[i] = costs.get(egraph.canonicalize(node), 0.0)
+        elif cost_config is not None:
+            shapes = []
+            for ch in node.children:
+                r = egraph.find(ch)
+                if r not in shape_cache:
+                    shape_cache[r] = _class_shape(egraph, r)
+                shapes.append(shape_cache[r])
+            cost[i] = node_cost(cost_config, node.symbol, tuple(shapes))
+    uf = egraph._uf
+    return LeafState(
+        sym,
+        koff,
+        np.array(kids, np.uint32),
+        cid,
+        cost,
+        np.array(uf.parent, np.uint32),
+        np.array(uf.rank, np.uint8),
+        NONE if egraph.root is None else int(egraph.root),
+    )
+
+
+@dataclass
+class Batch:
+    """Concatenated leaves with per-leaf bases (the C-ABI upload format)."""
+
+    leaves: list = field(default_factory=list)
+
+    def pack(self) -> dict:
+        L = len(self.leaves)
+        nb = np.zeros(L + 1, np.uint64)
+        kb = np.zeros(L + 1, np.uint64)
+        ub = np.zeros(L + 1, np.uint64)
+        for i, lf in enumerate(self.leaves):
+            nb[i + 1] = nb[i] + lf.n
+            kb[i + 1] = kb[i] + lf.n_kids
+            ub[i + 1] = ub[i] + lf.n_ids
+        cat = lambda name, dt: (np.concatenate([getattr(lf, name) for lf in self.leaves]).astype(dt, copy=False)
+                                if L else np.zeros(0, dt))
+        # per-leaf CSR offsets are leaf-relative; store n+1 entries per leaf
+        koff = np.concatenate([lf.hc_koff for lf in self.leaves]).astype(np.uint32) if L else np.zeros(0, np.uint32)
+        return {
+            "n_leaves": L,
+            "node_base": nb,
+            "kid_base": kb,
+            "id_base": ub,
+            "hc_sym": cat("hc_sym", np.uint32),
+            "hc_koff": koff,
+            "hc_kids": cat("hc_kids", np.uint32),
+            "hc_cid": cat("hc_cid", np.uint32),
+            "hc_cost": cat("hc_cost", np.float64),
+            "uf_parent": cat("uf_parent", np.uint32),
+            "uf_rank": cat("uf_rank", np.uint8),
+            "root": np.array([lf.root for lf in self.leaves], np.uint32),
+        }
