@@ -1,0 +1,144 @@
+/*
+ * esat_b200 -- C ABI of the B200-native (sm_100a) hot path of the MCTS-guided
+ * equality-saturation optimizer (arXiv 2410.05534; reference = /root/reference/pkg/src/esat).
+ *
+ * The reference's boundary for this path is a pure-Python function-level API (no plugin
+ * registry or FFI exists). Each entry point below replaces one reference
+ * function, batched over many e-graph "leaves" (MCTS leaves / rollout states):
+ *
+ *   esat_rebuild       <- EGraph.rebuild                 egraph.py:203-238 (+ _regroup)
+ *   esat_ematch        <- ematch / joint_match (1 source) rewrite.py:400-433
+ *   esat_ematch(EXISTS)<- is_rule_applicable             rewrite.py:579-589
+ *   esat_join          <- joint_match (>= 2 sources)      rewrite.py:405-433
+ *   esat_extract       <- extract_default_greedy          extraction.py:157-166
+ *                         extract_ocf_greedy              extraction.py:229-242
+ *                         (+ validate_extraction / _reachable_chosen, extraction.py:67-115)
+ *   esat_batch_upload  <- EGraph.snapshot into device slots (egraph.py:300-312)
+ *
+ * Plain C types only. All functions return ESAT_OK (0) or an ESAT_E_* code; the message
+ * is available from esat_last_error(ctx). Threading: one host thread per context (the
+ * reference's single-writer contract, egraph.py:133); a context owns one CUDA stream.
+ *
+ * ---------------------------------------------------------------------------------------
+ * Batch arena (host upload format; paper_2410_05534_b200/arena.py):
+ *   L leaves; per-leaf bases node_base/kid_base/id_base (uint64, L+1 entries each).
+ *   hc_sym  u32[N]   interned symbol per hashcons entry (insertion order = reference order)
+ *   hc_koff u32[N+L] CSR child offsets, n+1 leaf-relative entries per leaf at node_base[l]+l
+ *   hc_kids u32[K]   child class ids as stored in the entry key
+ *   hc_cid  u32[N]   class id stored for the entry
+ *   hc_cost f64[N]   operator cost of the node (cost model)
+ *   uf_parent u32[U], uf_rank u8[U]   union-find (egraph.py:80-115)
+ *   root    u32[L]   raw root id per leaf (0xFFFFFFFF = none)
+ *
+ * Clean view (written by esat_rebuild, read by ematch/extract), per leaf:
+ *   C classes with ascending canonical ids cls_id[C]; cls_off[C+1] node ranges; nodes in
+ *   node_sort_key order (egraph.py:65-70) with nd_sym, nd_cost, nd_koff (CSR) and nd_kpos
+ *   (children as class POSITIONS); nd_hc maps a view node to its new hashcons entry.
+ *
+ * Symbol table: name id, arity, rank (order of (name, repr(payload))), attribute codes
+ *   (order-preserving ints: ints numerically then strings) -- paper_2410_05534_b200/symtab.py.
+ *
+ * Pattern program (int32, paper_2410_05534_b200/patterns.py compile_pattern):
+ *   [P, V, Q] then P records of 6 words {kind(0 var/1 app), ident(var idx | name id),
+ *   arity, nslots(-1 = no attribute spec), slot_off, child_off} (offsets from the program
+ *   start), then attribute slots (>=0 literal code, <0 pvar -(q+1)), then child indices.
+ *   Var/pvar indices follow sorted names. A match record is W = 1+V+Q u32 words
+ *   [root class id][var class ids][pvar codes], sorted ascending and unique per leaf
+ *   (rewrite.py:396-397, 420-433).
+ */
+#ifndef ESAT_B200_H
+#define ESAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESAT_OK 0
+#define ESAT_E_ARG 1          /* bad argument -> ValueError / StructuralError            */
+#define ESAT_E_CUDA 2         /* CUDA runtime failure                                    */
+#define ESAT_E_CAPACITY 3     /* output/pool capacity exceeded -> grow and retry         */
+#define ESAT_E_STATE 4        /* call out of order (e.g. ematch before rebuild): the
+                                 reference's "requires a rebuilt e-graph" StructuralError */
+
+/* per-leaf extraction status (esat_extract) -> exception mapping in extraction.py */
+#define ESAT_X_OK 0
+#define ESAT_X_NOT_CONVERGED 1     /* ExtractionError("greedy extraction failed to converge") */
+#define ESAT_X_INFEASIBLE 2        /* InfeasibleExtraction("root e-class has no finite-cost program") */
+#define ESAT_X_CYCLIC 3            /* ExtractionError("cyclic selection through e-class %u") */
+#define ESAT_X_CHILD_NOT_CHOSEN 4  /* ExtractionError("child e-class %u required but not chosen") */
+#define ESAT_X_ROOT_NOT_CHOSEN 5   /* ExtractionError("root e-class not chosen") */
+#define ESAT_X_NO_ROOT 6           /* StructuralError("e-graph has no root") */
+#define ESAT_X_CAPACITY 7          /* OCF history pool too small: grow and retry */
+
+#define ESAT_METHOD_DEFAULT 0
+#define ESAT_METHOD_OCF 1
+
+#define ESAT_MATCH_LIST 0
+#define ESAT_MATCH_EXISTS 1
+
+typedef struct esat_ctx esat_ctx;
+typedef struct esat_batch esat_batch;
+
+/* context: one per GPU per process */
+int esat_ctx_create(int device, esat_ctx** out);
+int esat_ctx_destroy(esat_ctx* ctx);
+const char* esat_last_error(const esat_ctx* ctx);
+int esat_ctx_sync(esat_ctx* ctx);
+
+/* symbol table (replaces Symbol interning; egraph.py:34-70, rewrite.py:275-277) */
+int esat_symtab_upload(esat_ctx* ctx, uint32_t n_syms, const uint32_t* name_id, const uint32_t* arity,
+                       const uint32_t* rank, const uint32_t* param_off, const int32_t* param_codes);
+
+/* pattern programs (compiled from rewrite.py:43-65 patterns) */
+int esat_patterns_upload(esat_ctx* ctx, uint32_t n_patterns, const uint32_t* prog_off,
+                         uint32_t n_words, const int32_t* prog_words);
+
+/* batches: device-resident leaf arenas */
+int esat_batch_create(esat_ctx* ctx, uint32_t n_leaves, const uint64_t* node_base, const uint64_t* kid_base,
+                      const uint64_t* id_base, esat_batch** out);
+int esat_batch_destroy(esat_batch* b);
+int esat_batch_upload(esat_batch* b, const uint32_t* hc_sym, const uint32_t* hc_koff, const uint32_t* hc_kids,
+                      const uint32_t* hc_cid, const double* hc_cost, const uint32_t* uf_parent,
+                      const uint8_t* uf_rank, const uint32_t* root);
+
+/* EGraph.rebuild over every leaf; per-leaf merge counts stay on device (download below) */
+int esat_rebuild(esat_batch* b);
+
+/* e-match patterns[0..n) over every leaf (mode LIST or EXISTS) */
+int esat_ematch(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode);
+/* joint_match of multi-pattern rules over the LIST results of their source patterns.
+ * rule r: n_src[r] sources (pattern ids src[src_off[r]..]); var_map/pvar_map give the output
+ * slot of each source var/pvar (sorted combined names); out record = [S roots][NV][NQ]. */
+int esat_join(esat_batch* b, uint32_t n_rules, const uint32_t* src_off, const uint32_t* src,
+              const uint32_t* map_off, const uint32_t* var_map, const uint32_t* pvar_map,
+              const uint32_t* n_vars, const uint32_t* n_pvars);
+
+/* greedy extraction (method DEFAULT or OCF) over every leaf; OCF constituent histories live in a
+ * per-leaf pool of entries_per_node * n entries per pass parity (ESAT_X_CAPACITY -> grow, retry) */
+int esat_batch_set_pool(esat_batch* b, double entries_per_node);
+int esat_extract(esat_batch* b, int method);
+
+/* downloads (host buffers sized from the batch bases) */
+int esat_download_rebuild(esat_batch* b, uint32_t* n_out, uint32_t* merges, uint32_t* hc_sym, uint32_t* hc_koff,
+                          uint32_t* hc_kids, uint32_t* hc_cid, double* hc_cost, uint32_t* uf_parent, uint8_t* uf_rank);
+int esat_download_view(esat_batch* b, uint32_t* C, uint32_t* root_pos, uint32_t* cls_id, uint32_t* cls_off,
+                       uint32_t* nd_sym, uint32_t* nd_koff, uint32_t* nd_kpos, double* nd_cost, uint32_t* nd_hc);
+/* match results of the i-th pattern (ematch) or rule (join) of the LAST call: per-leaf
+ * counts[L] and word offsets[L+1] (into words); words may be NULL to query sizes. */
+int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t* counts, uint64_t* word_off,
+                          uint32_t* words, uint64_t words_cap);
+int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, double* root_cost,
+                          double* class_cost, uint32_t* choice, uint8_t* reachable, uint32_t* passes);
+
+/* device pointers of per-leaf summary results (for fused collectives over NCCL) */
+int esat_result_device_ptrs(esat_batch* b, void** root_cost, void** status);
+
+/* timing of the last compute call on the context stream, in milliseconds (CUDA events) */
+float esat_last_kernel_ms(const esat_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESAT_B200_H */

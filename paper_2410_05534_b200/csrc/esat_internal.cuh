@@ -1,0 +1,140 @@
+// Internal device-side definitions shared by the esat_b200 kernels (sm_100a only).
+//
+// Layout: one *batch* = L leaf e-graphs concatenated (paper_2410_05534_b200/arena.py).
+// Leaf l owns node-indexed rows [nb[l], nb[l+1]), kid rows [kb[l], kb[l+1]), id rows
+// [ub[l], ub[l+1]); CSR offset arrays store n+1 leaf-relative entries at nb[l] + l.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef __CUDACC__
+#error "CUDA only"
+#endif
+
+namespace esat {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+
+// ---- batch view handed to every kernel (by value) ------------------------------
+struct Dev {
+    uint32_t L;
+    const uint64_t *nb, *kb, *ub, *tb;      // node / kid / id / hash-table bases [L+1]
+    // dirty hashcons input (egraph.py:138 insertion order) + union-find
+    const uint32_t *hc_sym, *hc_koff, *hc_kids, *hc_cid;
+    const double* hc_cost;
+    uint32_t* uf_parent;
+    uint8_t* uf_rank;
+    const uint32_t* root;
+    // rebuild output: compacted hashcons
+    uint32_t *o_n, *o_merges, *o_sym, *o_koff, *o_kids, *o_cid;
+    double* o_cost;
+    // clean view (input of ematch / extraction)
+    uint32_t *v_C, *v_root, *cls_id, *cls_off, *nd_sym, *nd_koff, *nd_kpos, *nd_hc;
+    double* nd_cost;
+    // rebuild scratch
+    uint32_t *s_ksym, *s_kkids, *s_cval, *s_val, *s_first, *s_perm;   // node/kid rows
+    uint8_t* s_flag;
+    uint32_t *s_sym2, *s_koff2, *s_kids2, *s_cid2;                   // second-pass input copy
+    double* s_cost2;
+    uint32_t *s_cnt, *s_pos, *s_coff;                                // id rows
+    uint32_t *s_tc, *s_ts;                                           // hash tables (tb rows)
+    // symbol table
+    const uint32_t *sym_name, *sym_arity, *sym_rank, *sym_poff;
+    const int32_t* sym_par;
+    uint32_t n_syms;
+};
+
+// ---- extraction launch arguments (k_extract.cu) ---------------------------------
+struct XArgs {
+    int method;                 // 0 default, 1 OCF
+    uint32_t *status, *err_class, *passes;
+    double *root_cost, *class_cost, *prev;
+    uint32_t *choice, *level, *order, *lvcnt, *stk, *stki;
+    uint8_t *reach;
+    // OCF history pool: per leaf [pool_base[l], pool_base[l+1]) entries per parity
+    const uint64_t* pool_base;
+    uint32_t *pool_key;          // 2 parities x entries
+    double* pool_val;
+    uint64_t pool_stride;        // offset of parity 1
+    uint32_t *hoff, *hlen;       // [2][node rows] history slot per class position
+    uint64_t slot_stride;
+};
+
+enum : uint32_t { X_OK = 0, X_NOT_CONVERGED = 1, X_INFEASIBLE = 2, X_CYCLIC = 3, X_CHILD_NOT_CHOSEN = 4,
+                  X_ROOT_NOT_CHOSEN = 5, X_NO_ROOT = 6, X_CAPACITY = 7 };
+
+// ---- small helpers ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Path-compressing find. Only called while no union is in flight (unions are issued by
+// one thread between barriers), so concurrent compressions all write the same root.
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
+    uint32_t r = x;
+    uint32_t p = parent[r];
+    while (p != r) { r = p; p = parent[r]; }
+    while (true) {
+        uint32_t nx = parent[x];
+        if (nx == r) break;
+        parent[x] = r;
+        x = nx;
+    }
+    return r;
+}
+
+// Rank union with ties to the lower id (egraph.py:103-115). Single-thread only.
+__device__ __forceinline__ uint32_t uf_union(uint32_t* parent, uint8_t* rank, uint32_t a, uint32_t b) {
+    uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+    if (ra == rb) return ra;
+    if (rank[ra] < rank[rb]) { uint32_t t = ra; ra = rb; rb = t; }
+    else if (rank[ra] == rank[rb]) {
+        if (rb < ra) { uint32_t t = ra; ra = rb; rb = t; }
+        rank[ra] = (uint8_t)(rank[ra] + 1);
+    }
+    parent[rb] = ra;
+    return ra;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t h) {
+    h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull; h ^= h >> 33;
+    return h;
+}
+
+__device__ __forceinline__ uint32_t key_hash(uint32_t sym, const uint32_t* k, uint32_t a) {
+    uint64_t h = mix64(0x9E3779B97F4A7C15ull + sym);
+    for (uint32_t i = 0; i < a; i++) h = mix64(h ^ (k[i] + 0x632BE59BD9B4E019ull));
+    return (uint32_t)(h ^ (h >> 32) ^ a);
+}
+
+// CTA-wide exclusive scan of per-thread values (blockDim.x <= 1024). Returns this thread's
+// exclusive prefix; *total receives the CTA sum. Uses `smem` (>= 33 words).
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* smem, uint32_t* total) {
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) smem[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < nw ? smem[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= (uint32_t)o) w += y;
+        }
+        smem[lane] = w;   // inclusive per-warp prefix
+    }
+    __syncthreads();
+    uint32_t warp_base = wid ? smem[wid - 1] : 0u;
+    *total = smem[nw - 1];
+    __syncthreads();
+    return warp_base + x - v;
+}
+
+// Python max(a, b): returns a unless b > a (extraction.py:214, 217).
+__device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
+
+}  // namespace esat

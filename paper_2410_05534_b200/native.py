@@ -1,0 +1,261 @@
+"""ctypes binding of libesat_b200.so (include/esat_b200.h) -- the only compute path.
+
+There is no CPU fallback: if the library or a CUDA device is missing, every entry
+point raises ``NativeUnavailable``. ``DeviceBatch`` owns one device-resident batch
+of leaf e-graphs and exposes the C-ABI stages with numpy host buffers.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_DIR = Path(__file__).resolve().parent / "_lib"
+LIB_PATH = LIB_DIR / "libesat_b200.so"
+NONE = 0xFFFFFFFF
+
+OK, E_ARG, E_CUDA, E_CAPACITY, E_STATE = 0, 1, 2, 3, 4
+X_OK, X_NOT_CONVERGED, X_INFEASIBLE, X_CYCLIC, X_CHILD_NOT_CHOSEN, X_ROOT_NOT_CHOSEN, X_NO_ROOT, X_CAPACITY = range(8)
+METHODS = {"default": 0, "default_greedy": 0, "ocf": 1, "ocf_greedy": 1}
+MATCH_LIST, MATCH_EXISTS = 0, 1
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library (or a B200) is not available; there is deliberately no fallback."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"esat_b200 error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def build() -> Path:
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", str(Path(__file__).resolve().parent / "csrc")], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise NativeUnavailable(f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(str(LIB_PATH))
+        vp = C.c_void_p
+        L.esat_last_error.restype = C.c_char_p
+        L.esat_last_error.argtypes = [vp]
+        L.esat_last_kernel_ms.restype = C.c_float
+        L.esat_last_kernel_ms.argtypes = [vp]
+        for name in ("esat_ctx_create", "esat_ctx_destroy", "esat_ctx_sync", "esat_symtab_upload",
+                     "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
+                     "esat_rebuild", "esat_ematch", "esat_join", "esat_extract", "esat_batch_set_pool",
+                     "esat_download_rebuild", "esat_download_view", "esat_download_matches",
+                     "esat_download_extract", "esat_result_device_ptrs"):
+            getattr(L, name).restype = C.c_int
+        L.esat_batch_set_pool.argtypes = [vp, C.c_double]
+        _lib = L
+    return _lib
+
+
+EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_sync", "esat_symtab_upload",
+            "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
+            "esat_rebuild", "esat_ematch", "esat_join", "esat_batch_set_pool", "esat_extract",
+            "esat_download_rebuild", "esat_download_view", "esat_download_matches", "esat_download_extract",
+            "esat_result_device_ptrs", "esat_last_kernel_ms")
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, np.uint32)
+
+
+class Context:
+    """One CUDA context/stream per GPU per process (esat_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        self.h = C.c_void_p()
+        rc = self.L.esat_ctx_create(C.c_int(device), C.byref(self.h))
+        if rc != OK:
+            raise NativeUnavailable(f"esat_ctx_create(device={device}) failed with code {rc}: no usable B200")
+        self.device = device
+        self.symtab_version = None
+
+    def check(self, rc: int):
+        if rc != OK:
+            raise NativeError(rc, self.L.esat_last_error(self.h).decode())
+
+    def close(self):
+        if self.h:
+            self.L.esat_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    __del__ = close
+
+    def sync(self):
+        self.check(self.L.esat_ctx_sync(self.h))
+
+    def last_ms(self) -> float:
+        return float(self.L.esat_last_kernel_ms(self.h))
+
+    def upload_symtab(self, arrays: dict):
+        n = len(arrays["name"])
+        keep = [_u32(arrays["name"]), _u32(arrays["arity"]), _u32(arrays["rank"]), _u32(arrays["poff"]),
+                np.ascontiguousarray(arrays["params"], np.int32)]
+        self.check(self.L.esat_symtab_upload(self.h, C.c_uint32(n), *[_p(a) for a in keep]))
+
+    def upload_patterns(self, programs: list):
+        words = np.concatenate([np.asarray(p, np.int32) for p in programs]) if programs else np.zeros(1, np.int32)
+        off = np.cumsum([0] + [len(p) for p in programs]).astype(np.uint32)
+        self.check(self.L.esat_patterns_upload(self.h, C.c_uint32(len(programs)), _p(off),
+                                               C.c_uint32(len(words)), _p(words)))
+
+
+class DeviceBatch:
+    """A device-resident batch of leaf e-graphs (esat_batch)."""
+
+    def __init__(self, ctx: Context, packed: dict):
+        self.ctx = ctx
+        self.L = ctx.L
+        self.packed = packed
+        self.n_leaves = packed["n_leaves"]
+        self.nb = np.ascontiguousarray(packed["node_base"], np.uint64)
+        self.kb = np.ascontiguousarray(packed["kid_base"], np.uint64)
+        self.ub = np.ascontiguousarray(packed["id_base"], np.uint64)
+        self.h = C.c_void_p()
+        ctx.check(self.L.esat_batch_create(ctx.h, C.c_uint32(self.n_leaves), _p(self.nb), _p(self.kb), _p(self.ub),
+                                           C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.L.esat_batch_destroy(self.h)
+            self.h = C.c_void_p()
+
+    __del__ = close
+
+    @property
+    def N(self):
+        return int(self.nb[-1])
+
+    @property
+    def K(self):
+        return int(self.kb[-1])
+
+    @property
+    def U(self):
+        return int(self.ub[-1])
+
+    def upload(self, packed: dict | None = None):
+        p = packed or self.packed
+        self._keep = [p["hc_sym"], p["hc_koff"], p["hc_kids"], p["hc_cid"], p["hc_cost"], p["uf_parent"],
+                      p["uf_rank"], p["root"]]
+        self.ctx.check(self.L.esat_batch_upload(self.h, *[_p(a) for a in self._keep]))
+
+    def rebuild(self):
+        self.ctx.check(self.L.esat_rebuild(self.h))
+
+    def set_pool(self, entries_per_node: float):
+        self.ctx.check(self.L.esat_batch_set_pool(self.h, C.c_double(entries_per_node)))
+
+    def extract(self, method: str):
+        self.ctx.check(self.L.esat_extract(self.h, C.c_int(METHODS[method])))
+
+    def ematch(self, pattern_ids, mode: int = MATCH_LIST):
+        ids = _u32(pattern_ids)
+        self.ctx.check(self.L.esat_ematch(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode)))
+
+    def join(self, specs: list):
+        """specs: per rule (source pattern ids, var maps per source, pvar maps per source, NV, NQ)."""
+        src_off, src, map_off, vmap, qmap, nv, nq = [0], [], [0], [], [], [], []
+        for ids, vmaps, qmaps, NV, NQ in specs:
+            src.extend(ids)
+            src_off.append(len(src))
+            # per source: var map then pvar map, offsets per source
+            for vm, qm in zip(vmaps, qmaps):
+                vmap.extend(vm)
+                qmap.extend(qm)
+            nv.append(NV)
+            nq.append(NQ)
+        # map offsets are per source (var_map and pvar_map each indexed by their own offsets)
+        vo, qo = [0], [0]
+        for ids, vmaps, qmaps, *_ in specs:
+            for vm, qm in zip(vmaps, qmaps):
+                vo.append(vo[-1] + len(vm))
+                qo.append(qo[-1] + len(qm))
+        arrs = [_u32(src_off), _u32(src), _u32(np.stack([vo, qo], 1).reshape(-1)), _u32(vmap or [0]),
+                _u32(qmap or [0]), _u32(nv), _u32(nq)]
+        self._keep_join = arrs
+        self.ctx.check(self.L.esat_join(self.h, C.c_uint32(len(specs)), *[_p(a) for a in arrs]))
+
+    # ---- downloads ---------------------------------------------------------------
+    def download_rebuild(self) -> dict:
+        L, N, K, U = self.n_leaves, self.N, self.K, self.U
+        o = {"n": np.zeros(L, np.uint32), "merges": np.zeros(L, np.uint32), "hc_sym": np.zeros(N, np.uint32),
+             "hc_koff": np.zeros(N + L, np.uint32), "hc_kids": np.zeros(K, np.uint32),
+             "hc_cid": np.zeros(N, np.uint32), "hc_cost": np.zeros(N, np.float64),
+             "uf_parent": np.zeros(U, np.uint32), "uf_rank": np.zeros(U, np.uint8)}
+        self.ctx.check(self.L.esat_download_rebuild(self.h, *[_p(o[k]) for k in (
+            "n", "merges", "hc_sym", "hc_koff", "hc_kids", "hc_cid", "hc_cost", "uf_parent", "uf_rank")]))
+        return o
+
+    def download_view(self) -> dict:
+        L, N, K = self.n_leaves, self.N, self.K
+        o = {"C": np.zeros(L, np.uint32), "root_pos": np.zeros(L, np.uint32), "cls_id": np.zeros(N, np.uint32),
+             "cls_off": np.zeros(N + L, np.uint32), "nd_sym": np.zeros(N, np.uint32),
+             "nd_koff": np.zeros(N + L, np.uint32), "nd_kpos": np.zeros(K, np.uint32),
+             "nd_cost": np.zeros(N, np.float64), "nd_hc": np.zeros(N, np.uint32)}
+        self.ctx.check(self.L.esat_download_view(self.h, *[_p(o[k]) for k in (
+            "C", "root_pos", "cls_id", "cls_off", "nd_sym", "nd_koff", "nd_kpos", "nd_cost", "nd_hc")]))
+        return o
+
+    def download_extract(self) -> dict:
+        L, N = self.n_leaves, self.N
+        o = {"status": np.zeros(L, np.uint32), "err_class": np.zeros(L, np.uint32),
+             "root_cost": np.zeros(L, np.float64), "class_cost": np.zeros(N, np.float64),
+             "choice": np.zeros(N, np.uint32), "reachable": np.zeros(N, np.uint8), "passes": np.zeros(L, np.uint32)}
+        self.ctx.check(self.L.esat_download_extract(self.h, *[_p(o[k]) for k in (
+            "status", "err_class", "root_cost", "class_cost", "choice", "reachable", "passes")]))
+        return o
+
+    def download_matches(self, index: int, from_join: bool = False):
+        L = self.n_leaves
+        cnt = np.zeros(L, np.uint32)
+        off = np.zeros(L + 1, np.uint64)
+        self.ctx.check(self.L.esat_download_matches(self.h, C.c_int(int(from_join)), C.c_uint32(index), _p(cnt),
+                                                    _p(off), None, C.c_uint64(0)))
+        words = np.zeros(max(int(off[-1]), 1), np.uint32)
+        self.ctx.check(self.L.esat_download_matches(self.h, C.c_int(int(from_join)), C.c_uint32(index), _p(cnt),
+                                                    _p(off), _p(words), C.c_uint64(len(words))))
+        return words, off, cnt
+
+
+def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max_factor: float = 4096.0) -> dict:
+    """Run extraction, growing the OCF history pool on ESAT_X_CAPACITY (host regrow path)."""
+    while True:
+        batch.extract(method)
+        out = batch.download_extract()
+        if method.startswith("ocf") and np.any(out["status"] == X_CAPACITY) and factor < max_factor:
+            factor *= 4
+            batch.set_pool(factor)
+            continue
+        return out
+
+
+def available() -> bool:
+    try:
+        lib()
+        Context(int(os.environ.get("ESAT_DEVICE", "0"))).close()
+        return True
+    except (NativeUnavailable, OSError):
+        return False
