@@ -11,6 +11,7 @@ namespace esat {
 template <int T> __global__ void k_rebuild(Dev);
 template <int T> __global__ void k_extract(Dev, XArgs);
 }  // namespace esat
+#include "k_ematch_args.cuh"
 
 using namespace esat;
 
@@ -76,6 +77,16 @@ struct esat_batch {
     uint64_t* d_pb = nullptr;
     uint32_t* pool_key = nullptr;
     double* pool_val = nullptr;
+    // e-matching results of the last esat_ematch / esat_join call
+    uint32_t m_P = 0, j_R = 0;
+    std::vector<uint32_t> m_W, j_W;
+    uint32_t *d_pat_ids = nullptr, *d_m_count = nullptr, *d_m_W = nullptr, *d_j_count = nullptr;
+    uint64_t *d_m_off = nullptr, *d_j_off = nullptr;
+    uint32_t *stage = nullptr, *m_out = nullptr, *j_out = nullptr, *d_over = nullptr;
+    uint64_t stage_cap = 0, m_cap = 0, j_cap = 0;
+    unsigned long long* d_tops = nullptr;   // [0] stage, [1] ematch out, [2] join stage, [3] join out
+    uint32_t* d_jspec = nullptr;
+    uint64_t jspec_cap = 0;
 };
 
 namespace {
@@ -244,6 +255,9 @@ int esat_batch_destroy(esat_batch* b) {
     cudaSetDevice(b->ctx->device);
     for (void* p : b->owned) cudaFree(p);
     cudaFree(b->d_pb); cudaFree(b->pool_key); cudaFree(b->pool_val);
+    cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
+    cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
+    cudaFree(b->d_over); cudaFree(b->d_tops); cudaFree(b->d_jspec);
     delete b;
     return ESAT_OK;
 }
@@ -400,17 +414,180 @@ int esat_result_device_ptrs(esat_batch* b, void** root_cost, void** status) {
 
 }  // extern "C"
 
-// ---- e-matching entry points: implemented in k_ematch.cu (weak stubs until linked) ----
+
+// ---- e-matching (k_ematch.cu) ---------------------------------------------------------
+namespace {
+
+template <typename T>
+int regrow(esat_ctx* c, T** p, uint64_t* cap, uint64_t need) {
+    if (*cap >= need && *p) return ESAT_OK;
+    uint64_t n = need + need / 4 + 1024;
+    cudaFree(*p);
+    *p = nullptr;
+    CK(c, cudaMalloc((void**)p, sizeof(T) * n));
+    *cap = n;
+    return ESAT_OK;
+}
+
+int ensure_match_meta(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    if (!b->d_tops) CK(c, cudaMalloc((void**)&b->d_tops, 8 * sizeof(unsigned long long)));
+    if (!b->d_over) CK(c, cudaMalloc((void**)&b->d_over, 2 * sizeof(uint32_t)));
+    return ESAT_OK;
+}
+
+}  // namespace
+
 extern "C" {
-__attribute__((weak)) int esat_ematch(esat_batch* b, uint32_t, const uint32_t*, int) {
-    return b ? fail(b->ctx, ESAT_E_STATE, "esat_ematch not built") : ESAT_E_ARG;
+
+int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
+    if (!b || (P && !pat_ids) || (mode != ESAT_MATCH_LIST && mode != ESAT_MATCH_EXISTS)) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "ematch requires a rebuilt e-graph");
+    for (uint32_t i = 0; i < P; i++)
+        if (pat_ids[i] >= c->n_pat) return fail(c, ESAT_E_ARG, "pattern id %u out of range", pat_ids[i]);
+    cudaSetDevice(c->device);
+    const uint64_t L = b->L;
+    int r;
+    if ((r = ensure_match_meta(b))) return r;
+    cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_off); cudaFree(b->d_m_W);
+    b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
+    CK(c, cudaMalloc((void**)&b->d_pat_ids, 4ull * (P ? P : 1)));
+    CK(c, cudaMalloc((void**)&b->d_m_count, 4ull * (P * L ? P * L : 1)));
+    CK(c, cudaMalloc((void**)&b->d_m_off, 8ull * (P * L ? P * L : 1)));
+    CK(c, cudaMalloc((void**)&b->d_m_W, 4ull * (P ? P : 1)));
+    b->m_W.resize(P);
+    for (uint32_t i = 0; i < P; i++) {
+        const int32_t* pg = c->pat_words.data() + c->pat_off[pat_ids[i]];
+        b->m_W[i] = 1 + pg[1] + pg[2];
+        if (pg[0] > MAX_PN || pg[1] > MAX_V || pg[2] > MAX_V || (int)b->m_W[i] > MAX_W)
+            return fail(c, ESAT_E_ARG, "pattern %u exceeds device limits", pat_ids[i]);
+    }
+    CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
+    b->m_P = P;
+    if (!b->stage_cap) {
+        if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
+        if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
+    }
+    for (int attempt = 0; attempt < 4; attempt++) {
+        CK(c, cudaMemsetAsync(b->d_tops, 0, 8 * sizeof(unsigned long long), c->stream));
+        CK(c, cudaMemsetAsync(b->d_over, 0, 2 * sizeof(uint32_t), c->stream));
+        MArgs a{};
+        a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = mode;
+        a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops;
+        a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
+        Dev d = b->d;
+        d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
+        d.sym_par = c->sym_par; d.n_syms = c->n_syms;
+        tic(c);
+        if (L && P) k_ematch<128><<<dim3((unsigned)L, P), 128, 0, c->stream>>>(d, a);
+        toc(c);
+        if ((r = launch_check(c, "k_ematch"))) return r;
+        if (mode == ESAT_MATCH_EXISTS) return ESAT_OK;
+        uint32_t over = 0;
+        unsigned long long tops[2];
+        CK(c, cudaMemcpyAsync(&over, b->d_over, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(tops, b->d_tops, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (!over) return ESAT_OK;
+        if ((r = regrow(c, &b->stage, &b->stage_cap, tops[0]))) return r;
+        if ((r = regrow(c, &b->m_out, &b->m_cap, tops[1] > tops[0] ? tops[1] : tops[0]))) return r;
+    }
+    return fail(c, ESAT_E_CAPACITY, "ematch output did not fit after regrowing");
 }
-__attribute__((weak)) int esat_join(esat_batch* b, uint32_t, const uint32_t*, const uint32_t*, const uint32_t*,
-                                    const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*) {
-    return b ? fail(b->ctx, ESAT_E_STATE, "esat_join not built") : ESAT_E_ARG;
+
+int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t* src, const uint32_t* map_off,
+              const uint32_t* vmap, const uint32_t* qmap, const uint32_t* nv, const uint32_t* nq) {
+    if (!b || (R && (!src_off || !src || !map_off || !nv || !nq))) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->m_P) return fail(c, ESAT_E_STATE, "esat_join needs the source matches of a LIST esat_ematch call");
+    cudaSetDevice(c->device);
+    const uint64_t L = b->L;
+    const uint32_t nsrc = src_off[R];
+    b->j_W.resize(R);
+    for (uint32_t r = 0; r < R; r++) {
+        const uint32_t S = src_off[r + 1] - src_off[r];
+        if (S < 1 || S > MAX_S) return fail(c, ESAT_E_ARG, "rule %u: %u sources (max %d)", r, S, MAX_S);
+        for (uint32_t s = src_off[r]; s < src_off[r + 1]; s++)
+            if (src[s] >= b->m_P) return fail(c, ESAT_E_ARG, "join source %u not in the last ematch call", src[s]);
+        b->j_W[r] = S + nv[r] + nq[r];
+        if (b->j_W[r] > (uint32_t)MAX_W || nv[r] > 64 || nq[r] > 64) return fail(c, ESAT_E_ARG, "rule %u too wide", r);
+    }
+    const uint32_t nmap_v = map_off[2 * nsrc], nmap_q = map_off[2 * nsrc + 1];
+    // spec words: src_off[R+1] src[nsrc] map_off[2*(nsrc+1)] vmap[nmap_v] qmap[nmap_q] nv[R] nq[R]
+    const uint64_t words = (R + 1) + nsrc + 2ull * (nsrc + 1) + nmap_v + nmap_q + 2ull * R;
+    int r_;
+    if ((r_ = regrow(c, &b->d_jspec, &b->jspec_cap, words))) return r_;
+    std::vector<uint32_t> spec;
+    spec.reserve(words);
+    spec.insert(spec.end(), src_off, src_off + R + 1);
+    spec.insert(spec.end(), src, src + nsrc);
+    spec.insert(spec.end(), map_off, map_off + 2 * (nsrc + 1));
+    spec.insert(spec.end(), vmap, vmap + nmap_v);
+    spec.insert(spec.end(), qmap, qmap + nmap_q);
+    spec.insert(spec.end(), nv, nv + R);
+    spec.insert(spec.end(), nq, nq + R);
+    CK(c, cudaMemcpyAsync(b->d_jspec, spec.data(), 4 * spec.size(), cudaMemcpyHostToDevice, c->stream));
+    cudaFree(b->d_j_count); cudaFree(b->d_j_off);
+    b->d_j_count = nullptr; b->d_j_off = nullptr;
+    CK(c, cudaMalloc((void**)&b->d_j_count, 4ull * (R * L ? R * L : 1)));
+    CK(c, cudaMalloc((void**)&b->d_j_off, 8ull * (R * L ? R * L : 1)));
+    b->j_R = R;
+    if (!b->j_cap && (r_ = regrow(c, &b->j_out, &b->j_cap, 4 * b->N + 4096))) return r_;
+    const uint32_t* p = b->d_jspec;
+    for (int attempt = 0; attempt < 4; attempt++) {
+        CK(c, cudaMemsetAsync(b->d_tops + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+        CK(c, cudaMemsetAsync(b->d_over + 1, 0, sizeof(uint32_t), c->stream));
+        JArgs a{};
+        a.R = R;
+        a.src_off = p; a.src = p + (R + 1); a.map_off = a.src + nsrc; a.vmap = a.map_off + 2 * (nsrc + 1);
+        a.qmap = a.vmap + nmap_v; a.nv = a.qmap + nmap_q; a.nq = a.nv + R;
+        a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
+        a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
+        a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
+        tic(c);
+        if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 0, c->stream>>>((uint32_t)L, a);
+        toc(c);
+        if ((r_ = launch_check(c, "k_join"))) return r_;
+        uint32_t over = 0;
+        unsigned long long tops[2];
+        CK(c, cudaMemcpyAsync(&over, b->d_over + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (!over) return ESAT_OK;
+        if ((r_ = regrow(c, &b->j_out, &b->j_cap, tops[1]))) return r_;
+    }
+    return fail(c, ESAT_E_CAPACITY, "join output did not fit after regrowing");
 }
-__attribute__((weak)) int esat_download_matches(esat_batch* b, int, uint32_t, uint32_t*, uint64_t*, uint32_t*,
-                                                uint64_t) {
-    return b ? fail(b->ctx, ESAT_E_STATE, "esat_download_matches not built") : ESAT_E_ARG;
+
+int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t* counts, uint64_t* word_off,
+                          uint32_t* words, uint64_t words_cap) {
+    if (!b || !counts || !word_off) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    const uint32_t n = from_join ? b->j_R : b->m_P;
+    if (index >= n) return fail(c, ESAT_E_ARG, "match index %u out of range (%u)", index, n);
+    cudaSetDevice(c->device);
+    const uint64_t L = b->L;
+    const uint32_t W = from_join ? b->j_W[index] : b->m_W[index];
+    std::vector<uint64_t> off(L);
+    CK(c, cudaMemcpyAsync(counts, (from_join ? b->d_j_count : b->d_m_count) + index * L, 4 * L,
+                          cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(off.data(), (from_join ? b->d_j_off : b->d_m_off) + index * L, 8 * L,
+                          cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    uint64_t acc = 0;
+    for (uint64_t l = 0; l < L; l++) { word_off[l] = acc; acc += (uint64_t)counts[l] * W; }
+    word_off[L] = acc;
+    if (!words) return ESAT_OK;
+    if (words_cap < acc) return fail(c, ESAT_E_CAPACITY, "need %llu words", (unsigned long long)acc);
+    const uint32_t* src = from_join ? b->j_out : b->m_out;
+    for (uint64_t l = 0; l < L; l++)
+        if (counts[l])
+            CK(c, cudaMemcpyAsync(words + word_off[l], src + off[l], 4ull * counts[l] * W, cudaMemcpyDeviceToHost,
+                                  c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return ESAT_OK;
 }
-}
+
+}  // extern "C"

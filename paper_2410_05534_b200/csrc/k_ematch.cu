@@ -1,0 +1,383 @@
+// K1-K3: batched e-matching (rewrite.py:353-433) and multi-pattern joins.
+//
+// k_ematch: one CTA per (leaf, pattern). Root classes are split into contiguous per-thread
+// chunks so that concatenating thread outputs keeps the reference's order (matches sort
+// by root first, rewrite.py:396-397). Each thread runs the backtracking matcher of
+// _match_in_class (rewrite.py:371-393) iteratively over the pattern's pre-order: an App
+// node scans the e-nodes of its class in node_sort_key order with the name/arity/attribute
+// test of _match_param_spec (353-368); a Var binds on first sight and checks equality after.
+// Pass 1 counts, a block scan places every thread's raw records in a staging area, pass 2
+// writes them, sorts + dedups each root class's slice (rewrite.py:420-433), and a second scan
+// compacts the unique records into the output pool. EXISTS mode (is_rule_applicable,
+// rewrite.py:579-589) stops at the first match.
+//
+// k_join: one CTA per (leaf, multi-pattern rule). joint_match threads bindings from source to
+// source (rewrite.py:410-419); on device the sources are matched independently (k_ematch) and
+// joined on equal shared var/pvar bindings -- the same set. Threads own
+// whole groups of source-0 records with equal root; for each combination of root groups of
+// the other sources the consistent products form one block with a fixed roots prefix, which is
+// sorted locally, so blocks come out in (roots, vars, pvars) = _subst_key order.
+#include "k_ematch_args.cuh"
+
+namespace esat {
+
+namespace {
+
+struct Matcher {
+    const int32_t* prog;        // shared-memory copy
+    int P, V, Q;
+    // leaf view
+    const uint32_t *cls_id, *cls_off, *nd_sym, *nd_koff, *nd_kpos;
+    const uint32_t *s_name, *s_arity, *s_poff;
+    const int32_t* s_par;
+};
+
+__device__ __forceinline__ const int32_t* rec(const Matcher& m, int i) { return m.prog + 3 + 6 * i; }
+
+// Enumerate all matches rooted at class position r; emit(rec_words) per raw match.
+// Returns the number of raw matches (stops after the first when `first_only`).
+template <typename Emit>
+__device__ uint32_t match_class(const Matcher& m, uint32_t r, bool first_only, Emit emit) {
+    uint32_t cls[MAX_PN], choice[MAX_PN], pmask[MAX_PN];
+    uint32_t vars[MAX_V];
+    int32_t pv[MAX_V];
+    uint32_t pset = 0, vbound_here = 0;
+    for (int v = 0; v < m.V; v++) vars[v] = NONE;
+    uint32_t n = 0;
+    cls[0] = r;
+    int i = 0;
+    bool entering = true;
+    while (i >= 0) {
+        if (i == m.P) {
+            n++;
+            emit(m.cls_id[r], vars, pv);
+            if (first_only) return n;
+            i--;
+            entering = false;
+            continue;
+        }
+        const int32_t* pr = rec(m, i);
+        if (pr[0] == 0) {  // Var
+            const int v = pr[1];
+            if (entering) {
+                const uint32_t cid = m.cls_id[cls[i]];
+                if (vars[v] == NONE) { vars[v] = cid; vbound_here |= 1u << i; i++; continue; }
+                if (vars[v] == cid) { vbound_here &= ~(1u << i); i++; continue; }
+                i--;
+                entering = false;
+                continue;
+            }
+            if (vbound_here >> i & 1u) { vars[v] = NONE; vbound_here &= ~(1u << i); }
+            i--;
+            continue;
+        }
+        // App
+        const int32_t name = pr[1], arity = pr[2], nslots = pr[3];
+        const int32_t* slots = m.prog + pr[4];
+        const int32_t* kids = m.prog + pr[5];
+        const uint32_t lo = m.cls_off[cls[i]], hi = m.cls_off[cls[i] + 1];
+        uint32_t nd;
+        if (entering) { nd = lo; pmask[i] = 0; }
+        else {
+            pset &= ~pmask[i];   // undo attribute bindings made at this node
+            pmask[i] = 0;
+            nd = choice[i] + 1;
+        }
+        bool found = false;
+        for (; nd < hi; nd++) {
+            const uint32_t s = m.nd_sym[nd];
+            if ((int32_t)m.s_name[s] != name || (int32_t)m.s_arity[s] != arity) continue;
+            if (nslots >= 0) {
+                const uint32_t p0 = m.s_poff[s];
+                if ((int32_t)(m.s_poff[s + 1] - p0) != nslots) continue;
+                uint32_t newly = 0;
+                bool ok = true;
+                for (int j = 0; j < nslots && ok; j++) {
+                    const int32_t sl = slots[j], av = m.s_par[p0 + j];
+                    if (sl >= 0) ok = (sl == av);
+                    else {
+                        const int q = -sl - 1;
+                        if (!((pset | newly) >> q & 1u)) { pv[q] = av; newly |= 1u << q; }
+                        else ok = (pv[q] == av);
+                    }
+                }
+                if (!ok) continue;
+                pset |= newly;
+                pmask[i] = newly;
+            }
+            found = true;
+            break;
+        }
+        if (!found) { i--; entering = false; continue; }
+        choice[i] = nd;
+        const uint32_t k0 = m.nd_koff[nd];
+        for (int j = 0; j < arity; j++) cls[kids[j]] = m.nd_kpos[k0 + j];
+        i++;
+        entering = true;
+    }
+    return n;
+}
+
+__device__ __forceinline__ int cmpw(const uint32_t* a, const uint32_t* b, uint32_t W) {
+    for (uint32_t i = 0; i < W; i++)
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    return 0;
+}
+
+// insertion sort + unique of n records of W words in place; returns unique count
+__device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
+    uint32_t tmp[MAX_W];
+    for (uint32_t i = 1; i < n; i++) {
+        for (uint32_t w = 0; w < W; w++) tmp[w] = base[i * W + w];
+        uint32_t j = i;
+        while (j > 0 && cmpw(base + (j - 1) * W, tmp, W) > 0) {
+            for (uint32_t w = 0; w < W; w++) base[j * W + w] = base[(j - 1) * W + w];
+            j--;
+        }
+        for (uint32_t w = 0; w < W; w++) base[j * W + w] = tmp[w];
+    }
+    if (n == 0) return 0;
+    uint32_t o = 1;
+    for (uint32_t i = 1; i < n; i++)
+        if (cmpw(base + (o - 1) * W, base + i * W, W) != 0) {
+            if (o != i)
+                for (uint32_t w = 0; w < W; w++) base[o * W + w] = base[i * W + w];
+            o++;
+        }
+    return o;
+}
+
+}  // namespace
+
+template <int T>
+__global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
+    const uint32_t l = blockIdx.x, pi = blockIdx.y, tid = threadIdx.x;
+    const uint32_t L = d.L;
+    __shared__ int32_t sprog[3 + 6 * MAX_PN + 4 * MAX_PN];
+    __shared__ uint32_t sh_scan[33];
+    __shared__ unsigned long long sh_base;
+    const uint32_t pid = a.pat_ids[pi];
+    const uint32_t po = a.prog_off[pid], pn = a.prog_off[pid + 1] - po;
+    for (uint32_t w = tid; w < pn; w += T) sprog[w] = a.prog[po + w];
+    __syncthreads();
+    Matcher m;
+    m.prog = sprog;
+    m.P = sprog[0]; m.V = sprog[1]; m.Q = sprog[2];
+    const uint64_t b = d.nb[l];
+    m.cls_id = d.cls_id + b;
+    m.cls_off = d.cls_off + b + l;
+    m.nd_sym = d.nd_sym + b;
+    m.nd_koff = d.nd_koff + b + l;
+    m.nd_kpos = d.nd_kpos + d.kb[l];
+    m.s_name = d.sym_name; m.s_arity = d.sym_arity; m.s_poff = d.sym_poff; m.s_par = d.sym_par;
+    const uint32_t W = 1 + m.V + m.Q;
+    const uint32_t C = d.v_C[l];
+    const uint32_t ch = (C + T - 1) / T;
+    const uint32_t c_lo = min(C, tid * ch), c_hi = min(C, c_lo + ch);
+    auto nothing = [](uint32_t, const uint32_t*, const int32_t*) {};
+
+    if (a.mode == 1) {  // existence only
+        uint32_t any = 0;
+        for (uint32_t r = c_lo; r < c_hi && !any; r++) any = match_class(m, r, true, nothing);
+        any = __syncthreads_or(any);
+        if (tid == 0) { a.count[(uint64_t)pi * L + l] = any ? 1u : 0u; a.off[(uint64_t)pi * L + l] = 0; }
+        return;
+    }
+    // pass 1: raw counts
+    uint32_t raw = 0;
+    for (uint32_t r = c_lo; r < c_hi; r++) raw += match_class(m, r, false, nothing);
+    uint32_t tot;
+    const uint32_t pre = block_exscan(raw, sh_scan, &tot);
+    if (tid == 0) {
+        unsigned long long base = atomicAdd(&a.tops[0], (unsigned long long)tot * W);
+        if (base + (unsigned long long)tot * W > a.stage_cap) { atomicOr(a.overflow, 1u); base = ~0ull; }
+        sh_base = base;
+    }
+    __syncthreads();
+    const unsigned long long sbase = sh_base;
+    uint32_t uniq = 0;
+    uint32_t* mine = a.stage + (sbase == ~0ull ? 0 : sbase) + (uint64_t)pre * W;
+    if (sbase != ~0ull) {
+        uint32_t cur = 0;
+        for (uint32_t r = c_lo; r < c_hi; r++) {
+            const uint32_t seg = cur;
+            match_class(m, r, false, [&](uint32_t root, const uint32_t* vars, const int32_t* pv) {
+                uint32_t* o = mine + (uint64_t)cur * W;
+                o[0] = root;
+                for (int v = 0; v < m.V; v++) o[1 + v] = vars[v];
+                for (int q = 0; q < m.Q; q++) o[1 + m.V + q] = (uint32_t)pv[q];
+                cur++;
+            });
+            cur = seg + sort_unique(mine + (uint64_t)seg * W, cur - seg, W);
+        }
+        uniq = cur;
+    }
+    const uint32_t upre = block_exscan(uniq, sh_scan, &tot);
+    if (tid == 0) {
+        unsigned long long base = ~0ull;
+        if (sbase != ~0ull) {
+            base = atomicAdd(&a.tops[1], (unsigned long long)tot * W);
+            if (base + (unsigned long long)tot * W > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+        }
+        sh_base = base;
+        a.count[(uint64_t)pi * L + l] = tot;
+        a.off[(uint64_t)pi * L + l] = base == ~0ull ? 0 : base;
+    }
+    __syncthreads();
+    if (sh_base != ~0ull)
+        for (uint64_t w = 0; w < (uint64_t)uniq * W; w++) a.out[sh_base + (uint64_t)upre * W + w] = mine[w];
+}
+
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct Src {
+    const uint32_t* w;   // records
+    uint32_t n, W, V, Q;
+    const uint32_t *vmap, *qmap;
+};
+
+// Combination of one record per source: consistency on shared vars/pvars; fills out[].
+__device__ __forceinline__ bool combine(const Src* src, int S, const uint32_t* idx, uint32_t NV, uint32_t NQ,
+                                        uint32_t* out) {
+    uint64_t vset = 0, qset = 0;
+    for (int s = 0; s < S; s++) {
+        const uint32_t* r = src[s].w + (uint64_t)idx[s] * src[s].W;
+        out[s] = r[0];
+        for (uint32_t v = 0; v < src[s].V; v++) {
+            const uint32_t o = src[s].vmap[v];
+            if (!(vset >> o & 1ull)) { vset |= 1ull << o; out[S + o] = r[1 + v]; }
+            else if (out[S + o] != r[1 + v]) return false;
+        }
+        for (uint32_t q = 0; q < src[s].Q; q++) {
+            const uint32_t o = src[s].qmap[q];
+            if (!(qset >> o & 1ull)) { qset |= 1ull << o; out[S + NV + o] = r[1 + src[s].V + q]; }
+            else if (out[S + NV + o] != r[1 + src[s].V + q]) return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ uint32_t group_end(const Src& s, uint32_t i) {
+    const uint32_t root = s.w[(uint64_t)i * s.W];
+    uint32_t j = i + 1;
+    while (j < s.n && s.w[(uint64_t)j * s.W] == root) j++;
+    return j;
+}
+
+__device__ __forceinline__ uint32_t group_start_at_or_after(const Src& s, uint32_t p) {
+    if (p == 0 || p >= s.n) return p >= s.n ? s.n : 0;
+    while (p < s.n && s.w[(uint64_t)p * s.W] == s.w[(uint64_t)(p - 1) * s.W]) p++;
+    return p;
+}
+
+// Visit every block (source-0 group g0 x root groups of sources 1..S-1); for each block call
+// f(block_first_idx[], block_end_idx[]).
+template <typename F>
+__device__ void for_blocks(const Src* src, int S, uint32_t g0_lo, uint32_t g0_hi, F f) {
+    uint32_t lo[MAX_S], hi[MAX_S];
+    lo[0] = g0_lo; hi[0] = g0_hi;
+    // odometer over groups of sources 1..S-1
+    for (int s = 1; s < S; s++) { lo[s] = 0; hi[s] = group_end(src[s], 0); }
+    for (;;) {
+        f(lo, hi);
+        int s = S - 1;
+        for (; s >= 1; s--) {
+            lo[s] = hi[s];
+            if (lo[s] < src[s].n) { hi[s] = group_end(src[s], lo[s]); break; }
+            lo[s] = 0;
+            hi[s] = group_end(src[s], 0);
+        }
+        if (s < 1) return;
+    }
+}
+
+template <typename Emit>
+__device__ uint32_t block_products(const Src* src, int S, const uint32_t* lo, const uint32_t* hi, uint32_t NV,
+                                   uint32_t NQ, Emit emit) {
+    uint32_t idx[MAX_S], rec_[MAX_W];
+    for (int s = 0; s < S; s++) idx[s] = lo[s];
+    uint32_t n = 0;
+    for (;;) {
+        if (combine(src, S, idx, NV, NQ, rec_)) { emit(rec_); n++; }
+        int s = S - 1;
+        for (; s >= 0; s--) {
+            if (++idx[s] < hi[s]) break;
+            idx[s] = lo[s];
+        }
+        if (s < 0) return n;
+    }
+}
+
+}  // namespace
+
+template <int T>
+__global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
+    const uint32_t l = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
+    __shared__ uint32_t sh_scan[33];
+    __shared__ unsigned long long sh_base;
+    const uint32_t s0 = a.src_off[r], S = a.src_off[r + 1] - s0;
+    const uint32_t NV = a.nv[r], NQ = a.nq[r], W = S + NV + NQ;
+    Src src[MAX_S];
+    bool empty = false;
+    for (uint32_t s = 0; s < S; s++) {
+        const uint32_t p = a.src[s0 + s];
+        const uint64_t mi = (uint64_t)p * L + l;
+        src[s].n = a.m_count[mi];
+        src[s].w = a.m_words + a.m_off[mi];
+        src[s].W = a.m_W[p];
+        const uint32_t vo = a.map_off[2 * (s0 + s)], qo = a.map_off[2 * (s0 + s) + 1];
+        src[s].V = a.map_off[2 * (s0 + s + 1)] - vo;
+        src[s].Q = a.map_off[2 * (s0 + s + 1) + 1] - qo;
+        src[s].vmap = a.vmap + vo;
+        src[s].qmap = a.qmap + qo;
+        if (!src[s].n) empty = true;
+    }
+    // threads own whole root groups of source 0
+    uint32_t g_lo = 0, g_hi = 0;
+    if (!empty) {
+        const uint32_t n0 = src[0].n, ch = (n0 + T - 1) / T;
+        g_lo = group_start_at_or_after(src[0], min(n0, tid * ch));
+        g_hi = group_start_at_or_after(src[0], min(n0, (tid + 1) * ch));
+    }
+    auto count_only = [](const uint32_t*) {};
+    uint32_t cnt = 0;
+    for (uint32_t g = g_lo; g < g_hi;) {
+        const uint32_t ge = group_end(src[0], g);
+        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+            cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
+        });
+        g = ge;
+    }
+    uint32_t tot;
+    const uint32_t pre = block_exscan(cnt, sh_scan, &tot);
+    if (tid == 0) {
+        unsigned long long base = atomicAdd(&a.tops[1], (unsigned long long)tot * W);
+        if (base + (unsigned long long)tot * W > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+        sh_base = base;
+        a.count[(uint64_t)r * L + l] = tot;
+        a.off[(uint64_t)r * L + l] = base == ~0ull ? 0 : base;
+    }
+    __syncthreads();
+    if (sh_base == ~0ull) return;
+    uint32_t* out = a.out + sh_base + (uint64_t)pre * W;
+    uint32_t cur = 0;
+    for (uint32_t g = g_lo; g < g_hi;) {
+        const uint32_t ge = group_end(src[0], g);
+        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+            const uint32_t start = cur;
+            block_products(src, S, lo, hi, NV, NQ, [&](const uint32_t* rr) {
+                for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
+                cur++;
+            });
+            // products of one block share the roots prefix; distinct pairs give distinct keys
+            sort_unique(out + (uint64_t)start * W, cur - start, W);
+        });
+        g = ge;
+    }
+}
+
+template __global__ void k_ematch<128>(Dev, MArgs);
+template __global__ void k_join<128>(uint32_t, JArgs);
+
+}  // namespace esat

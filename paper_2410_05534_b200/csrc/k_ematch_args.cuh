@@ -1,0 +1,49 @@
+// Launch arguments of k_ematch / k_join (k_ematch.cu), shared with esat_api.cu.
+#pragma once
+#include "esat_internal.cuh"
+
+namespace esat {
+
+constexpr int MAX_PN = 32;   // pattern nodes
+constexpr int MAX_V = 16;    // vars / pvars per pattern
+constexpr int MAX_W = 40;    // words per record
+constexpr int MAX_S = 4;     // sources per multi-pattern rule
+
+struct MArgs {
+    const int32_t* prog;        // all pattern programs
+    const uint32_t* prog_off;   // [n_patterns_total + 1]
+    const uint32_t* pat_ids;    // patterns of this call [P]
+    uint32_t P;
+    int mode;                   // 0 list, 1 exists
+    uint32_t* stage;
+    uint64_t stage_cap;
+    unsigned long long* tops;   // [0] stage top, [1] out top (words)
+    uint32_t* out;
+    uint64_t out_cap;
+    uint32_t* count;            // [P][L]
+    uint64_t* off;              // [P][L] word offsets into out
+    uint32_t* overflow;
+};
+
+struct JArgs {
+    uint32_t R;
+    const uint32_t *src_off, *src, *map_off, *vmap, *qmap, *nv, *nq;
+    // single-pattern inputs (from the last k_ematch call)
+    const uint32_t* m_count;
+    const uint64_t* m_off;
+    const uint32_t* m_words;
+    const uint32_t* m_W;        // words per record of call-pattern p
+    uint32_t* stage;
+    uint64_t stage_cap;
+    unsigned long long* tops;
+    uint32_t* out;
+    uint64_t out_cap;
+    uint32_t* count;            // [R][L]
+    uint64_t* off;
+    uint32_t* overflow;
+};
+
+template <int T> __global__ void k_ematch(Dev, MArgs);
+template <int T> __global__ void k_join(uint32_t, JArgs);
+
+}  // namespace esat
