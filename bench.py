@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: MCTS leaf pipeline (rebuild -> all-rule e-match -> OCF extraction) on B200.
+
+BASELINE.json metric: "MCTS leaf extractions/sec + e-match matches/sec at 1/2/4/8 B200 vs
+CPU ref". Workload (configs[1]): NasRNN analog, MCTS-guided saturation + runtime-estimating
+(OCF) extraction. A *step* is one MCTS simulation step over a batch of leaves: every leaf's
+dirty e-graph (left by apply_rule's unions) is rebuilt, matched against all 22 TASO-analog
+rules (20 single + 2 multi-pattern joins) and OCF-extracted; under torchrun the per-leaf
+results are all-gathered over NCCL (the MCTS exchange of rewards / best costs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+The leaves are the reference's own rollout states (tests/golden/bench_<model>.npz, made by
+tests/golden/make_bench_leaves.py), replicated to B leaves per rank with a per-rank rotation.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MCTS leaf extractions/sec + e-match matches/sec at 1/2/4/8 B200 vs CPU ref"
+UNIT = "leaf extractions/s"
+
+
+def load_golden_leaves(model: str):
+    """Fallback leaf set: the analog's reference rollout states from tests/golden/analog_<model>."""
+    import gzip
+
+    from paper_2410_05534_b200.arena import LeafState
+    from paper_2410_05534_b200.symtab import NO_MATCH_CODE
+
+    g = json.load(gzip.open(ROOT / "tests" / "golden" / f"analog_{model}.json.gz"))
+    st = g["symtab"]
+    leaves = [LeafState.from_json(c["state"]) for c in g["cases"]]
+    symarr = {k: np.array(st[k], np.int32 if k == "params" else np.uint32)
+              for k in ("name", "arity", "rank", "poff", "params")}
+    names = {n: i for i, n in enumerate(st["names"])}
+    codes = {(type(v), v): i for i, v in enumerate(st["values"])}
+    ref = np.array([float.fromhex(c["extract"]["ocf"]["cost"]) for c in g["cases"]])
+    return (leaves, symarr, lambda n: names.get(n, -1), lambda v: codes.get((type(v), v), NO_MATCH_CODE), ref,
+            {"model": model, "source": "golden"})
+
+
+def load_leaves(model: str):
+    from paper_2410_05534_b200.arena import LeafState
+
+    path = ROOT / "tests" / "golden" / f"bench_{model}.npz"
+    if not path.exists():
+        return load_golden_leaves(model)
+    z = np.load(path)
+    meta = json.loads(str(z["meta"]))
+    L = int(z["n_leaves"])
+    nb, kb, ub = z["node_base"].astype(np.int64), z["kid_base"].astype(np.int64), z["id_base"].astype(np.int64)
+    leaves = []
+    for l in range(L):
+        n0, n1, k0, k1, u0, u1 = nb[l], nb[l + 1], kb[l], kb[l + 1], ub[l], ub[l + 1]
+        leaves.append(LeafState(z["hc_sym"][n0:n1], z["hc_koff"][n0 + l:n1 + l + 1], z["hc_kids"][k0:k1],
+                                z["hc_cid"][n0:n1], z["hc_cost"][n0:n1], z["uf_parent"][u0:u1],
+                                z["uf_rank"][u0:u1], int(z["root"][l])))
+    symarr = {"name": z["sym_name"], "arity": z["sym_arity"], "rank": z["sym_rank"], "poff": z["sym_poff"],
+              "params": z["sym_params"]}
+    names = {n: i for i, n in enumerate(meta["names"])}
+    codes = {(type(v), v): i for i, v in enumerate(meta["values"])}
+    name_id = lambda n: names.get(n, -1)  # noqa: E731
+    from paper_2410_05534_b200.symtab import NO_MATCH_CODE
+
+    code = lambda v: codes.get((type(v), v), NO_MATCH_CODE)  # noqa: E731
+    return leaves, symarr, name_id, code, z["ref_ocf"], meta
+
+
+def make_batch(leaves, B: int, rotate: int):
+    from paper_2410_05534_b200.arena import Batch
+
+    n = len(leaves)
+    return Batch([leaves[(rotate + i) % n] for i in range(B)]).pack(), [(rotate + i) % n for i in range(B)]
+
+
+def rules():
+    from paper_2410_05534_b200.patterns import load_rules
+
+    return load_rules("taso_analog")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(view, packed, counts_by_rule, rules_c):
+    """SURVEY.md 8(d) compulsory traffic: per leaf rebuild 44N+8C, extraction 20N+20C,
+    e-match per pattern 16N+8C+4*M*W (N live e-nodes, C classes, M matches, W words)."""
+    L = packed["n_leaves"]
+    nb = packed["node_base"].astype(np.int64)
+    n_in = np.diff(nb)
+    N = view["n"].astype(np.int64)
+    C = view["C"].astype(np.int64)
+    b_rebuild = int(np.sum(44 * n_in + 8 * C))
+    b_extract = int(np.sum(20 * N + 20 * C))
+    n_pat = sum(len(r.pattern_ids) for r in rules_c)
+    b_ematch = int(n_pat * np.sum(16 * N + 8 * C))
+    for r, cnt in zip(rules_c, counts_by_rule):
+        W = len(r.pattern_ids) + len(r.var_names) + len(r.pvar_names)
+        b_ematch += int(4 * W * int(cnt.sum()))
+    return {"rebuild": b_rebuild, "ematch": b_ematch, "extract": b_extract}
+
+
+def cpu_baseline(leaves, symarr, rules_c, budget_s: float = 15.0, threads: int = 0):
+    """The oracle port on host cores: bounded sample of the same per-leaf pipeline."""
+    from oracle import oracle as O
+    from paper_2410_05534_b200.arena import Batch
+
+    threads = threads or len(os.sched_getaffinity(0))
+    done, t_total, reps = 0, 0.0, 0
+    sample = min(len(leaves), max(threads * 4, 32))
+    packed = Batch(leaves[:sample]).pack()
+    while t_total < budget_s and reps < 50:
+        t0 = time.perf_counter()
+        O.pipeline(packed, symarr, rules_c, "ocf", threads)
+        t_total += time.perf_counter() - t0
+        done += sample
+        reps += 1
+    return done / t_total, threads, f"{sample} distinct leaves x {reps} reps ({t_total:.1f}s of CPU pipeline)"
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the oracle port) on the
+    box's host cores, on the same workload/metric; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    leaves, symarr, name_id, code, ref_ocf, meta = load_leaves(args.model)
+    from paper_2410_05534_b200.pipeline import compile_rules
+
+    _, rules_c = compile_rules(rules(), name_id, code)
+    from oracle import oracle as O
+    from paper_2410_05534_b200.arena import Batch
+
+    threads = len(os.sched_getaffinity(0))
+    sample = min(len(leaves), max(threads * 4, 32))
+    packed = Batch(leaves[:sample]).pack()
+    for _ in range(args.warmup):
+        O.pipeline(packed, symarr, rules_c, "ocf", threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.pipeline(packed, symarr, rules_c, "ocf", threads)
+    dt = time.perf_counter() - t0
+    v = sample * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+u32",
+            "data": "synthetic (reference-generated MCTS rollout leaves)",
+            "config": {"workload": f"{args.model} analog, MCTS leaf step (rebuild + 22-rule e-match + OCF), "
+                                   f"CPU oracle port, {sample} leaves/step", "model": args.model,
+                       "global_batch": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sample} leaves per step x {args.steps} steps"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=4096, help="leaves per rank per step")
+    ap.add_argument("--model", default="nasrnn")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    from paper_2410_05534_b200 import native
+    from paper_2410_05534_b200.pipeline import LeafPipeline
+
+    leaves, symarr, name_id, code, ref_ocf, meta = load_leaves(args.model)
+    ctx = native.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    pipe = LeafPipeline(ctx, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=8.0)
+    B = args.batch
+    packed, src_idx = make_batch(leaves, B, rotate=rank * B)  # contiguous shard of the global leaf sequence
+    batch = pipe.load(packed)
+
+    # warm-up (also sizes the match pools and checks parity against the reference's costs)
+    for _ in range(max(args.warmup, 3)):
+        pipe.step()
+    torch.cuda.synchronize()
+    ext = batch.download_extract()
+    while np.any(ext["status"] == native.X_CAPACITY):   # size the OCF history pool once, outside timing
+        pipe.pool *= 2
+        batch.set_pool(pipe.pool)
+        pipe.step()
+        ext = batch.download_extract()
+    exp = np.asarray(ref_ocf)[src_idx]
+    parity_ok = bool(np.all(ext["status"] == 0) and np.array_equal(ext["root_cost"].view(np.uint64),
+                                                                      exp.view(np.uint64)))
+    view = batch.download_rebuild()
+    view.update(batch.download_view())
+    counts = pipe.match_counts()
+    total_matches = int(counts.sum())
+    abytes = algorithmic_bytes(view, packed, counts, pipe.rules)
+
+    res_cost = torch.empty(B, dtype=torch.float64, device=dev)
+    res_stat = torch.empty(B, dtype=torch.int32, device=dev)
+    from paper_2410_05534_b200.parallel import allgather_leaf_results
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    stage_ms = {"rebuild": 0.0, "ematch": 0.0, "extract": 0.0}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            e = ev[k]
+            e[0].record(stream)
+            pipe.rebuild()
+            e[1].record(stream)
+            pipe.ematch()
+            e[2].record(stream)
+            pipe.extract()
+            e[3].record(stream)
+            if world > 1:  # MCTS exchange: every rank needs every leaf's reward/cost
+                batch.copy_results(res_cost.data_ptr(), res_stat.data_ptr())
+                gath_cost, gath_stat = allgather_leaf_results(res_cost, res_stat)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    for e in ev:
+        stage_ms["rebuild"] += e[0].elapsed_time(e[1])
+        stage_ms["ematch"] += e[1].elapsed_time(e[2])
+        stage_ms["extract"] += e[2].elapsed_time(e[3])
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    K = args.steps
+    value = B * world * K / (ms / 1e3)
+
+    # ---- e2e through the public API with host buffers (pinned), per step: H2D arena, 4 launches,
+    #      D2H root costs + statuses ----
+    pinned = {}
+    for k, v in packed.items():
+        if isinstance(v, np.ndarray):
+            t = torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+            pinned[k] = t.numpy()
+        else:
+            pinned[k] = v
+    h2d = sum(int(pinned[k].nbytes) for k in ("hc_sym", "hc_koff", "hc_kids", "hc_cid", "hc_cost", "uf_parent",
+                                             "uf_rank", "root"))
+    out_cost = torch.empty(B, dtype=torch.float64).pin_memory().numpy()
+    out_stat = torch.empty(B, dtype=torch.int32).pin_memory().numpy()
+    d2h = out_cost.nbytes + out_stat.nbytes
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        batch.upload(pinned)
+        pipe.step()
+        ext_h = batch.download_extract_small(out_cost, out_stat)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = B * world * args.e2e_steps / e2e_s
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    per_stage = {k: v / K for k, v in stage_ms.items()}
+    dom = max(per_stage, key=per_stage.get)
+    achieved = abytes[dom] / (per_stage[dom] / 1e3) / 1e9
+    traffic = None
+    tr = ROOT / "profiles" / "traffic.json"
+    if tr.exists():
+        traffic = json.loads(tr.read_text()).get(dom)
+    cpu = None
+    if not args.no_cpu_baseline:
+        _, rules_c = __import__("paper_2410_05534_b200.pipeline", fromlist=["x"]).compile_rules(rules(), name_id, code)
+        v, cores, sample = cpu_baseline(leaves, symarr, rules_c)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    n_nodes = np.diff(packed["node_base"].astype(np.int64))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+u32", "data": "synthetic (reference-generated MCTS rollout leaves of the analog graph)",
+        "config": {"workload": f"{args.model} analog MCTS leaf step: rebuild + 22-rule e-match (20 single, "
+                               f"2 multi-pattern joins) + OCF extraction, {B} leaves/rank",
+                   "model": args.model, "global_batch": B * world, "leaves_per_rank": B,
+                   "distinct_leaves": len(leaves), "nodes_per_leaf_mean": float(n_nodes.mean()),
+                   "parallelism": f"leaf-sharded x{world} (NCCL all-gather of per-leaf results)",
+                   "l2": f"inputs larger than L2 ({(packed['hc_sym'].nbytes * 7) / 1e6:.0f} MB leaf arena per rank)"},
+        "matches_per_s": total_matches * world * K / (ms / 1e3),
+        "matches_per_step": total_matches * world,
+        "rebuilds_per_s": B * world / (per_stage["rebuild"] / 1e3),
+        "extractions_per_s": B * world / (per_stage["extract"] / 1e3),
+        "ematch_matches_per_s": total_matches * world / (per_stage["ematch"] / 1e3),
+        "stage_ms": per_stage,
+        "parity_vs_reference": parity_ok,
+        "parity_detail": {"status_nonzero": int(np.sum(ext["status"] != 0)),
+                          "cost_mismatch": int(np.sum(ext["root_cost"].view(np.uint64) != exp.view(np.uint64))),
+                          "ocf_pool_entries_per_node": pipe.pool},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_step": abytes[dom]},
+        "roofline_by_stage": {k: {"achieved_gbs": abytes[k] / (per_stage[k] / 1e3) / 1e9,
+                                  "frac": abytes[k] / (per_stage[k] / 1e3) / 1e9 / peak} for k in per_stage},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": pipe.LAUNCHES_PER_STEP * K,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,11 @@ int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t
 int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, double* root_cost,
                           double* class_cost, uint32_t* choice, uint8_t* reachable, uint32_t* passes);
 
+/* run all work of this context on a caller-owned CUDA stream (e.g. torch's current stream) */
+int esat_ctx_set_stream(esat_ctx* ctx, void* cuda_stream);
+/* device-to-device copy of per-leaf root costs (f64[L]) and statuses (u32[L]) into caller
+ * buffers on the context stream -- feeds the NCCL all-gather of MCTS leaf results */
+int esat_copy_results(esat_batch* b, void* dev_root_cost, void* dev_status);
 /* device pointers of per-leaf summary results (for fused collectives over NCCL) */
 int esat_result_device_ptrs(esat_batch* b, void** root_cost, void** status);
 

@@ -154,3 +154,19 @@ def extract(packed: dict, view: dict, method: str, threads: int = 0) -> dict:
 
 if os.environ.get("ESAT_ORACLE_FORBID"):  # product-path guard used by tests
     raise ImportError("oracle import forbidden in this process")
+
+
+def pipeline(packed: dict, symarr: dict, compiled_rules, method: str = "ocf", threads: int = 0) -> dict:
+    """The CPU restatement of one MCTS leaf step over a batch: rebuild, every rule's
+    (joint) match, greedy extraction -- the same stages as paper_2410_05534_b200.pipeline."""
+    view = rebuild(packed, symarr["rank"], threads)
+    matches = 0
+    for r in compiled_rules:
+        if r.multi:
+            _, _, cnt, _ = joint(packed, view, symarr, [r._programs[i] for i in range(len(r.pattern_ids))],
+                                 r.var_maps, r.pvar_maps, len(r.var_names), len(r.pvar_names), threads)
+        else:
+            _, _, cnt, _ = ematch(packed, view, symarr, r._programs[0], threads)
+        matches += int(cnt.sum())
+    ext = extract(packed, view, method, threads)
+    return {"view": view, "extract": ext, "matches": matches}

@@ -18,6 +18,7 @@ using namespace esat;
 struct esat_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    bool own_stream = true;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;
     char err[512] = {0};
@@ -145,7 +146,7 @@ int esat_ctx_destroy(esat_ctx* c) {
     cudaFree(c->sym_par); cudaFree(c->d_pat); cudaFree(c->d_pat_off);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return ESAT_OK;
 }
@@ -229,6 +230,10 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     double* hcost;
     OWN(hs, N); OWN(hk, NL); OWN(hkids, K); OWN(hc, N); OWN(hcost, N); OWN(root, L);
     d.hc_sym = hs; d.hc_koff = hk; d.hc_kids = hkids; d.hc_cid = hc; d.hc_cost = hcost; d.root = root;
+    uint32_t* upi;
+    uint8_t* uri;
+    OWN(upi, U); OWN(uri, U);
+    d.uf_parent_in = upi; d.uf_rank_in = uri;
     OWN(d.uf_parent, U); OWN(d.uf_rank, U);
     OWN(d.o_n, L); OWN(d.o_merges, L); OWN(d.o_sym, N); OWN(d.o_koff, NL); OWN(d.o_kids, K); OWN(d.o_cid, N);
     OWN(d.o_cost, N);
@@ -275,8 +280,8 @@ int esat_batch_upload(esat_batch* b, const uint32_t* sym, const uint32_t* koff, 
     CK(c, cudaMemcpyAsync((void*)b->d.hc_kids, kids, 4 * K, cudaMemcpyHostToDevice, s));
     CK(c, cudaMemcpyAsync((void*)b->d.hc_cid, cid, 4 * N, cudaMemcpyHostToDevice, s));
     CK(c, cudaMemcpyAsync((void*)b->d.hc_cost, cost, 8 * N, cudaMemcpyHostToDevice, s));
-    CK(c, cudaMemcpyAsync(b->d.uf_parent, parent, 4 * U, cudaMemcpyHostToDevice, s));
-    CK(c, cudaMemcpyAsync(b->d.uf_rank, rank, U, cudaMemcpyHostToDevice, s));
+    CK(c, cudaMemcpyAsync((void*)b->d.uf_parent_in, parent, 4 * U, cudaMemcpyHostToDevice, s));
+    CK(c, cudaMemcpyAsync((void*)b->d.uf_rank_in, rank, U, cudaMemcpyHostToDevice, s));
     CK(c, cudaMemcpyAsync((void*)b->d.root, root, 4 * L, cudaMemcpyHostToDevice, s));
     b->uploaded = true;
     b->rebuilt = false;
@@ -402,6 +407,28 @@ int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, 
     if (reachable) CK(c, cudaMemcpyAsync(reachable, b->x.reach, N, cudaMemcpyDeviceToHost, s));
     if (passes) CK(c, cudaMemcpyAsync(passes, b->x.passes, 4 * L, cudaMemcpyDeviceToHost, s));
     CK(c, cudaStreamSynchronize(s));
+    return ESAT_OK;
+}
+
+int esat_ctx_set_stream(esat_ctx* c, void* stream) {
+    if (!c) return ESAT_E_ARG;
+    if (c->own_stream && c->stream) {
+        cudaStreamSynchronize(c->stream);
+        cudaStreamDestroy(c->stream);
+    }
+    c->own_stream = false;
+    c->stream = (cudaStream_t)stream;
+    return ESAT_OK;
+}
+
+int esat_copy_results(esat_batch* b, void* dev_root_cost, void* dev_status) {
+    if (!b) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    cudaSetDevice(c->device);
+    if (dev_root_cost)
+        CK(c, cudaMemcpyAsync(dev_root_cost, b->x.root_cost, 8ull * b->L, cudaMemcpyDeviceToDevice, c->stream));
+    if (dev_status)
+        CK(c, cudaMemcpyAsync(dev_status, b->x.status, 4ull * b->L, cudaMemcpyDeviceToDevice, c->stream));
     return ESAT_OK;
 }
 

@@ -22,7 +22,9 @@ struct Dev {
     // dirty hashcons input (egraph.py:138 insertion order) + union-find
     const uint32_t *hc_sym, *hc_koff, *hc_kids, *hc_cid;
     const double* hc_cost;
-    uint32_t* uf_parent;
+    const uint32_t* uf_parent_in;     // pristine input union-find (rebuild is a pure function of it)
+    const uint8_t* uf_rank_in;
+    uint32_t* uf_parent;              // working / output union-find
     uint8_t* uf_rank;
     const uint32_t* root;
     // rebuild output: compacted hashcons

@@ -81,6 +81,9 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d) {
     PassIn in{d.hc_sym + b, d.hc_koff + b + l, d.hc_kids + k0, d.hc_cid + b, d.hc_cost + b};
     uint32_t n = n0;
     if (tid == 0) sh_merges = 0;
+    // the working union-find starts as a copy of the leaf's input (snapshot semantics)
+    for (uint32_t x = tid; x < U; x += T) { parent[x] = d.uf_parent_in[u0 + x]; rank[x] = d.uf_rank_in[u0 + x]; }
+    __syncthreads();
 
     for (;;) {  // ---------------- pass (egraph.py:206-225) ----------------
         for (uint32_t s = tid; s < tsz; s += T) { tc[s] = NONE; ts[s] = NONE; }

@@ -1,0 +1,185 @@
+"""Device execution of the hot path for host e-graph objects (the drop-in layer).
+
+Each function takes an e-graph with the reference's structure -- ours
+(`paper_2410_05534_b200.egraph.EGraph`) or the reference's own `esat.egraph.EGraph`, the
+layer only touches `hashcons`, `_uf`, `classes`, `root`, `dirty`, `language`, `_version` --
+exports it to the SoA arena (arena.py), runs the CUDA kernel through the C-ABI and writes
+the result back in the reference's representation:
+
+    rebuild(eg)                 egraph.py:203-238   -> k_rebuild
+    joint_match(eg, patterns)   rewrite.py:405-433  -> k_ematch (+ k_join)
+    any_match(eg, pattern)      rewrite.py:579-589  -> k_ematch EXISTS
+    extract(eg, costs, method)  extraction.py:121-242 -> k_extract
+
+A rebuilt e-graph's device view is cached per object and version, so matching and
+extraction right after a rebuild reuse the resident arena.
+"""
+
+from __future__ import annotations
+
+import os
+from collections import defaultdict
+
+import numpy as np
+
+from . import native
+from .arena import NONE, Batch, export_state
+from .patterns import compile_pattern
+from .symtab import SymbolTable
+
+
+class Session:
+    """Process-wide device context + symbol table (one per GPU per process)."""
+
+    def __init__(self, device: int | None = None):
+        self.ctx = native.Context(int(os.environ.get("ESAT_DEVICE", "0")) if device is None else device)
+        self.symtab = SymbolTable()
+        self._uploaded = -1
+
+    def sync_symtab(self):
+        self.symtab.finalize()
+        if self._uploaded != self.symtab._version:
+            self.ctx.upload_symtab(self.symtab.arrays())
+            self._uploaded = self.symtab._version
+
+
+_SESSION: Session | None = None
+
+
+def session() -> Session:
+    global _SESSION
+    if _SESSION is None:
+        _SESSION = Session()
+    return _SESSION
+
+
+class _Resident:
+    __slots__ = ("version", "batch", "view", "packed", "costs_key")
+
+    def __init__(self, version, batch, view, packed, costs_key=None):
+        self.version, self.batch, self.view, self.packed, self.costs_key = version, batch, view, packed, costs_key
+
+
+def _node_class(eg):
+    for node in eg.hashcons:
+        return type(node), type(node.symbol)
+    from .egraph import ENode, Symbol
+
+    return ENode, Symbol
+
+
+def _upload(eg, costs=None):
+    s = session()
+    leaf = export_state(eg, s.symtab, costs=costs)
+    if costs is not None:
+        missing = [n for n in eg.hashcons if eg.canonicalize(n) not in costs]
+        if missing:
+            raise KeyError(missing[0])
+    s.sync_symtab()
+    packed = Batch([leaf]).pack()
+    b = native.DeviceBatch(s.ctx, packed)
+    b.upload(packed)
+    b.rebuild()
+    return b, packed
+
+
+def rebuild(eg) -> int:
+    """EGraph.rebuild on the device; the host structure is replaced by the device result."""
+    b, packed = _upload(eg)
+    out = b.download_rebuild()
+    view = b.download_view()
+    merges = int(out["merges"][0])
+    n = int(out["n"][0])
+    st = session().symtab
+    ENodeT, _ = _node_class(eg)
+    sym = out["hc_sym"][:n]
+    koff = out["hc_koff"][: n + 1]
+    kids = out["hc_kids"]
+    cid = out["hc_cid"][:n]
+    nodes = [ENodeT(st.symbols[int(sym[i])], tuple(int(k) for k in kids[koff[i]:koff[i + 1]])) for i in range(n)]
+    eg.hashcons = {nodes[i]: int(cid[i]) for i in range(n)}
+    eg._uf.parent = [int(x) for x in out["uf_parent"]]
+    eg._uf.rank = [int(x) for x in out["uf_rank"]]
+    groups = defaultdict(set)
+    parents = defaultdict(set)
+    for node, c in eg.hashcons.items():
+        groups[c].add(node)
+        for ch in set(node.children):
+            parents[ch].add((node, c))   # keys are canonical after the final pass
+    EClassT = type(next(iter(eg.classes.values()))) if eg.classes else None
+    if EClassT is None:
+        from .egraph import EClass as EClassT  # noqa: N806
+    order = [int(c) for c in view["cls_id"][: int(view["C"][0])]]
+    eg.classes = {c: EClassT(c, groups[c], parents.get(c, set())) for c in order}
+    eg.dirty.clear()
+    eg._version += merges
+    eg._esat_resident = _Resident(eg._version, b, view, packed)
+    return merges
+
+
+def _resident(eg, costs=None):
+    if eg.dirty:
+        return None
+    r = getattr(eg, "_esat_resident", None)
+    key = None if costs is None else id(costs)
+    if r is not None and r.version == eg._version and (costs is None or r.costs_key == key):
+        session().sync_symtab()
+        return r
+    b, packed = _upload(eg, costs)
+    r = _Resident(eg._version, b, b.download_view(), packed, key)
+    eg._esat_resident = r
+    return r
+
+
+def joint_match(eg, patterns, language=None):
+    """Ordered, deduplicated substitutions of `patterns` (rewrite.py:405-433) on the device.
+    Returns (records[M, W], var names, pvar names, n_roots) with class ids / attribute values."""
+    r = _resident(eg)
+    s = session()
+    st = s.symtab
+    comps = [compile_pattern(p, lambda n: st.name_id(n, create=False), st.code) for p in patterns]
+    s.ctx.upload_patterns([c.program for c in comps])
+    r.batch.ematch(list(range(len(comps))))
+    vn = sorted({v for c in comps for v in c.var_names})
+    qn = sorted({q for c in comps for q in c.pvar_names})
+    if len(comps) == 1:
+        words, off, cnt = r.batch.download_matches(0)
+    else:
+        r.batch.join([(list(range(len(comps))), [[vn.index(v) for v in c.var_names] for c in comps],
+                       [[qn.index(q) for q in c.pvar_names] for c in comps], len(vn), len(qn))])
+        words, off, cnt = r.batch.download_matches(0, from_join=True)
+    W = len(comps) + len(vn) + len(qn)
+    recs = words[: int(cnt[0]) * W].reshape(-1, W) if cnt[0] else np.zeros((0, W), np.uint32)
+    return recs, vn, qn, len(comps)
+
+
+def any_match(eg, pattern) -> bool:
+    r = _resident(eg)
+    s = session()
+    st = s.symtab
+    c = compile_pattern(pattern, lambda n: st.name_id(n, create=False), st.code)
+    s.ctx.upload_patterns([c.program])
+    r.batch.ematch([0], mode=native.MATCH_EXISTS)
+    _, _, cnt = r.batch.download_matches(0)
+    return bool(cnt[0])
+
+
+def extract(eg, costs: dict, method: str):
+    """Greedy extraction on the device. Returns (status, err_class, root_cost, chosen {cid: ENode})."""
+    r = _resident(eg, costs)
+    out = native.extract_with_retry(r.batch, method)
+    st = int(out["status"][0])
+    if st != native.X_OK:
+        return st, int(out["err_class"][0]), None, None
+    v = r.view
+    C = int(v["C"][0])
+    cls_id = v["cls_id"][:C]
+    nko = v["nd_koff"]
+    ENodeT, _ = _node_class(eg)
+    symt = session().symtab
+    chosen = {}
+    for k in np.nonzero(out["reachable"][:C])[0]:
+        j = int(out["choice"][k])
+        kids = tuple(int(cls_id[p]) for p in v["nd_kpos"][nko[j]:nko[j + 1]])
+        chosen[int(cls_id[k])] = ENodeT(symt.symbols[int(v["nd_sym"][j])], kids)
+    return st, NONE, float(out["root_cost"][0]), chosen

@@ -58,7 +58,8 @@ def lib():
                      "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
                      "esat_rebuild", "esat_ematch", "esat_join", "esat_extract", "esat_batch_set_pool",
                      "esat_download_rebuild", "esat_download_view", "esat_download_matches",
-                     "esat_download_extract", "esat_result_device_ptrs"):
+                     "esat_download_extract", "esat_result_device_ptrs", "esat_ctx_set_stream",
+                     "esat_copy_results"):
             getattr(L, name).restype = C.c_int
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
         _lib = L
@@ -69,7 +70,7 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
             "esat_rebuild", "esat_ematch", "esat_join", "esat_batch_set_pool", "esat_extract",
             "esat_download_rebuild", "esat_download_view", "esat_download_matches", "esat_download_extract",
-            "esat_result_device_ptrs", "esat_last_kernel_ms")
+            "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results")
 
 
 def _p(a):
@@ -105,6 +106,10 @@ class Context:
 
     def sync(self):
         self.check(self.L.esat_ctx_sync(self.h))
+
+    def set_stream(self, cuda_stream_handle: int):
+        """Issue all work on a caller-owned stream (torch.cuda.current_stream().cuda_stream)."""
+        self.check(self.L.esat_ctx_set_stream(self.h, C.c_void_p(cuda_stream_handle)))
 
     def last_ms(self) -> float:
         return float(self.L.esat_last_kernel_ms(self.h))
@@ -198,6 +203,10 @@ class DeviceBatch:
         self._keep_join = arrs
         self.ctx.check(self.L.esat_join(self.h, C.c_uint32(len(specs)), *[_p(a) for a in arrs]))
 
+    def copy_results(self, root_cost_ptr: int, status_ptr: int):
+        """D2D copy of per-leaf root costs / statuses into caller device buffers (torch tensors)."""
+        self.ctx.check(self.L.esat_copy_results(self.h, C.c_void_p(root_cost_ptr), C.c_void_p(status_ptr)))
+
     # ---- downloads ---------------------------------------------------------------
     def download_rebuild(self) -> dict:
         L, N, K, U = self.n_leaves, self.N, self.K, self.U
@@ -227,6 +236,12 @@ class DeviceBatch:
         self.ctx.check(self.L.esat_download_extract(self.h, *[_p(o[k]) for k in (
             "status", "err_class", "root_cost", "class_cost", "choice", "reachable", "passes")]))
         return o
+
+    def download_extract_small(self, root_cost: np.ndarray, status: np.ndarray):
+        """D2H of the per-leaf root costs (f64) and statuses (u32) only -- the MCTS reward inputs."""
+        self.ctx.check(self.L.esat_download_extract(self.h, _p(status), None, _p(root_cost), None, None, None,
+                                                    None))
+        return root_cost, status
 
     def download_matches(self, index: int, from_join: bool = False):
         L = self.n_leaves

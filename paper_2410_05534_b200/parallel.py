@@ -1,0 +1,43 @@
+"""Multi-GPU leaf/seed sharding and the MCTS result exchange.
+
+Leaves of one MCTS batch step (and MCTS seeds) are independent e-graphs, so the data
+path shards with no collective: rank r owns the contiguous global leaf range
+``leaf_shard(total, world, r)``. The one real exchange is the MCTS update: every rank
+needs every leaf's (status, root cost) to backpropagate Eq. 3 rewards,
+so per step the per-leaf results are all-gathered (NCCL over NVLink on B200s; gloo in the
+CPU tests). Rank-ordered concatenation of contiguous shards is global leaf order, so the
+merged statistics are identical at any world size.
+"""
+
+from __future__ import annotations
+
+
+def leaf_shard(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [start, end) share of `total` leaves for `rank` (first ranks take the remainder)."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def allgather_leaf_results(root_cost, status, group=None):
+    """All-gather equal-size per-rank result tensors; returns tensors in global leaf order."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out_c = torch.empty(root_cost.numel() * world, dtype=root_cost.dtype, device=root_cost.device)
+    out_s = torch.empty(status.numel() * world, dtype=status.dtype, device=status.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out_c, root_cost, group=group)
+        dist.all_gather_into_tensor(out_s, status, group=group)
+    else:
+        dist.all_gather(list(out_c.chunk(world)), root_cost, group=group)
+        dist.all_gather(list(out_s.chunk(world)), status, group=group)
+    return out_c, out_s
+
+
+def rewards(prev_cost, new_cost):
+    """Eq. 3 per leaf step: max(runtime_{i-1} - runtime_i, 0)."""
+    import torch
+
+    return torch.clamp(prev_cost - new_cost, min=0.0)

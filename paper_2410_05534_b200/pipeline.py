@@ -1,0 +1,105 @@
+"""The batched MCTS-leaf pipeline on one B200: rebuild -> all-rule e-match -> join -> extract.
+
+One MCTS simulation step hands every leaf e-graph of a batch through
+the reference's hot path:
+
+    EGraph.rebuild()                      egraph.py:203      (the end of apply_rule, rewrite.py:569)
+    joint_match(rule.sources) for every rule                  rewrite.py:405  (applicability / next step)
+    extract_ocf_greedy / extract_default_greedy               extraction.py:229 / 157
+
+``LeafPipeline`` compiles the rule set against a symbol table, keeps one device batch
+resident and runs the four launches (k_rebuild, k_ematch, k_join, k_extract) per step.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .patterns import compile_pattern
+
+
+@dataclass
+class CompiledRule:
+    rule: object
+    pattern_ids: list      # positions in the e-match call
+    var_names: list        # combined, sorted
+    pvar_names: list
+    var_maps: list         # per source: output slot of each source var
+    pvar_maps: list
+
+    @property
+    def multi(self) -> bool:
+        return len(self.pattern_ids) > 1
+
+
+def compile_rules(rules, name_id, code):
+    programs, out = [], []
+    for r in rules:
+        comps = [compile_pattern(p, name_id, code) for p in r.sources]
+        vn = sorted({v for c in comps for v in c.var_names})
+        qn = sorted({q for c in comps for q in c.pvar_names})
+        ids = []
+        for c in comps:
+            ids.append(len(programs))
+            programs.append(c.program)
+        cr = CompiledRule(r, ids, vn, qn, [[vn.index(v) for v in c.var_names] for c in comps],
+                          [[qn.index(q) for q in c.pvar_names] for c in comps])
+        cr._programs = [c.program for c in comps]
+        out.append(cr)
+    return programs, out
+
+
+class LeafPipeline:
+    def __init__(self, ctx: native.Context, symtab_arrays: dict, rules, name_id, code,
+                 method: str = "ocf", pool_entries_per_node: float = 8.0):
+        self.ctx = ctx
+        self.method = method
+        self.pool = pool_entries_per_node
+        ctx.upload_symtab(symtab_arrays)
+        self.programs, self.rules = compile_rules(rules, name_id, code)
+        ctx.upload_patterns(self.programs)
+        self.pattern_ids = list(range(len(self.programs)))
+        self.joins = [r for r in self.rules if r.multi]
+        self.batch = None
+
+    def load(self, packed: dict):
+        if self.batch is not None:
+            self.batch.close()
+        self.batch = native.DeviceBatch(self.ctx, packed)
+        self.batch.set_pool(self.pool)
+        self.batch.upload(packed)
+        return self.batch
+
+    # the four stages -------------------------------------------------------------
+    def rebuild(self):
+        self.batch.rebuild()
+
+    def ematch(self):
+        self.batch.ematch(self.pattern_ids)
+        if self.joins:
+            self.batch.join([(r.pattern_ids, r.var_maps, r.pvar_maps, len(r.var_names), len(r.pvar_names))
+                             for r in self.joins])
+
+    def extract(self):
+        self.batch.extract(self.method)
+
+    def step(self):
+        self.rebuild()
+        self.ematch()
+        self.extract()
+
+    LAUNCHES_PER_STEP = 4  # k_rebuild, k_ematch, k_join, k_extract
+
+    def match_counts(self) -> np.ndarray:
+        """Unique matches per rule per leaf of the last step: [rules, leaves]."""
+        rows = []
+        for j, r in enumerate(self.rules):
+            if r.multi:
+                _, _, cnt = self.batch.download_matches(self.joins.index(r), from_join=True)
+            else:
+                _, _, cnt = self.batch.download_matches(r.pattern_ids[0])
+            rows.append(cnt)
+        return np.stack(rows) if rows else np.zeros((0, self.batch.n_leaves), np.uint32)

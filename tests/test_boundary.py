@@ -1,0 +1,68 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and exports every
+symbol include/esat_b200.h declares; host format helpers round-trip; no CPU fallback."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_header_symbols_exported():
+    from paper_2410_05534_b200 import native
+
+    header = (ROOT / "include" / "esat_b200.h").read_text()
+    declared = set(re.findall(r"^(?:int|const char\*|float)\s+(esat_\w+)\(", header, re.M))
+    assert declared, "no declarations parsed"
+    lib = native.lib()  # loads the sm_100a .so (no GPU needed to dlopen)
+    missing = sorted(s for s in declared if not hasattr(lib, s))
+    assert not missing, missing
+    assert declared == set(native.EXPORTED)
+
+
+def test_no_cpu_fallback_without_gpu():
+    """Without a usable B200 the product path must fail loudly, never fall back to the oracle."""
+    import torch
+
+    from paper_2410_05534_b200 import native
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(native.NativeUnavailable):
+        native.Context(0)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = ROOT / "paper_2410_05534_b200"
+    for f in pkg.rglob("*.py"):
+        src = f.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_leafstate_json_roundtrip():
+    from golden_io import load_group
+
+    from paper_2410_05534_b200.arena import Batch, LeafState
+
+    c = load_group("toy")["cases"][3]
+    lf = LeafState.from_json(c["state"])
+    assert LeafState.from_json(lf.to_json()).to_json() == c["state"]
+    p = Batch([lf, lf]).pack()
+    assert p["node_base"].tolist() == [0, lf.n, 2 * lf.n]
+    assert len(p["hc_koff"]) == 2 * (lf.n + 1)
+
+
+def test_pattern_program_layout():
+    from paper_2410_05534_b200.patterns import compile_pattern, parse_pattern
+
+    pat = parse_pattern("(conv2d[?s,?p,none] ?x (ewadd ?w1 ?w2))")
+    names = {"conv2d": 3, "ewadd": 5}
+    prog = compile_pattern(pat, lambda n: names.get(n, -1), lambda v: {"none": 9}.get(v, 0x3FFFFFFF)).program
+    P, V, Q = prog[:3]
+    assert (P, V, Q) == (5, 3, 2)
+    rec0 = prog[3:9]
+    assert rec0[0] == 1 and rec0[1] == 3 and rec0[2] == 2 and rec0[3] == 3
+    slots = prog[rec0[4]: rec0[4] + 3]
+    assert slots.tolist() == [-(1 + 1), -(0 + 1), 9]  # ?s -> pvar 1 (sorted p,s), ?p -> 0, literal none
