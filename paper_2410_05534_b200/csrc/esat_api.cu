@@ -72,7 +72,7 @@ struct esat_batch {
     // owned device buffers
     std::vector<void*> owned;
     // OCF pool
-    double pool_factor = 8.0;
+    double pool_factor = 32.0;
     std::vector<uint64_t> pb;
     uint64_t pool_total = 0;
     uint64_t* d_pb = nullptr;
@@ -249,7 +249,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
-    OWN(x.hoff, 2 * N); OWN(x.hlen, 2 * N);
+    OWN(x.hoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.chg, 2 * N);
     x.slot_stride = N;
     *out = b;
     return ESAT_OK;
@@ -326,8 +326,8 @@ static int ensure_pool(esat_batch* b) {
     b->d_pb = nullptr; b->pool_key = nullptr; b->pool_val = nullptr;
     CK(c, cudaMalloc((void**)&b->d_pb, 8ull * (b->L + 1)));
     CK(c, cudaMemcpy(b->d_pb, b->pb.data(), 8ull * (b->L + 1), cudaMemcpyHostToDevice));
-    CK(c, cudaMalloc((void**)&b->pool_key, 2 * 4ull * b->pool_total));
-    CK(c, cudaMalloc((void**)&b->pool_val, 2 * 8ull * b->pool_total));
+    CK(c, cudaMalloc((void**)&b->pool_key, 4ull * b->pool_total));
+    CK(c, cudaMalloc((void**)&b->pool_val, 8ull * b->pool_total));
     return ESAT_OK;
 }
 
@@ -344,7 +344,7 @@ int esat_extract(esat_batch* b, int method) {
         x.pool_base = b->d_pb;
         x.pool_key = b->pool_key;
         x.pool_val = b->pool_val;
-        x.pool_stride = b->pool_total;
+        x.pool_stride = 0;   // one cumulative region per leaf
     }
     tic(c);
     if (b->L) k_extract<128><<<b->L, 128, 0, c->stream>>>(b->d, x);

@@ -53,12 +53,14 @@ struct XArgs {
     double *root_cost, *class_cost, *prev;
     uint32_t *choice, *level, *order, *lvcnt, *stk, *stki;
     uint8_t *reach;
-    // OCF history pool: per leaf [pool_base[l], pool_base[l+1]) entries per parity
+    // OCF history pool: per leaf [pool_base[l], pool_base[l+1]) entries, bump-allocated over all
+    // passes (unchanged classes keep pointing at earlier histories)
     const uint64_t* pool_base;
     uint32_t *pool_key;          // 2 parities x entries
     double* pool_val;
     uint64_t pool_stride;        // offset of parity 1
-    uint32_t *hoff, *hlen;       // [2][node rows] history slot per class position
+    uint32_t *hoff, *hlen;       // [2][node rows] history slot per class position (pass parity)
+    uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip)
     uint64_t slot_stride;
 };
 

@@ -309,6 +309,52 @@ __device__ uint32_t block_products(const Src* src, int S, const uint32_t* lo, co
     }
 }
 
+
+constexpr uint32_t JOIN_SMEM_KEYS = 4096;   // source-1 index sorted in shared memory
+
+// Block-wide bitonic sort of n (power of two) u64 keys in shared memory.
+__device__ void block_bitonic(unsigned long long* k, uint32_t n) {
+    for (uint32_t size = 2; size <= n; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < n / 2; i += blockDim.x) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const unsigned long long a = k[lo], b = k[hi];
+                if ((a > b) == up) { k[lo] = b; k[hi] = a; }
+            }
+        }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t lower_bound_key(const unsigned long long* k, uint32_t n, unsigned long long x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (k[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Products of the source-0 records [g, ge) (one root group) with the source-1 records that share
+// the join variable (runs of the sorted index); consistent ones are emitted in index order.
+template <typename Emit>
+__device__ uint32_t indexed_products(const Src* src, uint32_t g, uint32_t ge, uint32_t v0, const unsigned long long* keys,
+                                     uint32_t n1, uint32_t NV, uint32_t NQ, Emit emit) {
+    uint32_t rec_[MAX_W], idx[2];
+    uint32_t n = 0;
+    for (uint32_t i = g; i < ge; i++) {
+        const uint32_t x = src[0].w[(uint64_t)i * src[0].W + 1 + v0];
+        for (uint32_t p = lower_bound_key(keys, n1, (unsigned long long)x << 32); p < n1 && (uint32_t)(keys[p] >> 32) == x; p++) {
+            idx[0] = i;
+            idx[1] = (uint32_t)keys[p];
+            if (combine(src, 2, idx, NV, NQ, rec_)) { emit(rec_); n++; }
+        }
+    }
+    return n;
+}
+
 }  // namespace
 
 template <int T>
@@ -340,13 +386,32 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         g_lo = group_start_at_or_after(src[0], min(n0, tid * ch));
         g_hi = group_start_at_or_after(src[0], min(n0, (tid + 1) * ch));
     }
+    // sort-join fast path: two sources sharing a variable -> index source 1 by that variable
+    __shared__ unsigned long long sh_keys[JOIN_SMEM_KEYS];
+    uint32_t v0 = NONE, v1 = NONE;
+    if (S == 2 && !empty)
+        for (uint32_t b = 0; b < src[1].V && v0 == NONE; b++)
+            for (uint32_t a0 = 0; a0 < src[0].V; a0++)
+                if (src[0].vmap[a0] == src[1].vmap[b]) { v0 = a0; v1 = b; break; }
+    const bool indexed = v0 != NONE && src[1].n <= JOIN_SMEM_KEYS;
+    uint32_t n1p = 0;
+    if (indexed) {
+        n1p = 1;
+        while (n1p < src[1].n) n1p <<= 1;
+        for (uint32_t i = tid; i < n1p; i += T)
+            sh_keys[i] = i < src[1].n ? ((unsigned long long)src[1].w[(uint64_t)i * src[1].W + 1 + v1] << 32) | i
+                                      : ~0ull;
+        block_bitonic(sh_keys, n1p);
+    }
     auto count_only = [](const uint32_t*) {};
     uint32_t cnt = 0;
     for (uint32_t g = g_lo; g < g_hi;) {
         const uint32_t ge = group_end(src[0], g);
-        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
-            cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
-        });
+        if (indexed) cnt += indexed_products(src, g, ge, v0, sh_keys, src[1].n, NV, NQ, count_only);
+        else
+            for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+                cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
+            });
         g = ge;
     }
     uint32_t tot;
@@ -364,15 +429,25 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     uint32_t cur = 0;
     for (uint32_t g = g_lo; g < g_hi;) {
         const uint32_t ge = group_end(src[0], g);
-        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+        if (indexed) {
+            // one root group of source 0: runs per record are sorted; sort the group's union
             const uint32_t start = cur;
-            block_products(src, S, lo, hi, NV, NQ, [&](const uint32_t* rr) {
+            indexed_products(src, g, ge, v0, sh_keys, src[1].n, NV, NQ, [&](const uint32_t* rr) {
                 for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
                 cur++;
             });
-            // products of one block share the roots prefix; distinct pairs give distinct keys
-            sort_unique(out + (uint64_t)start * W, cur - start, W);
-        });
+            if (ge - g > 1) sort_unique(out + (uint64_t)start * W, cur - start, W);
+        } else {
+            for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+                const uint32_t start = cur;
+                block_products(src, S, lo, hi, NV, NQ, [&](const uint32_t* rr) {
+                    for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
+                    cur++;
+                });
+                // products of one block share the roots prefix; distinct pairs give distinct keys
+                sort_unique(out + (uint64_t)start * W, cur - start, W);
+            });
+        }
         g = ge;
     }
 }

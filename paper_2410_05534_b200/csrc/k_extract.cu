@@ -314,15 +314,33 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
         const int pass = (int)it;
         c.pass = pass;
         for (uint32_t k = tid; k < C; k += T) prev[k] = cost[k];
-        if (tid == 0) { sh_flag = 0; sh_top = 0; }
+        if (tid == 0) { sh_flag = 0; if (pass == 0) sh_top = 0; }
         __syncthreads();
+        const int par = pass & 1, ppar = par ^ 1;
+        uint8_t* chg_cur = x.chg + par * x.slot_stride + b;
+        const uint8_t* chg_prv = x.chg + ppar * x.slot_stride + b;
         for (uint32_t lv = 0; lv < nlv; lv++) {
             const uint32_t lo = lv ? lvcnt[lv - 1] : 0u, hi = lvcnt[lv];
             for (uint32_t idx = lo + tid; idx < hi; idx += T) {
                 const uint32_t k = order[idx];
                 c.k = k;
+                // Dirty skip (exact): the class's inputs are its children's (cost, history) as read
+                // under the Gauss-Seidel rule; if none changed since the class's last evaluation its
+                // outputs are identical, so only the history slot pointer is carried forward.
+                bool need = pass == 0;
+                for (uint32_t nd = coff[k]; nd < coff[k + 1] && !need; nd++)
+                    for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
+                        const uint32_t j = c.kpos[q];
+                        if (j < k ? chg_cur[j] : chg_prv[j]) { need = true; break; }
+                    }
+                if (!need) {
+                    chg_cur[k] = 0;
+                    if (ocf && C > 1) { hoffw[par][k] = hoffw[ppar][k]; hlenw[par][k] = hlenw[ppar][k]; }
+                    continue;
+                }
                 double bv = __longlong_as_double(0x7ff0000000000000ll);
                 uint32_t bn = NONE;
+                bool changed = pass == 0;
                 if (!ocf) {
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++) {
                         double v = c.ncost[nd];
@@ -335,7 +353,6 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                     uint32_t hn = NONE, hsize = 0, hgoff = 0;
                     double h_cc1 = 0, h_cc2 = 0;
                     bool h_skip2 = true, h_gen = false;
-                    const int par = pass & 1;
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++) {
                         double v;
                         if (c.nko[nd + 1] - c.nko[nd] <= 2) {
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                             if (v < hb) { hb = v; hn = nd; hsize = size; h_cc1 = cc1; h_cc2 = cc2; h_skip2 = skip2; h_gen = false; }
                         } else {
                             uint32_t goff, gn;
-                            v = ocf_generic(c, nd, &sh_top, pcap, pkw[par], pvw[par], &goff, &gn, &sh_over);
+                            v = ocf_generic(c, nd, &sh_top, pcap, pkw[0], pvw[0], &goff, &gn, &sh_over);
                             if (v < hb) { hb = v; hn = nd; hsize = gn; hgoff = goff; h_gen = true; }
                         }
                         if (bn == NONE || v < bv) { bv = v; bn = nd; }
@@ -360,13 +377,21 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                         } else {
                             off = atomicAdd(&sh_top, hsize);
                             if ((uint64_t)off + hsize > pcap) { sh_over = 1; hsize = 0; off = 0; }
-                            else ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw[par] + off, pvw[par] + off);
+                            else ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw[0] + off, pvw[0] + off);
                         }
                         hoffw[par][k] = off;
                         hlenw[par][k] = hsize;
+                        if (!changed) {  // did the flushed history change w.r.t. last pass?
+                            const uint32_t o2 = hoffw[ppar][k], n2 = hlenw[ppar][k];
+                            if (n2 != hsize) changed = true;
+                            for (uint32_t i = 0; i < hsize && !changed; i++)
+                                changed = pkw[0][off + i] != pkw[0][o2 + i] ||
+                                          __double_as_longlong(pvw[0][off + i]) != __double_as_longlong(pvw[0][o2 + i]);
+                        }
                     }
                 }
-                if (bn != NONE && bv < cost[k]) { cost[k] = bv; ch[k] = bn; sh_flag = 1; }
+                if (bn != NONE && bv < cost[k]) { cost[k] = bv; ch[k] = bn; sh_flag = 1; changed = true; }
+                chg_cur[k] = changed ? 1 : 0;
             }
             __syncthreads();
         }
