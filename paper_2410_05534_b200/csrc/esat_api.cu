@@ -1,6 +1,7 @@
 // C ABI of libesat_b200 (declared in include/esat_b200.h): context, batch arena, launches.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -347,7 +348,12 @@ int esat_extract(esat_batch* b, int method) {
         x.pool_stride = 0;   // one cumulative region per leaf
     }
     tic(c);
-    if (b->L) k_extract<128><<<b->L, 128, 0, c->stream>>>(b->d, x);
+    static const int xt = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 32;
+    if (b->L) {
+        if (xt == 128) k_extract<128><<<b->L, 128, 0, c->stream>>>(b->d, x);
+        else if (xt == 64) k_extract<64><<<b->L, 64, 0, c->stream>>>(b->d, x);
+        else k_extract<32><<<b->L, 32, 0, c->stream>>>(b->d, x);
+    }
     toc(c);
     return launch_check(c, "k_extract");
 }

@@ -337,19 +337,58 @@ __device__ __forceinline__ uint32_t lower_bound_key(const unsigned long long* k,
     return lo;
 }
 
-// Products of the source-0 records [g, ge) (one root group) with the source-1 records that share
-// the join variable (runs of the sorted index); consistent ones are emitted in index order.
-template <typename Emit>
-__device__ uint32_t indexed_products(const Src* src, uint32_t g, uint32_t ge, uint32_t v0, const unsigned long long* keys,
-                                     uint32_t n1, uint32_t NV, uint32_t NQ, Emit emit) {
-    uint32_t rec_[MAX_W], idx[2];
+// Output plan of a two-source join (shared memory): output word w comes from source src[w]
+// at word idx[w]; nchk pairs of (source-0 word, source-1 word) must be equal.
+struct JoinPlan {
+    uint8_t src[MAX_W], idx[MAX_W];
+    uint8_t c0[2 * MAX_V], c1[2 * MAX_V];
+    uint32_t nchk, W;
+};
+
+__device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ) {
+    p.W = 2 + NV + NQ;
+    p.src[0] = 0; p.idx[0] = 0; p.src[1] = 1; p.idx[1] = 0;
+    for (uint32_t o = 0; o < NV + NQ; o++) { p.src[2 + o] = 255; p.idx[2 + o] = 0; }
+    p.nchk = 0;
+    for (uint32_t v = 0; v < s[0].V; v++) { p.src[2 + s[0].vmap[v]] = 0; p.idx[2 + s[0].vmap[v]] = 1 + v; }
+    for (uint32_t q = 0; q < s[0].Q; q++) {
+        p.src[2 + NV + s[0].qmap[q]] = 0;
+        p.idx[2 + NV + s[0].qmap[q]] = 1 + s[0].V + q;
+    }
+    for (uint32_t v = 0; v < s[1].V; v++) {
+        const uint32_t o = 2 + s[1].vmap[v];
+        if (p.src[o] == 0) { p.c0[p.nchk] = p.idx[o]; p.c1[p.nchk] = 1 + v; p.nchk++; }
+        else { p.src[o] = 1; p.idx[o] = 1 + v; }
+    }
+    for (uint32_t q = 0; q < s[1].Q; q++) {
+        const uint32_t o = 2 + NV + s[1].qmap[q];
+        if (p.src[o] == 0) { p.c0[p.nchk] = p.idx[o]; p.c1[p.nchk] = 1 + s[1].V + q; p.nchk++; }
+        else { p.src[o] = 1; p.idx[o] = 1 + s[1].V + q; }
+    }
+}
+
+// Products of the source-0 records [g, ge) (one root group) with the source-1 records sharing the
+// join variable (runs of the sorted index); consistent pairs are written (out != null) in index
+// order. Returns the number of products.
+__device__ uint32_t indexed_products(const uint32_t* w0, uint32_t W0, const uint32_t* w1, uint32_t W1,
+                                     const JoinPlan& jp, uint32_t g, uint32_t ge, uint32_t v0,
+                                     const unsigned long long* keys, uint32_t n1, uint32_t* out) {
     uint32_t n = 0;
+    const uint32_t W = jp.W;
     for (uint32_t i = g; i < ge; i++) {
-        const uint32_t x = src[0].w[(uint64_t)i * src[0].W + 1 + v0];
-        for (uint32_t p = lower_bound_key(keys, n1, (unsigned long long)x << 32); p < n1 && (uint32_t)(keys[p] >> 32) == x; p++) {
-            idx[0] = i;
-            idx[1] = (uint32_t)keys[p];
-            if (combine(src, 2, idx, NV, NQ, rec_)) { emit(rec_); n++; }
+        const uint32_t* m1 = w0 + (uint64_t)i * W0;
+        const uint32_t x = m1[1 + v0];
+        for (uint32_t p = lower_bound_key(keys, n1, (unsigned long long)x << 32); p < n1 && (uint32_t)(keys[p] >> 32) == x;
+             p++) {
+            const uint32_t* m2 = w1 + (uint64_t)(uint32_t)keys[p] * W1;
+            bool ok = true;
+            for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1[jp.c0[c]] == m2[jp.c1[c]];
+            if (!ok) continue;
+            if (out) {
+                uint32_t* o = out + (uint64_t)n * W;
+                for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.idx[w]] : m1[jp.idx[w]];
+            }
+            n++;
         }
     }
     return n;
@@ -403,11 +442,17 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                                       : ~0ull;
         block_bitonic(sh_keys, n1p);
     }
+    const uint32_t* w0 = src[0].w;
+    const uint32_t* w1 = src[S > 1 ? 1 : 0].w;
+    const uint32_t W0 = src[0].W, W1 = src[S > 1 ? 1 : 0].W;
+    __shared__ JoinPlan sh_plan;
+    if (indexed && tid == 0) make_plan(sh_plan, src, NV, NQ);
+    __syncthreads();
     auto count_only = [](const uint32_t*) {};
     uint32_t cnt = 0;
     for (uint32_t g = g_lo; g < g_hi;) {
         const uint32_t ge = group_end(src[0], g);
-        if (indexed) cnt += indexed_products(src, g, ge, v0, sh_keys, src[1].n, NV, NQ, count_only);
+        if (indexed) cnt += indexed_products(w0, W0, w1, W1, sh_plan, g, ge, v0, sh_keys, src[1].n, nullptr);
         else
             for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
                 cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
@@ -432,10 +477,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         if (indexed) {
             // one root group of source 0: runs per record are sorted; sort the group's union
             const uint32_t start = cur;
-            indexed_products(src, g, ge, v0, sh_keys, src[1].n, NV, NQ, [&](const uint32_t* rr) {
-                for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
-                cur++;
-            });
+            cur += indexed_products(w0, W0, w1, W1, sh_plan, g, ge, v0, sh_keys, src[1].n, out + (uint64_t)cur * W);
             if (ge - g > 1) sort_unique(out + (uint64_t)start * W, cur - start, W);
         } else {
             for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {

@@ -4,9 +4,9 @@
 
 namespace esat {
 
-constexpr int MAX_PN = 32;   // pattern nodes
-constexpr int MAX_V = 16;    // vars / pvars per pattern
-constexpr int MAX_W = 40;    // words per record
+constexpr int MAX_PN = 16;   // pattern nodes (larger patterns are rejected with ESAT_E_ARG)
+constexpr int MAX_V = 8;     // vars / pvars per pattern
+constexpr int MAX_W = 24;    // words per record
 constexpr int MAX_S = 4;     // sources per multi-pattern rule
 
 struct MArgs {

@@ -269,28 +269,50 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
         level[k] = 0;
         x.reach[b + k] = 0;
     }
-    if (tid == 0) { sh_maxlv = 0; sh_over = 0; }
+    if (tid == 0) sh_over = 0;
     __syncthreads();
-    // ---- K7: wavefront levels over lower-position children (monotone relaxation) ----
-    for (;;) {
-        if (tid == 0) sh_flag = 0;
-        __syncthreads();
-        for (uint32_t k = tid; k < C; k += T) {
-            uint32_t lv = 0;
-            for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
-                for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
-                    const uint32_t j = c.kpos[q];
-                    if (j < k) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
-                }
-            if (lv > level[k]) { level[k] = lv; sh_flag = 1; }
+    // ---- K7: wavefront levels over lower-position children ----
+    // level[k] = 1 + max level of k's lower-position children. Warp 0 walks the classes in
+    // position order 32 at a time: children below the chunk are final; dependencies inside the
+    // chunk are resolved by re-evaluating the chunk until no lane changes (chain length + 1 rounds).
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t mx = 0;
+        for (uint32_t k0 = 0; k0 < C; k0 += 32) {
+            const uint32_t k = k0 + tid;
+            uint32_t base = 0;
+            if (k < C)
+                for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
+                    for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
+                        const uint32_t j = c.kpos[q];
+                        if (j < k0) { const uint32_t t = level[j] + 1; base = t > base ? t : base; }
+                    }
+            if (k < C) level[k] = base;
+            __syncwarp();
+            for (;;) {
+                uint32_t lv = base;
+                if (k < C)
+                    for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
+                        for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
+                            const uint32_t j = c.kpos[q];
+                            if (j >= k0 && j < k) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
+                        }
+                const bool upd = k < C && lv != level[k];
+                __syncwarp();
+                if (upd) level[k] = lv;
+                __syncwarp();
+                if (!__any_sync(0xffffffffu, upd)) break;
+            }
+            const uint32_t lk = k < C ? level[k] : 0u;
+            mx = max(mx, __reduce_max_sync(0xffffffffu, lk));
         }
-        __syncthreads();
-        if (!sh_flag) break;
+        if (tid == 0) sh_maxlv = mx;
     }
+    __syncthreads();
     // counting sort of classes by level
     for (uint32_t k = tid; k <= C; k += T) lvcnt[k] = 0;
     __syncthreads();
-    for (uint32_t k = tid; k < C; k += T) { atomicAdd(&lvcnt[level[k]], 1u); atomicMax(&sh_maxlv, level[k]); }
+    for (uint32_t k = tid; k < C; k += T) atomicAdd(&lvcnt[level[k]], 1u);
     __syncthreads();
     const uint32_t nlv = C ? sh_maxlv + 1 : 0;
     uint32_t base = 0;
@@ -396,7 +418,9 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
             __syncthreads();
         }
         passes++;
-        if (!sh_flag) { st = X_OK; break; }
+        const bool any_change = sh_flag != 0;
+        __syncthreads();   // everyone has read the flag before thread 0 resets it for the next pass
+        if (!any_change) { st = X_OK; break; }
     }
     if (sh_over) st = X_CAPACITY;
 
@@ -435,7 +459,8 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
     }
 }
 
+template __global__ void k_extract<32>(Dev, XArgs);
+template __global__ void k_extract<64>(Dev, XArgs);
 template __global__ void k_extract<128>(Dev, XArgs);
-template __global__ void k_extract<256>(Dev, XArgs);
 
 }  // namespace esat
