@@ -89,6 +89,7 @@ struct esat_batch {
     unsigned long long* d_tops = nullptr;   // [0] stage, [1] ematch out, [2] join stage, [3] join out
     uint32_t* d_jspec = nullptr;
     uint64_t jspec_cap = 0;
+    uint32_t* d_raw = nullptr;
 };
 
 namespace {
@@ -96,7 +97,8 @@ namespace {
 template <typename T>
 int own(esat_batch* b, T** p, size_t n) {
     *p = nullptr;
-    CK(b->ctx, cudaMalloc((void**)p, sizeof(T) * (n ? n : 1)));
+    // +64 B: TMA bulk copies read 16-B aligned spans that may round past the last element
+    CK(b->ctx, cudaMalloc((void**)p, sizeof(T) * (n ? n : 1) + 64));
     b->owned.push_back((void*)*p);
     return ESAT_OK;
 }
@@ -263,7 +265,7 @@ int esat_batch_destroy(esat_batch* b) {
     cudaFree(b->d_pb); cudaFree(b->pool_key); cudaFree(b->pool_val);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
-    cudaFree(b->d_over); cudaFree(b->d_tops); cudaFree(b->d_jspec);
+    cudaFree(b->d_over); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
     delete b;
     return ESAT_OK;
 }
@@ -475,6 +477,7 @@ extern "C" {
 
 int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     if (!b || (P && !pat_ids) || (mode != ESAT_MATCH_LIST && mode != ESAT_MATCH_EXISTS)) return ESAT_E_ARG;
+    if (P > 32) return fail(b->ctx, ESAT_E_ARG, "at most 32 patterns per esat_ematch call (got %u)", P);
     esat_ctx* c = b->ctx;
     if (!b->rebuilt) return fail(c, ESAT_E_STATE, "ematch requires a rebuilt e-graph");
     for (uint32_t i = 0; i < P; i++)
@@ -499,6 +502,7 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
     b->m_P = P;
+    if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * L * 32 * 128));
     if (!b->stage_cap) {
         if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
         if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
@@ -508,13 +512,28 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
         CK(c, cudaMemsetAsync(b->d_over, 0, 2 * sizeof(uint32_t), c->stream));
         MArgs a{};
         a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = mode;
-        a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops;
+        a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw;
         a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
         Dev d = b->d;
         d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
         d.sym_par = c->sym_par; d.n_syms = c->n_syms;
+        // dynamic SMEM for staging the largest leaf's view (bounded; bigger leaves read global memory)
+        uint64_t mx = 0;
+        for (uint64_t l = 0; l < L; l++) {
+            const uint64_t n = b->nb[l + 1] - b->nb[l], k = b->kb[l + 1] - b->kb[l];
+            const uint64_t bytes = 4 * (4 * n + 2 + k) + 5 * 32 + 4 * n + 32;   // view + class op masks
+            mx = bytes > mx ? bytes : mx;
+        }
+        const uint32_t cap_bytes = 100 * 1024;
+        a.smem_bytes = (uint32_t)(mx < cap_bytes ? mx : cap_bytes);
+        if (getenv("ESAT_EMATCH_NOSTAGE")) a.smem_bytes = 0;
+        static uint32_t attr_set = 0;
+        if (a.smem_bytes > attr_set) {
+            CK(c, cudaFuncSetAttribute(k_ematch<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_bytes));
+            attr_set = cap_bytes;
+        }
         tic(c);
-        if (L && P) k_ematch<128><<<dim3((unsigned)L, P), 128, 0, c->stream>>>(d, a);
+        if (L && P) k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, a);
         toc(c);
         if ((r = launch_check(c, "k_ematch"))) return r;
         if (mode == ESAT_MATCH_EXISTS) return ESAT_OK;

@@ -138,6 +138,50 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* smem, uin
     return warp_base + x - v;
 }
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) global -> shared with an mbarrier ---------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// Stage a u32 array [src, src+n) into 16-B aligned shared memory at *cursor with one bulk copy of
+// the enclosing 16-B aligned span; returns the element pointer inside shared memory. Issued by one
+// thread; *tx accumulates the bytes the mbarrier must expect. Global buffers carry >= 16 B of
+// padding so the rounded-up span never leaves the allocation.
+__device__ __forceinline__ const uint32_t* stage_u32(const uint32_t* src, uint32_t n, unsigned char** cursor,
+                                                     uint64_t* bar, uint32_t* tx, bool issue) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t a0 = a & ~uintptr_t(15), a1 = (a + 4ull * n + 15) & ~uintptr_t(15);
+    unsigned char* dst = *cursor;
+    const uint32_t bytes = (uint32_t)(a1 - a0);
+    if (issue && bytes) bulk_g2s(dst, reinterpret_cast<const void*>(a0), bytes, bar);
+    *tx += bytes;
+    *cursor = dst + bytes;
+    return reinterpret_cast<const uint32_t*>(dst + (a - a0));
+}
+__device__ __forceinline__ uint32_t staged_bytes_u32(const uint32_t* src, uint32_t n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    return (uint32_t)(((a + 4ull * n + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
+}
+
 // Python max(a, b): returns a unless b > a (extraction.py:214, 217).
 __device__ __forceinline__ double pymax(double a, double b) { return b > a ? b : a; }
 

@@ -17,6 +17,8 @@
 // whole groups of source-0 records with equal root; for each combination of root groups of
 // the other sources the consistent products form one block with a fixed roots prefix, which is
 // sorted locally, so blocks come out in (roots, vars, pvars) = _subst_key order.
+#include <cstdio>
+
 #include "k_ematch_args.cuh"
 
 namespace esat {
@@ -151,81 +153,226 @@ __device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
 
 template <int T>
 __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
-    const uint32_t l = blockIdx.x, pi = blockIdx.y, tid = threadIdx.x;
-    const uint32_t L = d.L;
-    __shared__ int32_t sprog[3 + 6 * MAX_PN + 4 * MAX_PN];
+    // One CTA per leaf runs every pattern of the call. The leaf's clean view (class ids/offsets,
+    // node symbols, child CSR) is staged into shared memory with TMA bulk copies when it fits,
+    // so the backtracking matcher's dependent loads hit SMEM instead of L2.
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr uint32_t PROG_WORDS = 1024, SYM_WORDS = 1024;
+    __shared__ int32_t sprog[PROG_WORDS];
+    __shared__ uint32_t ssym[SYM_WORDS];
     __shared__ uint32_t sh_scan[33];
     __shared__ unsigned long long sh_base;
-    const uint32_t pid = a.pat_ids[pi];
-    const uint32_t po = a.prog_off[pid], pn = a.prog_off[pid + 1] - po;
-    for (uint32_t w = tid; w < pn; w += T) sprog[w] = a.prog[po + w];
-    __syncthreads();
-    Matcher m;
-    m.prog = sprog;
-    m.P = sprog[0]; m.V = sprog[1]; m.Q = sprog[2];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr uint32_t MAXP = 32;   // patterns per call (host-checked)
+    __shared__ uint32_t sh_tot[MAXP];
+    __shared__ unsigned long long sh_pbase[MAXP];
+    const uint32_t l = blockIdx.x, tid = threadIdx.x;
+    if (tid < MAXP) sh_tot[tid] = 0;
+    const uint32_t L = d.L;
     const uint64_t b = d.nb[l];
-    m.cls_id = d.cls_id + b;
-    m.cls_off = d.cls_off + b + l;
-    m.nd_sym = d.nd_sym + b;
-    m.nd_koff = d.nd_koff + b + l;
-    m.nd_kpos = d.nd_kpos + d.kb[l];
-    m.s_name = d.sym_name; m.s_arity = d.sym_arity; m.s_poff = d.sym_poff; m.s_par = d.sym_par;
-    const uint32_t W = 1 + m.V + m.Q;
     const uint32_t C = d.v_C[l];
+    const uint32_t* g_cls_id = d.cls_id + b;
+    const uint32_t* g_cls_off = d.cls_off + b + l;
+    const uint32_t N = g_cls_off[C];
+    const uint32_t* g_nd_sym = d.nd_sym + b;
+    const uint32_t* g_nd_koff = d.nd_koff + b + l;
+    const uint32_t K = g_nd_koff[N];
+    const uint32_t* g_nd_kpos = d.nd_kpos + d.kb[l];
+    Matcher m;
+    const uint32_t need = staged_bytes_u32(g_cls_id, C) + staged_bytes_u32(g_cls_off, C + 1) +
+                          staged_bytes_u32(g_nd_sym, N) + staged_bytes_u32(g_nd_koff, N + 1) +
+                          staged_bytes_u32(g_nd_kpos, K);
+    if (need <= a.smem_bytes) {
+        if (tid == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        unsigned char* cur = dsm;
+        uint32_t tx = 0;
+        const bool issuer = tid == 0;
+        if (issuer) mbar_arrive_expect_tx(&bar, need);
+        m.cls_id = stage_u32(g_cls_id, C, &cur, &bar, &tx, issuer);
+        m.cls_off = stage_u32(g_cls_off, C + 1, &cur, &bar, &tx, issuer);
+        m.nd_sym = stage_u32(g_nd_sym, N, &cur, &bar, &tx, issuer);
+        m.nd_koff = stage_u32(g_nd_koff, N + 1, &cur, &bar, &tx, issuer);
+        m.nd_kpos = stage_u32(g_nd_kpos, K, &cur, &bar, &tx, issuer);
+    } else {
+        m.cls_id = g_cls_id; m.cls_off = g_cls_off; m.nd_sym = g_nd_sym; m.nd_koff = g_nd_koff; m.nd_kpos = g_nd_kpos;
+    }
+    // symbol table (name, arity, attribute CSR) in shared memory when it fits
+    const uint32_t ns = d.n_syms, npar = d.sym_poff[ns];
+    if (3 * ns + 1 + npar <= SYM_WORDS) {
+        for (uint32_t i = tid; i < ns; i += T) { ssym[i] = d.sym_name[i]; ssym[ns + i] = d.sym_arity[i]; }
+        for (uint32_t i = tid; i <= ns; i += T) ssym[2 * ns + i] = d.sym_poff[i];
+        for (uint32_t i = tid; i < npar; i += T) ssym[3 * ns + 1 + i] = (uint32_t)d.sym_par[i];
+        m.s_name = ssym; m.s_arity = ssym + ns; m.s_poff = ssym + 2 * ns;
+        m.s_par = reinterpret_cast<const int32_t*>(ssym + 3 * ns + 1);
+    } else {
+        m.s_name = d.sym_name; m.s_arity = d.sym_arity; m.s_poff = d.sym_poff; m.s_par = d.sym_par;
+    }
+    // the call's pattern programs
+    uint32_t pwords = 0;
+    for (uint32_t pi = 0; pi < a.P; pi++) pwords += a.prog_off[a.pat_ids[pi] + 1] - a.prog_off[a.pat_ids[pi]];
+    const bool progs_smem = pwords <= PROG_WORDS;
+    if (progs_smem) {
+        uint32_t o = 0;
+        for (uint32_t pi = 0; pi < a.P; pi++) {
+            const uint32_t po = a.prog_off[a.pat_ids[pi]], pn = a.prog_off[a.pat_ids[pi] + 1] - po;
+            for (uint32_t w = tid; w < pn; w += T) sprog[o + w] = a.prog[po + w];
+            o += pn;
+        }
+    }
+    __syncthreads();
+    if (need <= a.smem_bytes) mbar_wait(&bar, 0);
+
+    // per-class mask of the operator names present (ids < 32): a pattern whose root operator is
+    // absent from a class cannot match there, which prunes most (pattern, class) pairs at once
+    uint32_t* cmask = (need <= a.smem_bytes && need + 4 * C + 16 <= a.smem_bytes)
+                          ? reinterpret_cast<uint32_t*>(dsm + ((need + 15) & ~15u))
+                          : nullptr;
+    if (cmask) {
+        for (uint32_t k = tid; k < C; k += T) {
+            uint32_t mk = 0;
+            for (uint32_t nd = m.cls_off[k]; nd < m.cls_off[k + 1]; nd++) {
+                const uint32_t nm = m.s_name[m.nd_sym[nd]];
+                mk |= nm < 32 ? (1u << nm) : 0xFFFFFFFFu;
+            }
+            cmask[k] = mk;
+        }
+        __syncthreads();
+    }
     const uint32_t ch = (C + T - 1) / T;
     const uint32_t c_lo = min(C, tid * ch), c_hi = min(C, c_lo + ch);
     auto nothing = [](uint32_t, const uint32_t*, const int32_t*) {};
+    // per-pattern program pointers
+    auto prog_of = [&](uint32_t pi, uint32_t& poff_smem) -> const int32_t* {
+        const uint32_t pid = a.pat_ids[pi];
+        const uint32_t po = a.prog_off[pid], pn = a.prog_off[pid + 1] - po;
+        const int32_t* pg = progs_smem ? sprog + poff_smem : a.prog + po;
+        poff_smem += pn;
+        return pg;
+    };
+    auto set_prog = [&](const int32_t* pg) {
+        m.prog = pg;
+        m.P = pg[0]; m.V = pg[1]; m.Q = pg[2];
+    };
+    // root-operator filter bit (0 = no filtering: root is a variable or the name id is large)
+    auto root_bit = [&]() -> uint32_t {
+        const uint32_t rname = (uint32_t)m.prog[3 + 1];
+        return (cmask && m.prog[3] == 1 && rname < 32) ? (1u << rname) : 0u;
+    };
 
-    if (a.mode == 1) {  // existence only
-        uint32_t any = 0;
-        for (uint32_t r = c_lo; r < c_hi && !any; r++) any = match_class(m, r, true, nothing);
-        any = __syncthreads_or(any);
-        if (tid == 0) { a.count[(uint64_t)pi * L + l] = any ? 1u : 0u; a.off[(uint64_t)pi * L + l] = 0; }
+    if (a.mode == 1) {  // existence only (is_rule_applicable, rewrite.py:579-589)
+        uint32_t po = 0;
+        for (uint32_t pi = 0; pi < a.P; pi++) {
+            set_prog(prog_of(pi, po));
+            const uint32_t rbit = root_bit();
+            uint32_t any = 0;
+            for (uint32_t r = c_lo; r < c_hi && !any; r++)
+                if (!rbit || (cmask[r] & rbit)) any = match_class(m, r, true, nothing);
+            any = __syncthreads_or(any);
+            if (tid == 0) { a.count[(uint64_t)pi * L + l] = any ? 1u : 0u; a.off[(uint64_t)pi * L + l] = 0; }
+        }
         return;
     }
-    // pass 1: raw counts
-    uint32_t raw = 0;
-    for (uint32_t r = c_lo; r < c_hi; r++) raw += match_class(m, r, false, nothing);
-    uint32_t tot;
-    const uint32_t pre = block_exscan(raw, sh_scan, &tot);
+    // phase 1: raw match counts of every pattern (per thread, kept in a global scratch row so the
+    // fill phase can re-derive its placement; totals in SMEM)
+    uint32_t* raw = a.raw + ((uint64_t)l * MAXP) * T + tid;   // raw[pi * T]
+#define RAW(pi) raw[(uint64_t)(pi) * T]
+    {
+        uint32_t po = 0;
+        for (uint32_t pi = 0; pi < a.P; pi++) {
+            set_prog(prog_of(pi, po));
+            const uint32_t rbit = root_bit();
+            uint32_t n = 0;
+            for (uint32_t r = c_lo; r < c_hi; r++)
+                if (!rbit || (cmask[r] & rbit)) n += match_class(m, r, false, nothing);
+            RAW(pi) = n;
+#ifdef ESAT_DEBUG
+            if (l == 0 && pi == 0 && n) printf("phase1 leaf0 pat0 tid %u n %u raw %u P %d V %d Q %d\n", tid, n, RAW(pi), m.P, m.V, m.Q);
+#endif
+            const uint32_t t = __reduce_add_sync(0xffffffffu, n);
+            if (pi < MAXP && lane_id() == 0) atomicAdd(&sh_tot[pi], t);
+        }
+    }
+    (void)sh_scan;
+    __syncthreads();
+    // phase 2: one output allocation for the whole leaf (all patterns)
     if (tid == 0) {
-        unsigned long long base = atomicAdd(&a.tops[0], (unsigned long long)tot * W);
-        if (base + (unsigned long long)tot * W > a.stage_cap) { atomicOr(a.overflow, 1u); base = ~0ull; }
-        sh_base = base;
+        unsigned long long words = 0;
+        uint32_t po = 0;
+        for (uint32_t pi = 0; pi < a.P; pi++) {
+            const int32_t* pg = prog_of(pi, po);
+            sh_pbase[pi] = words;
+            words += (unsigned long long)sh_tot[pi] * (1 + pg[1] + pg[2]);
+        }
+        unsigned long long base = atomicAdd(&a.tops[1], words);
+        if (base + words > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+        for (uint32_t pi = 0; pi < a.P; pi++) sh_pbase[pi] = base == ~0ull ? ~0ull : base + sh_pbase[pi];
     }
     __syncthreads();
-    const unsigned long long sbase = sh_base;
-    uint32_t uniq = 0;
-    uint32_t* mine = a.stage + (sbase == ~0ull ? 0 : sbase) + (uint64_t)pre * W;
-    if (sbase != ~0ull) {
+    // phase 3: fill each pattern's records in place, sort + dedup per root class
+    uint32_t po = 0;
+    for (uint32_t pi = 0; pi < a.P; pi++) {
+        set_prog(prog_of(pi, po));
+        const uint32_t W = 1 + m.V + m.Q;
+        const uint64_t oi = (uint64_t)pi * L + l;
+        const unsigned long long pbase = sh_pbase[pi];
+        const uint32_t tot = sh_tot[pi];
+        if (pbase == ~0ull || tot == 0) {
+            if (tid == 0) { a.count[oi] = pbase == ~0ull ? 0 : tot; a.off[oi] = pbase == ~0ull ? 0 : pbase; }
+            continue;
+        }
+        uint32_t dummy;
+        const uint32_t pre = block_exscan(RAW(pi), sh_scan, &dummy);
+#ifdef ESAT_DEBUG
+        if (l == 0 && pi == 0 && RAW(pi)) printf("phase3 leaf0 pat0 tid %u raw %u pre %u P %d V %d Q %d\n", tid, RAW(pi), pre, m.P, m.V, m.Q);
+#endif
+        const uint32_t rbit = root_bit();
+        uint32_t* mine = a.out + pbase + (uint64_t)pre * W;
         uint32_t cur = 0;
         for (uint32_t r = c_lo; r < c_hi; r++) {
+            if (rbit && !(cmask[r] & rbit)) continue;
             const uint32_t seg = cur;
             match_class(m, r, false, [&](uint32_t root, const uint32_t* vars, const int32_t* pv) {
                 uint32_t* o = mine + (uint64_t)cur * W;
+#ifdef ESAT_DEBUG
+                if (cur >= RAW(pi) || pre + cur >= tot) {
+                    printf("k_ematch OOB leaf %u pat %u tid %u cur %u raw %u pre %u tot %u\n", l, pi, tid, cur,
+                           RAW(pi), pre, tot);
+                    __trap();
+                }
+#endif
                 o[0] = root;
                 for (int v = 0; v < m.V; v++) o[1 + v] = vars[v];
                 for (int q = 0; q < m.Q; q++) o[1 + m.V + q] = (uint32_t)pv[q];
                 cur++;
             });
-            cur = seg + sort_unique(mine + (uint64_t)seg * W, cur - seg, W);
+            if (cur - seg > 1) cur = seg + sort_unique(mine + (uint64_t)seg * W, cur - seg, W);
         }
-        uniq = cur;
-    }
-    const uint32_t upre = block_exscan(uniq, sh_scan, &tot);
-    if (tid == 0) {
-        unsigned long long base = ~0ull;
-        if (sbase != ~0ull) {
-            base = atomicAdd(&a.tops[1], (unsigned long long)tot * W);
-            if (base + (unsigned long long)tot * W > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+        const bool dup = cur != RAW(pi);
+        if (__syncthreads_or(dup)) {
+            // rare: duplicates (two e-nodes of a class giving the same binding) -> compact the
+            // unique records through the staging buffer, keeping per-thread order
+            uint32_t utot;
+            const uint32_t upre = block_exscan(cur, sh_scan, &utot);
+            if (tid == 0) {
+                unsigned long long sb = atomicAdd(&a.tops[0], (unsigned long long)utot * W);
+                if (sb + (unsigned long long)utot * W > a.stage_cap) { atomicOr(a.overflow, 1u); sb = ~0ull; }
+                sh_base = sb;
+            }
+            __syncthreads();
+            const unsigned long long sb = sh_base;
+            if (sb != ~0ull)
+                for (uint64_t w = 0; w < (uint64_t)cur * W; w++) a.stage[sb + (uint64_t)upre * W + w] = mine[w];
+            __syncthreads();
+            if (sb != ~0ull)
+                for (uint64_t w = tid; w < (uint64_t)utot * W; w += T) a.out[pbase + w] = a.stage[sb + w];
+            if (tid == 0) { a.count[oi] = utot; a.off[oi] = pbase; }
+            __syncthreads();
+        } else if (tid == 0) {
+            a.count[oi] = tot;
+            a.off[oi] = pbase;
         }
-        sh_base = base;
-        a.count[(uint64_t)pi * L + l] = tot;
-        a.off[(uint64_t)pi * L + l] = base == ~0ull ? 0 : base;
     }
-    __syncthreads();
-    if (sh_base != ~0ull)
-        for (uint64_t w = 0; w < (uint64_t)uniq * W; w++) a.out[sh_base + (uint64_t)upre * W + w] = mine[w];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -448,15 +595,72 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     __shared__ JoinPlan sh_plan;
     if (indexed && tid == 0) make_plan(sh_plan, src, NV, NQ);
     __syncthreads();
+    if (indexed) {
+        // ---- warp-cooperative sort-join: a warp owns whole root groups of source 0; the lanes
+        // walk the index run of each source-0 record 32 products at a time, compact consistent
+        // products with a ballot and write consecutive records (coalesced across the warp). ----
+        constexpr uint32_t NW = T / 32;
+        __shared__ uint32_t sh_wcnt[NW], sh_wpre[NW];
+        const uint32_t warp = tid >> 5, lane = tid & 31;
+        const uint32_t n0 = src[0].n, n1 = src[1].n, chw = (n0 + NW - 1) / NW;
+        const uint32_t wlo = group_start_at_or_after(src[0], min(n0, warp * chw));
+        const uint32_t whi = group_start_at_or_after(src[0], min(n0, (warp + 1) * chw));
+        const JoinPlan& jp = sh_plan;
+        auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
+            uint32_t n = 0;
+            for (uint32_t g = wlo; g < whi;) {
+                const uint32_t ge = group_end(src[0], g);
+                const uint32_t gstart = n;
+                for (uint32_t i = g; i < ge; i++) {
+                    const uint32_t* m1 = w0 + (uint64_t)i * W0;
+                    const uint32_t x = m1[1 + v0];
+                    const uint32_t p0 = lower_bound_key(sh_keys, n1, (unsigned long long)x << 32);
+                    const uint32_t p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
+                    for (uint32_t base = p0; base < p1; base += 32) {
+                        const uint32_t p = base + lane;
+                        bool ok = p < p1;
+                        const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)sh_keys[p] * W1 : w1;
+                        for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1[jp.c0[c]] == m2[jp.c1[c]];
+                        const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+                        if (out && ok) {
+                            uint32_t* o = out + (uint64_t)(n + __popc(mask & ((1u << lane) - 1u))) * W;
+                            for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.idx[w]] : m1[jp.idx[w]];
+                        }
+                        n += __popc(mask);
+                    }
+                }
+                if (out && ge - g > 1) {   // several source-0 records share the root: sort the group
+                    __syncwarp();
+                    if (lane == 0) sort_unique(out + (uint64_t)gstart * W, n - gstart, W);
+                    __syncwarp();
+                }
+                g = ge;
+            }
+            return n;
+        };
+        const uint32_t wc = walk(nullptr);
+        if (lane == 0) sh_wcnt[warp] = wc;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t acc = 0;
+            for (uint32_t w = 0; w < NW; w++) { sh_wpre[w] = acc; acc += sh_wcnt[w]; }
+            unsigned long long base = atomicAdd(&a.tops[1], (unsigned long long)acc * W);
+            if (base + (unsigned long long)acc * W > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+            sh_base = base;
+            a.count[(uint64_t)r * L + l] = acc;
+            a.off[(uint64_t)r * L + l] = base == ~0ull ? 0 : base;
+        }
+        __syncthreads();
+        if (sh_base != ~0ull) walk(a.out + sh_base + (uint64_t)sh_wpre[warp] * W);
+        return;
+    }
     auto count_only = [](const uint32_t*) {};
     uint32_t cnt = 0;
     for (uint32_t g = g_lo; g < g_hi;) {
         const uint32_t ge = group_end(src[0], g);
-        if (indexed) cnt += indexed_products(w0, W0, w1, W1, sh_plan, g, ge, v0, sh_keys, src[1].n, nullptr);
-        else
-            for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
-                cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
-            });
+        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
+            cnt += block_products(src, S, lo, hi, NV, NQ, count_only);
+        });
         g = ge;
     }
     uint32_t tot;
@@ -474,22 +678,15 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     uint32_t cur = 0;
     for (uint32_t g = g_lo; g < g_hi;) {
         const uint32_t ge = group_end(src[0], g);
-        if (indexed) {
-            // one root group of source 0: runs per record are sorted; sort the group's union
+        for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
             const uint32_t start = cur;
-            cur += indexed_products(w0, W0, w1, W1, sh_plan, g, ge, v0, sh_keys, src[1].n, out + (uint64_t)cur * W);
-            if (ge - g > 1) sort_unique(out + (uint64_t)start * W, cur - start, W);
-        } else {
-            for_blocks(src, S, g, ge, [&](const uint32_t* lo, const uint32_t* hi) {
-                const uint32_t start = cur;
-                block_products(src, S, lo, hi, NV, NQ, [&](const uint32_t* rr) {
-                    for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
-                    cur++;
-                });
-                // products of one block share the roots prefix; distinct pairs give distinct keys
-                sort_unique(out + (uint64_t)start * W, cur - start, W);
+            block_products(src, S, lo, hi, NV, NQ, [&](const uint32_t* rr) {
+                for (uint32_t w = 0; w < W; w++) out[(uint64_t)cur * W + w] = rr[w];
+                cur++;
             });
-        }
+            // products of one block share the roots prefix; distinct pairs give distinct keys
+            sort_unique(out + (uint64_t)start * W, cur - start, W);
+        });
         g = ge;
     }
 }

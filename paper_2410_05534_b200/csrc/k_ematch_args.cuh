@@ -23,6 +23,8 @@ struct MArgs {
     uint32_t* count;            // [P][L]
     uint64_t* off;              // [P][L] word offsets into out
     uint32_t* overflow;
+    uint32_t smem_bytes;        // dynamic shared memory for staging one leaf's view
+    uint32_t* raw;              // [L][32][T] per-thread raw match counts (count -> fill placement)
 };
 
 struct JArgs {

@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
-LIB_PATH = LIB_DIR / "libesat_b200.so"
+LIB_PATH = LIB_DIR / ("libesat_b200_debug.so" if os.environ.get("ESAT_DEBUG_LIB") else "libesat_b200.so")
 NONE = 0xFFFFFFFF
 
 OK, E_ARG, E_CUDA, E_CAPACITY, E_STATE = 0, 1, 2, 3, 4
