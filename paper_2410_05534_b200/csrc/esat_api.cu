@@ -502,7 +502,7 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
     b->m_P = P;
-    if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * L * 32 * 128));
+    if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts
     if (!b->stage_cap) {
         if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
         if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
@@ -521,7 +521,7 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
         uint64_t mx = 0;
         for (uint64_t l = 0; l < L; l++) {
             const uint64_t n = b->nb[l + 1] - b->nb[l], k = b->kb[l + 1] - b->kb[l];
-            const uint64_t bytes = 4 * (4 * n + 2 + k) + 5 * 32 + 4 * n + 32;   // view + class op masks
+            const uint64_t bytes = 4 * (2 * n + 1) + 2 * 32 + 4 * n + 32;   // cls_off + nd_sym + class op masks
             mx = bytes > mx ? bytes : mx;
         }
         const uint32_t cap_bytes = 100 * 1024;

@@ -179,9 +179,9 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     const uint32_t K = g_nd_koff[N];
     const uint32_t* g_nd_kpos = d.nd_kpos + d.kb[l];
     Matcher m;
-    const uint32_t need = staged_bytes_u32(g_cls_id, C) + staged_bytes_u32(g_cls_off, C + 1) +
-                          staged_bytes_u32(g_nd_sym, N) + staged_bytes_u32(g_nd_koff, N + 1) +
-                          staged_bytes_u32(g_nd_kpos, K);
+    // stage the hot part of the view (class node ranges + node symbols) with TMA bulk copies
+    const uint32_t need = staged_bytes_u32(g_cls_off, C + 1) + staged_bytes_u32(g_nd_sym, N);
+    m.cls_id = g_cls_id; m.nd_koff = g_nd_koff; m.nd_kpos = g_nd_kpos;
     if (need <= a.smem_bytes) {
         if (tid == 0) mbar_init(&bar, 1);
         __syncthreads();
@@ -189,13 +189,10 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         uint32_t tx = 0;
         const bool issuer = tid == 0;
         if (issuer) mbar_arrive_expect_tx(&bar, need);
-        m.cls_id = stage_u32(g_cls_id, C, &cur, &bar, &tx, issuer);
         m.cls_off = stage_u32(g_cls_off, C + 1, &cur, &bar, &tx, issuer);
         m.nd_sym = stage_u32(g_nd_sym, N, &cur, &bar, &tx, issuer);
-        m.nd_koff = stage_u32(g_nd_koff, N + 1, &cur, &bar, &tx, issuer);
-        m.nd_kpos = stage_u32(g_nd_kpos, K, &cur, &bar, &tx, issuer);
     } else {
-        m.cls_id = g_cls_id; m.cls_off = g_cls_off; m.nd_sym = g_nd_sym; m.nd_koff = g_nd_koff; m.nd_kpos = g_nd_kpos;
+        m.cls_off = g_cls_off; m.nd_sym = g_nd_sym;
     }
     // symbol table (name, arity, attribute CSR) in shared memory when it fits
     const uint32_t ns = d.n_syms, npar = d.sym_poff[ns];
@@ -273,105 +270,130 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         }
         return;
     }
-    // phase 1: raw match counts of every pattern (per thread, kept in a global scratch row so the
-    // fill phase can re-derive its placement; totals in SMEM)
-    uint32_t* raw = a.raw + ((uint64_t)l * MAXP) * T + tid;   // raw[pi * T]
-#define RAW(pi) raw[(uint64_t)(pi) * T]
-    {
+    // ---- LIST mode: balanced (pattern, class) work over the flattened index space ----
+    // pass 1 counts raw matches of every (pattern, root class) pair into a per-leaf scratch row;
+    // a segmented scan turns them into record offsets (pattern-major, class order = the
+    // reference's sort order by root); pass 2 writes each pair's records at its offset and
+    // sorts + dedups them in place (rewrite.py:420-433).
+    __shared__ uint32_t sp_off[MAXP], sp_W[MAXP], sp_rbit[MAXP], sp_dup[MAXP];
+    __shared__ uint32_t sp_rbase[MAXP + 1];
+    __shared__ unsigned long long sp_wbase[MAXP];
+    const uint32_t P = a.P;
+    if (tid == 0) {
         uint32_t po = 0;
-        for (uint32_t pi = 0; pi < a.P; pi++) {
-            set_prog(prog_of(pi, po));
-            const uint32_t rbit = root_bit();
-            uint32_t n = 0;
-            for (uint32_t r = c_lo; r < c_hi; r++)
-                if (!rbit || (cmask[r] & rbit)) n += match_class(m, r, false, nothing);
-            RAW(pi) = n;
-#ifdef ESAT_DEBUG
-            if (l == 0 && pi == 0 && n) printf("phase1 leaf0 pat0 tid %u n %u raw %u P %d V %d Q %d\n", tid, n, RAW(pi), m.P, m.V, m.Q);
-#endif
-            const uint32_t t = __reduce_add_sync(0xffffffffu, n);
-            if (pi < MAXP && lane_id() == 0) atomicAdd(&sh_tot[pi], t);
+        for (uint32_t pi = 0; pi < P; pi++) {
+            const uint32_t pid = a.pat_ids[pi];
+            const int32_t* pg = progs_smem ? sprog + po : a.prog + a.prog_off[pid];
+            sp_off[pi] = progs_smem ? po : a.prog_off[pid];
+            po += a.prog_off[pid + 1] - a.prog_off[pid];
+            sp_W[pi] = 1 + pg[1] + pg[2];
+            const uint32_t rname = (uint32_t)pg[3 + 1];
+            sp_rbit[pi] = (cmask && pg[3] == 1 && rname < 32) ? (1u << rname) : 0u;
+            sp_dup[pi] = 0;
         }
     }
-    (void)sh_scan;
     __syncthreads();
-    // phase 2: one output allocation for the whole leaf (all patterns)
-    if (tid == 0) {
+    auto prog_ptr = [&](uint32_t pi) -> const int32_t* { return (progs_smem ? sprog : a.prog) + sp_off[pi]; };
+    const uint32_t PC = P * C;
+    uint32_t* pc = a.raw + d.nb[l] * MAXP;   // [P][C] counts -> offsets (C <= n, P <= 32)
+    for (uint32_t i = tid; i < PC; i += T) {
+        const uint32_t pi = i / C, r = i - pi * C;
+        uint32_t n = 0;
+        const uint32_t rb = sp_rbit[pi];
+        if (!rb || (cmask[r] & rb)) {
+            set_prog(prog_ptr(pi));
+            n = match_class(m, r, false, nothing);
+        }
+        pc[i] = n;
+    }
+    __syncthreads();
+    // exclusive scan of pc in place: each warp owns a contiguous quarter and walks it 32 elements at
+    // a time (coalesced) with shuffle scans; pass A sums, pass B writes prefixes
+    {
+        constexpr uint32_t NW = T / 32;
+        __shared__ uint32_t sh_wsum[NW];
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+        const uint32_t qw = (PC + NW - 1) / NW, lo = min(PC, warp * qw), hi = min(PC, lo + qw);
+        uint32_t sum = 0;
+        for (uint32_t i = lo + lane; i < hi; i += 32) sum += pc[i];
+        sum = __reduce_add_sync(0xffffffffu, sum);
+        if (lane == 0) sh_wsum[warp] = sum;
+        __syncthreads();
+        uint32_t carry = 0, total = 0;
+        for (uint32_t w = 0; w < NW; w++) { if (w < warp) carry += sh_wsum[w]; total += sh_wsum[w]; }
+        for (uint32_t b0 = lo; b0 < hi; b0 += 32) {
+            const uint32_t i = b0 + lane;
+            const uint32_t v = i < hi ? pc[i] : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (i < hi) pc[i] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        __syncthreads();
+        if (tid <= P) sp_rbase[tid] = (tid < P && C) ? pc[tid * C] : (tid == P ? total : 0u);
+        __syncthreads();
+    }
+    if (tid == 0) {   // one output allocation for the whole leaf
         unsigned long long words = 0;
-        uint32_t po = 0;
-        for (uint32_t pi = 0; pi < a.P; pi++) {
-            const int32_t* pg = prog_of(pi, po);
-            sh_pbase[pi] = words;
-            words += (unsigned long long)sh_tot[pi] * (1 + pg[1] + pg[2]);
+        for (uint32_t pi = 0; pi < P; pi++) {
+            sp_wbase[pi] = words;
+            words += (unsigned long long)(sp_rbase[pi + 1] - sp_rbase[pi]) * sp_W[pi];
         }
         unsigned long long base = atomicAdd(&a.tops[1], words);
         if (base + words > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
-        for (uint32_t pi = 0; pi < a.P; pi++) sh_pbase[pi] = base == ~0ull ? ~0ull : base + sh_pbase[pi];
+        sh_base = base;
+        for (uint32_t pi = 0; pi < P; pi++) sp_wbase[pi] = base == ~0ull ? ~0ull : base + sp_wbase[pi];
     }
     __syncthreads();
-    // phase 3: fill each pattern's records in place, sort + dedup per root class
-    uint32_t po = 0;
-    for (uint32_t pi = 0; pi < a.P; pi++) {
-        set_prog(prog_of(pi, po));
-        const uint32_t W = 1 + m.V + m.Q;
-        const uint64_t oi = (uint64_t)pi * L + l;
-        const unsigned long long pbase = sh_pbase[pi];
-        const uint32_t tot = sh_tot[pi];
-        if (pbase == ~0ull || tot == 0) {
-            if (tid == 0) { a.count[oi] = pbase == ~0ull ? 0 : tot; a.off[oi] = pbase == ~0ull ? 0 : pbase; }
-            continue;
-        }
-        uint32_t dummy;
-        const uint32_t pre = block_exscan(RAW(pi), sh_scan, &dummy);
-#ifdef ESAT_DEBUG
-        if (l == 0 && pi == 0 && RAW(pi)) printf("phase3 leaf0 pat0 tid %u raw %u pre %u P %d V %d Q %d\n", tid, RAW(pi), pre, m.P, m.V, m.Q);
-#endif
-        const uint32_t rbit = root_bit();
-        uint32_t* mine = a.out + pbase + (uint64_t)pre * W;
-        uint32_t cur = 0;
-        for (uint32_t r = c_lo; r < c_hi; r++) {
-            if (rbit && !(cmask[r] & rbit)) continue;
-            const uint32_t seg = cur;
+    if (sh_base != ~0ull) {
+        const uint32_t grand = sp_rbase[P];
+        for (uint32_t i = tid; i < PC; i += T) {
+            const uint32_t beg = pc[i], end = (i + 1 < PC) ? pc[i + 1] : grand;
+            if (beg == end) continue;
+            const uint32_t pi = i / C, r = i - pi * C, W = sp_W[pi];
+            set_prog(prog_ptr(pi));
+            uint32_t* o0 = a.out + sp_wbase[pi] + (uint64_t)(beg - sp_rbase[pi]) * W;
+            uint32_t cur = 0;
             match_class(m, r, false, [&](uint32_t root, const uint32_t* vars, const int32_t* pv) {
-                uint32_t* o = mine + (uint64_t)cur * W;
-#ifdef ESAT_DEBUG
-                if (cur >= RAW(pi) || pre + cur >= tot) {
-                    printf("k_ematch OOB leaf %u pat %u tid %u cur %u raw %u pre %u tot %u\n", l, pi, tid, cur,
-                           RAW(pi), pre, tot);
-                    __trap();
-                }
-#endif
+                uint32_t* o = o0 + (uint64_t)cur * W;
                 o[0] = root;
                 for (int v = 0; v < m.V; v++) o[1 + v] = vars[v];
                 for (int q = 0; q < m.Q; q++) o[1 + m.V + q] = (uint32_t)pv[q];
                 cur++;
             });
-            if (cur - seg > 1) cur = seg + sort_unique(mine + (uint64_t)seg * W, cur - seg, W);
-        }
-        const bool dup = cur != RAW(pi);
-        if (__syncthreads_or(dup)) {
-            // rare: duplicates (two e-nodes of a class giving the same binding) -> compact the
-            // unique records through the staging buffer, keeping per-thread order
-            uint32_t utot;
-            const uint32_t upre = block_exscan(cur, sh_scan, &utot);
-            if (tid == 0) {
-                unsigned long long sb = atomicAdd(&a.tops[0], (unsigned long long)utot * W);
-                if (sb + (unsigned long long)utot * W > a.stage_cap) { atomicOr(a.overflow, 1u); sb = ~0ull; }
-                sh_base = sb;
+            if (cur > 1) {
+                const uint32_t u = sort_unique(o0, cur, W);
+                if (u != cur) {   // duplicate bindings from different e-nodes: mark the gap
+                    for (uint32_t w = u * W; w < cur * W; w++) o0[w] = NONE;
+                    atomicOr(&sp_dup[pi], 1u);
+                }
             }
-            __syncthreads();
-            const unsigned long long sb = sh_base;
-            if (sb != ~0ull)
-                for (uint64_t w = 0; w < (uint64_t)cur * W; w++) a.stage[sb + (uint64_t)upre * W + w] = mine[w];
-            __syncthreads();
-            if (sb != ~0ull)
-                for (uint64_t w = tid; w < (uint64_t)utot * W; w += T) a.out[pbase + w] = a.stage[sb + w];
-            if (tid == 0) { a.count[oi] = utot; a.off[oi] = pbase; }
-            __syncthreads();
-        } else if (tid == 0) {
-            a.count[oi] = tot;
-            a.off[oi] = pbase;
         }
+    }
+    __syncthreads();
+    if (tid < P) {
+        const uint32_t pi = tid;
+        const uint64_t oi = (uint64_t)pi * L + l;
+        uint32_t tot = sp_rbase[pi + 1] - sp_rbase[pi];
+        if (sh_base != ~0ull && sp_dup[pi]) {
+            // rare: squeeze out the gaps left by deduplicated slices (left-to-right, in order)
+            const uint32_t W = sp_W[pi];
+            uint32_t* base = a.out + sp_wbase[pi];
+            uint32_t o = 0;
+            for (uint32_t rr = 0; rr < tot; rr++)
+                if (base[(uint64_t)rr * W] != NONE) {
+                    if (o != rr)
+                        for (uint32_t w = 0; w < W; w++) base[(uint64_t)o * W + w] = base[(uint64_t)rr * W + w];
+                    o++;
+                }
+            tot = o;
+        }
+        a.count[oi] = sh_base == ~0ull ? 0 : tot;
+        a.off[oi] = sh_base == ~0ull ? 0 : sp_wbase[pi];
     }
 }
 
