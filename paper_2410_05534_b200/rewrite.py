@@ -1,0 +1,183 @@
+"""Rewrite engine with the reference's API (rewrite.py); matching runs on the B200.
+
+`ematch`, `joint_match` and `is_rule_applicable` execute `k_ematch`/`k_join` through
+`device.py` and return the reference's ordered, deduplicated `Substitution` list
+(rewrite.py:396-433). `apply_rule` keeps the reference's sequential instantiate /
+cycle-filter / shape-filter / union loop on the host (rewrite.py:526-573; the device apply
+loop is the next §8 row) and ends with the device rebuild.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import device
+from .egraph import EGraph, ENode, StructuralError
+from .patterns import (App, PVar, Rule, RuleSyntaxError, UnboundVariableError, Var, load_rules,  # noqa: F401
+                       parse_pattern, parse_rule, parse_rules, pattern_pvars, pattern_vars, print_pattern,
+                       print_rule)
+from .tensor_ir import InstantiationError, Language, TermLanguage  # noqa: F401
+
+_TERM = TermLanguage()
+
+
+def _lang(egraph, language):
+    return language or egraph.language or _TERM
+
+
+@dataclass(frozen=True)
+class Substitution:
+    vars: tuple
+    params: tuple
+    roots: tuple = ()
+
+    def var(self, name: str) -> int:
+        return dict(self.vars)[name]
+
+    def param(self, name: str):
+        return dict(self.params)[name]
+
+
+def joint_match(egraph: EGraph, patterns: list, language=None) -> list:
+    """All substitutions of `patterns` (threaded bindings), sorted by (roots, vars, params)."""
+    if egraph.dirty:
+        raise StructuralError("ematch requires a rebuilt e-graph")
+    recs, vn, qn, S = device.joint_match(egraph, list(patterns), language)
+    values = device.session().symtab.values
+    nv = len(vn)
+    out = []
+    for r in recs.tolist():
+        out.append(Substitution(tuple(zip(vn, r[S:S + nv])),
+                                tuple((q, values[c]) for q, c in zip(qn, r[S + nv:])), tuple(r[:S])))
+    return out
+
+
+def ematch(egraph: EGraph, pattern, language=None) -> list:
+    return joint_match(egraph, [pattern], language)
+
+
+def is_rule_applicable(egraph: EGraph, rule: Rule, language=None) -> bool:
+    """False guarantees apply_rule reports changed=False (rewrite.py:579-589): EXISTS-mode
+    e-match of every source independently."""
+    if egraph.dirty:
+        raise StructuralError("ematch requires a rebuilt e-graph")
+    return all(device.any_match(egraph, s) for s in rule.sources)
+
+
+@dataclass
+class ApplyReport:
+    rule_id: int
+    matches_found: int = 0
+    changed: bool = False
+    nodes_after: int = 0
+    classes_after: int = 0
+    hit_node_limit: bool = False
+    cycles_filtered: int = 0
+    shape_filtered: int = 0
+
+
+def _params(pat, sub) -> tuple:
+    if pat.params is None:
+        return ()
+    return tuple(sub.param(s.name) if isinstance(s, PVar) else s for s in pat.params)
+
+
+def _refs(eg, lang, pat, sub):
+    """(classes the instance would reference, existing class of the full instance or None)."""
+    if isinstance(pat, Var):
+        c = eg.find(sub.var(pat.name))
+        return {c}, c
+    refs, kids, complete = set(), [], True
+    for ch in pat.children:
+        r, c = _refs(eg, lang, ch, sub)
+        refs |= r
+        if c is None:
+            complete = False
+        else:
+            kids.append(c)
+    if complete:
+        sym = lang.make_symbol(pat.name, _params(pat, sub), tuple(lang.class_shape(eg, c) for c in kids))
+        hit = eg.hashcons.get(eg.canonicalize(ENode(sym, tuple(kids))))
+        if hit is not None:
+            return {eg.find(hit)}, eg.find(hit)
+    return refs, None
+
+
+def would_create_cycle(egraph: EGraph, children, matched_root: int) -> bool:
+    """True iff matched_root is reachable from any candidate child (rewrite.py:488-505)."""
+    goal = egraph.find(matched_root)
+    todo = [egraph.find(c) for c in children]
+    seen = set()
+    while todo:
+        c = todo.pop()
+        if c == goal:
+            return True
+        if c in seen:
+            continue
+        seen.add(c)
+        for node in egraph.classes[c].nodes:
+            todo.extend(egraph.find(x) for x in node.children)
+    return False
+
+
+def _shape(eg, lang, pat, sub):
+    if isinstance(pat, Var):
+        return lang.class_shape(eg, eg.find(sub.var(pat.name)))
+    shapes = tuple(_shape(eg, lang, c, sub) for c in pat.children)
+    return lang.symbol_shape(lang.make_symbol(pat.name, _params(pat, sub), shapes))
+
+
+def _instantiate(eg, lang, pat, sub) -> int:
+    if isinstance(pat, Var):
+        return eg.find(sub.var(pat.name))
+    kids = tuple(_instantiate(eg, lang, c, sub) for c in pat.children)
+    sym = lang.make_symbol(pat.name, _params(pat, sub), tuple(lang.class_shape(eg, c) for c in kids))
+    return eg.add(ENode(sym, kids))
+
+
+def apply_rule(egraph: EGraph, rule: Rule, node_limit: int = 0, language=None) -> ApplyReport:
+    """Apply every match of `rule`, union targets with matched classes, rebuild (rewrite.py:526-573)."""
+    lang = _lang(egraph, language)
+    if node_limit:
+        n = egraph.size()[0]
+        if n >= node_limit:
+            raise StructuralError(f"node limit {node_limit} not above current node count {n}")
+    rep = ApplyReport(rule_id=rule.id)
+    subs = joint_match(egraph, rule.sources, lang)
+    rep.matches_found = len(subs)
+    before = egraph.version
+    for sub in subs:
+        for k, tgt in enumerate(rule.targets):
+            root = egraph.find(sub.roots[k])
+            try:
+                refs, existing = _refs(egraph, lang, tgt, sub)
+            except InstantiationError:
+                rep.shape_filtered += 1
+                continue
+            if existing is not None and existing == root:
+                continue
+            if would_create_cycle(egraph, refs, root):
+                rep.cycles_filtered += 1
+                continue
+            try:
+                shape = _shape(egraph, lang, tgt, sub)
+            except InstantiationError:
+                rep.shape_filtered += 1
+                continue
+            have = lang.class_shape(egraph, root)
+            if shape is not None and have is not None and shape != have:
+                rep.shape_filtered += 1
+                continue
+            egraph.union(_instantiate(egraph, lang, tgt, sub), root)
+    egraph.rebuild()
+    rep.changed = egraph.version != before
+    rep.nodes_after, rep.classes_after = egraph.size()
+    rep.hit_node_limit = bool(node_limit) and rep.nodes_after >= node_limit
+    return rep
+
+
+def is_saturated(egraph: EGraph, rules: list, node_limit: int = 0, language=None) -> bool:
+    for r in rules:
+        if apply_rule(egraph.snapshot(), r, 0, language).changed:
+            return False
+    return True
