@@ -222,7 +222,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=4096, help="leaves per rank per step")
-    ap.add_argument("--model", default="nasrnn")
+    ap.add_argument("--model", default="nasrnn",
+                    choices=["nasrnn", "bert", "resnext50", "inception_v3", "nasnet_a"],
+                    help="leaf set: configs[1] NasRNN by default; the other BASELINE analogs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -61,6 +61,10 @@ struct XArgs {
     uint64_t pool_stride;        // offset of parity 1
     uint32_t *hoff, *hlen;       // [2][node rows] history slot per class position (pass parity)
     uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip)
+    uint8_t* need;               // [node rows] class needs re-evaluation in the current pass
+    uint32_t *lnode, *lcls, *lvn; // e-nodes in level order, their classes, level ends (node-parallel phase)
+    double* nval;                // [node rows] node cost of the current pass
+    uint32_t* naux;              // [2][node rows] generic-arity node history (offset, length)
     uint64_t slot_stride;
 };
 
