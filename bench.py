@@ -144,7 +144,7 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def algorithmic_bytes(view, packed, counts_by_rule, rules_c):
+def algorithmic_bytes(view, packed, counts_by_rule, rules_c, join_src_words=0):
     """SURVEY.md 8(d) compulsory traffic: per leaf rebuild 44N+8C, extraction 20N+20C,
     e-match per pattern 16N+8C+4*M*W (N live e-nodes, C classes, M matches, W words)."""
     L = packed["n_leaves"]
@@ -156,10 +156,15 @@ def algorithmic_bytes(view, packed, counts_by_rule, rules_c):
     b_extract = int(np.sum(20 * N + 20 * C))
     n_pat = sum(len(r.pattern_ids) for r in rules_c)
     b_ematch = int(n_pat * np.sum(16 * N + 8 * C))
+    b_join = 0
     for r, cnt in zip(rules_c, counts_by_rule):
         W = len(r.pattern_ids) + len(r.var_names) + len(r.pvar_names)
-        b_ematch += int(4 * W * int(cnt.sum()))
-    return {"rebuild": b_rebuild, "ematch": b_ematch, "extract": b_extract}
+        if r.multi:   # join: read the source match lists, write the joined records
+            b_join += int(4 * W * int(cnt.sum()))
+        else:
+            b_ematch += int(4 * W * int(cnt.sum()))
+    b_join += 4 * int(join_src_words)   # the joins read their sources' match lists
+    return {"rebuild": b_rebuild, "ematch": b_ematch, "join": b_join, "extract": b_extract}
 
 
 def cpu_baseline(leaves, symarr, rules_c, budget_s: float = 15.0, threads: int = 0):
@@ -169,9 +174,9 @@ def cpu_baseline(leaves, symarr, rules_c, budget_s: float = 15.0, threads: int =
 
     threads = threads or len(os.sched_getaffinity(0))
     done, t_total, reps = 0, 0.0, 0
-    sample = min(len(leaves), max(threads * 4, 32))
+    sample = len(leaves)                      # every distinct reference leaf of the workload
     packed = Batch(leaves[:sample]).pack()
-    while t_total < budget_s and reps < 50:
+    while t_total < budget_s and reps < 1000:
         t0 = time.perf_counter()
         O.pipeline(packed, symarr, rules_c, "ocf", threads)
         t_total += time.perf_counter() - t0
@@ -194,7 +199,7 @@ def run_reference(args):
     from paper_2410_05534_b200.arena import Batch
 
     threads = len(os.sched_getaffinity(0))
-    sample = min(len(leaves), max(threads * 4, 32))
+    sample = len(leaves)                      # every distinct reference leaf per step
     packed = Batch(leaves[:sample]).pack()
     for _ in range(args.warmup):
         O.pipeline(packed, symarr, rules_c, "ocf", threads)
@@ -228,6 +233,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ocf-pool", type=float, default=128.0,
+                    help="OCF history pool entries per e-node (grown automatically if too small)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -250,7 +257,7 @@ def main():
     ctx = native.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
-    pipe = LeafPipeline(ctx, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=8.0)
+    pipe = LeafPipeline(ctx, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=args.ocf_pool)
     B = args.batch
     packed, src_idx = make_batch(leaves, B, rotate=rank * B)  # contiguous shard of the global leaf sequence
     batch = pipe.load(packed)
@@ -272,14 +279,19 @@ def main():
     view.update(batch.download_view())
     counts = pipe.match_counts()
     total_matches = int(counts.sum())
-    abytes = algorithmic_bytes(view, packed, counts, pipe.rules)
+    src_words = 0
+    for r in pipe.joins:
+        for pid, prog in zip(r.pattern_ids, r._programs):
+            _, _, c_src = batch.download_matches(pid)
+            src_words += int(c_src.sum()) * (1 + int(prog[1]) + int(prog[2]))
+    abytes = algorithmic_bytes(view, packed, counts, pipe.rules, src_words)
 
     res_cost = torch.empty(B, dtype=torch.float64, device=dev)
     res_stat = torch.empty(B, dtype=torch.int32, device=dev)
     from paper_2410_05534_b200.parallel import allgather_leaf_results
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    stage_ms = {"rebuild": 0.0, "ematch": 0.0, "extract": 0.0}
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    stage_ms = {"rebuild": 0.0, "ematch": 0.0, "join": 0.0, "extract": 0.0}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -292,10 +304,12 @@ def main():
             e[0].record(stream)
             pipe.rebuild()
             e[1].record(stream)
-            pipe.ematch()
+            pipe.match()
             e[2].record(stream)
-            pipe.extract()
+            pipe.join()
             e[3].record(stream)
+            pipe.extract()
+            e[4].record(stream)
             if world > 1:  # MCTS exchange: every rank needs every leaf's reward/cost
                 batch.copy_results(res_cost.data_ptr(), res_stat.data_ptr())
                 gath_cost, gath_stat = allgather_leaf_results(res_cost, res_stat)
@@ -305,9 +319,8 @@ def main():
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
     for e in ev:
-        stage_ms["rebuild"] += e[0].elapsed_time(e[1])
-        stage_ms["ematch"] += e[1].elapsed_time(e[2])
-        stage_ms["extract"] += e[2].elapsed_time(e[3])
+        for j, name in enumerate(("rebuild", "ematch", "join", "extract")):
+            stage_ms[name] += e[j].elapsed_time(e[j + 1])
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -378,7 +391,7 @@ def main():
         "matches_per_step": total_matches * world,
         "rebuilds_per_s": B * world / (per_stage["rebuild"] / 1e3),
         "extractions_per_s": B * world / (per_stage["extract"] / 1e3),
-        "ematch_matches_per_s": total_matches * world / (per_stage["ematch"] / 1e3),
+        "ematch_matches_per_s": total_matches * world / ((per_stage["ematch"] + per_stage["join"]) / 1e3),
         "stage_ms": per_stage,
         "parity_vs_reference": parity_ok,
         "parity_detail": {"status_nonzero": int(np.sum(ext["status"] != 0)),

@@ -77,11 +77,19 @@ class LeafPipeline:
     def rebuild(self):
         self.batch.rebuild()
 
-    def ematch(self):
+    def match(self):
+        """k_ematch: every source pattern of every rule (LIST mode)."""
         self.batch.ematch(self.pattern_ids)
+
+    def join(self):
+        """k_join: multi-pattern rules over the source match lists."""
         if self.joins:
             self.batch.join([(r.pattern_ids, r.var_maps, r.pvar_maps, len(r.var_names), len(r.pvar_names))
                              for r in self.joins])
+
+    def ematch(self):
+        self.match()
+        self.join()
 
     def extract(self):
         self.batch.extract(self.method)
