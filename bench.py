@@ -233,7 +233,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ocf-pool", type=float, default=128.0,
+    ap.add_argument("--ocf-pool", type=float, default=32.0,
                     help="OCF history pool entries per e-node (grown automatically if too small)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -73,10 +73,10 @@ struct esat_batch {
     // owned device buffers
     std::vector<void*> owned;
     // OCF pool
-    double pool_factor = 32.0;
-    std::vector<uint64_t> pb;
-    uint64_t pool_total = 0;
-    uint64_t* d_pb = nullptr;
+    double pool_factor = 32.0;   // f64 history entries per e-node
+    std::vector<uint64_t> pb, pbk;
+    uint64_t pool_total = 0, pool_ktotal = 0;
+    uint64_t *d_pb = nullptr, *d_pbk = nullptr;
     uint32_t* pool_key = nullptr;
     double* pool_val = nullptr;
     // e-matching results of the last esat_ematch / esat_join call
@@ -252,7 +252,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
-    OWN(x.hoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.chg, 2 * N);
+    OWN(x.hoff, 2 * N); OWN(x.hvoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.chg, 2 * N);
     OWN(x.need, N); OWN(x.lnode, N); OWN(x.lcls, N); OWN(x.lvn, NL); OWN(x.nval, N); OWN(x.naux, 2 * N);
     x.slot_stride = N;
     *out = b;
@@ -263,7 +263,7 @@ int esat_batch_destroy(esat_batch* b) {
     if (!b) return ESAT_OK;
     cudaSetDevice(b->ctx->device);
     for (void* p : b->owned) cudaFree(p);
-    cudaFree(b->d_pb); cudaFree(b->pool_key); cudaFree(b->pool_val);
+    cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
     cudaFree(b->d_over); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
@@ -321,17 +321,24 @@ static int ensure_pool(esat_batch* b) {
     esat_ctx* c = b->ctx;
     if (b->pool_total) return ESAT_OK;
     b->pb.assign(b->L + 1, 0);
+    b->pbk.assign(b->L + 1, 0);
+    const double kf = b->pool_factor / 8.0 > 3.0 ? b->pool_factor / 8.0 : 3.0;
     for (uint32_t l = 0; l < b->L; l++) {
         const uint64_t n = b->nb[l + 1] - b->nb[l];
+        const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)
         b->pb[l + 1] = b->pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
+        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * nw + 4 * nw + 64;
     }
     b->pool_total = b->pb[b->L];
-    cudaFree(b->d_pb); cudaFree(b->pool_key); cudaFree(b->pool_val);
-    b->d_pb = nullptr; b->pool_key = nullptr; b->pool_val = nullptr;
+    b->pool_ktotal = b->pbk[b->L];
+    cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
+    b->d_pb = nullptr; b->d_pbk = nullptr; b->pool_key = nullptr; b->pool_val = nullptr;
     CK(c, cudaMalloc((void**)&b->d_pb, 8ull * (b->L + 1)));
+    CK(c, cudaMalloc((void**)&b->d_pbk, 8ull * (b->L + 1)));
     CK(c, cudaMemcpy(b->d_pb, b->pb.data(), 8ull * (b->L + 1), cudaMemcpyHostToDevice));
-    CK(c, cudaMalloc((void**)&b->pool_key, 4ull * b->pool_total));
-    CK(c, cudaMalloc((void**)&b->pool_val, 8ull * b->pool_total));
+    CK(c, cudaMemcpy(b->d_pbk, b->pbk.data(), 8ull * (b->L + 1), cudaMemcpyHostToDevice));
+    CK(c, cudaMalloc((void**)&b->pool_key, 4ull * b->pool_ktotal + 64));
+    CK(c, cudaMalloc((void**)&b->pool_val, 8ull * b->pool_total + 64));
     return ESAT_OK;
 }
 
@@ -346,6 +353,7 @@ int esat_extract(esat_batch* b, int method) {
         int r = ensure_pool(b);
         if (r) return r;
         x.pool_base = b->d_pb;
+        x.pool_kbase = b->d_pbk;
         x.pool_key = b->pool_key;
         x.pool_val = b->pool_val;
         x.pool_stride = 0;   // one cumulative region per leaf

@@ -53,13 +53,15 @@ struct XArgs {
     double *root_cost, *class_cost, *prev;
     uint32_t *choice, *level, *order, *lvcnt, *stk, *stki;
     uint8_t *reach;
-    // OCF history pool: per leaf [pool_base[l], pool_base[l+1]) entries, bump-allocated over all
-    // passes (unchanged classes keep pointing at earlier histories)
+    // OCF constituent-history pools, bump-allocated over all passes (unchanged classes keep
+    // pointing at earlier histories): bitsets (u32 words) per leaf [pool_kbase[l], pool_kbase[l+1]),
+    // contributions (f64) per leaf [pool_base[l], pool_base[l+1])
     const uint64_t* pool_base;
-    uint32_t *pool_key;          // 2 parities x entries
+    const uint64_t* pool_kbase;
+    uint32_t *pool_key;
     double* pool_val;
-    uint64_t pool_stride;        // offset of parity 1
-    uint32_t *hoff, *hlen;       // [2][node rows] history slot per class position (pass parity)
+    uint64_t pool_stride;        // unused (0)
+    uint32_t *hoff, *hvoff, *hlen; // [2][node rows] history slot per class position (pass parity)
     uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip)
     uint8_t* need;               // [node rows] class needs re-evaluation in the current pass
     uint32_t *lnode, *lcls, *lvn; // e-nodes in level order, their classes, level ends (node-parallel phase)

@@ -1,5 +1,5 @@
 // K7-K10: batched greedy extraction -- default cost and the paper's constituent-cost (OCF)
-// node cost -- over clean leaf views, one CTA per leaf.
+// node cost -- over clean leaf views, one CTA (one warp) per leaf.
 //
 // Reference (extraction.py:121-242): passes over classes in ascending canonical id
 // (Gauss-Seidel: a class reads this pass's cost of lower classes and last pass's cost of
@@ -12,10 +12,15 @@
 //
 // Device schedule: level(k) = 1 + max level of k's lower-position
 // children, so all classes of one level are independent within a pass; a pass is one sweep
-// of levels separated by CTA barriers, reading cost_cur for lower positions and the pass-
-// start snapshot cost_prev otherwise. Histories are sorted (class position, f64) arrays in a
-// per-leaf pool, double-buffered by pass parity; each class materialises only the history
-// of its winning node, sized exactly by a read-only cost walk first.
+// of levels separated by barriers, reading cost_cur for lower positions and the pass-start
+// snapshot cost_prev otherwise. A class whose inputs did not change since its last evaluation
+// is skipped (exact dirty skip).
+//
+// Constituent histories are stored as a dense bitset over class positions (ceil(C/32) words,
+// 16-B aligned) plus the f64 contributions in key order. Alg. 2's dictionary operations become
+// word operations: membership is a bit test, the overlap of a child's constituents with the
+// node's running history is an AND, the inherited (non-overlapping) constituents an OR, and
+// values are located by popcount ranks -- no searching, no data-dependent merge walks.
 #include "esat_internal.cuh"
 
 namespace esat {
@@ -23,42 +28,20 @@ namespace esat {
 namespace {
 
 struct Hist {
-    const uint32_t* key;
-    const double* val;
+    const uint32_t* bits;   // NW words (only when present)
+    const double* vals;     // n values in key order
     uint32_t n;
     bool present;
 };
 
-__device__ __forceinline__ bool hist_has(const Hist& h, uint32_t key) {
-    int lo = 0, hi = (int)h.n - 1;
-    while (lo <= hi) {
-        int mid = (lo + hi) >> 1;
-        uint32_t k = h.key[mid];
-        if (k == key) return true;
-        if (k < key) lo = mid + 1; else hi = mid - 1;
-    }
-    return false;
-}
-
-__device__ __forceinline__ int hist_find(const uint32_t* key, uint32_t n, uint32_t x) {
-    int lo = 0, hi = (int)n - 1;
-    while (lo <= hi) {
-        int mid = (lo + hi) >> 1;
-        uint32_t k = key[mid];
-        if (k == x) return mid;
-        if (k < x) lo = mid + 1; else hi = mid - 1;
-    }
-    return -1;
-}
-
 struct LeafCtx {
-    uint32_t C, k;             // class count, class being evaluated
+    uint32_t C, k, NW;         // classes, class being evaluated, bitset words (multiple of 4)
     int pass;
     const uint32_t *nko, *kpos;
     const double *ncost, *cost, *prev;
-    const uint32_t *pk[2];     // pool keys per parity (leaf base applied)
-    const double *pv[2];
-    const uint32_t *hoff[2], *hlen[2];
+    const uint32_t* pk;        // bitset pool (leaf base applied)
+    const double* pv;          // value pool
+    const uint32_t *hoff[2], *hvoff[2], *hlen[2];
 };
 
 __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
@@ -72,54 +55,70 @@ __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
     if (j < c.k) par = c.pass & 1;                // flushed earlier in this pass
     else if (c.pass == 0) return h;               // not flushed yet
     else par = (c.pass - 1) & 1;                  // last pass's flush
-    uint32_t off = c.hoff[par][j];
-    h.key = c.pk[par] + off;
-    h.val = c.pv[par] + off;
+    h.bits = c.pk + c.hoff[par][j];
+    h.vals = c.pv + c.hvoff[par][j];
     h.n = c.hlen[par][j];
     h.present = true;
     return h;
 }
 
-// Read-only OCF walk for arity <= 2 (extraction.py:205-221): cost and exact history size.
-__device__ __forceinline__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out,
-                                             double* cc1_out, double* cc2_out, bool* skip2_out) {
+__device__ __forceinline__ bool hbit(const Hist& h, uint32_t key) {
+    return h.present && ((h.bits[key >> 5] >> (key & 31)) & 1u);
+}
+
+__device__ __forceinline__ uint32_t bit_of(uint32_t key, uint32_t w) {
+    return (key >> 5) == w ? (1u << (key & 31)) : 0u;
+}
+
+// Read-only OCF walk for arity <= 2 (extraction.py:205-221): node cost and exact history size.
+__device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, double* cc1_out, double* cc2_out,
+                            bool* skip2_out) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
     double v = c.ncost[nd];
-    uint32_t size = 0;
     *skip2_out = true;
     if (a == 0) { *size_out = 0; return v; }
     const uint32_t c1 = c.kpos[q0];
     const Hist h1 = child_hist(c, c1);
-    // case 2 with an empty running history: max_cost = 0 (case 3 when no history)
+    // case 2 with an empty running history (max_cost = 0), or case 3 without a history
     const double cc1 = h1.present ? pymax(child_cost(c, c1) - 0.0, 0.0) : child_cost(c, c1);
     v = v + cc1;
-    const bool c1_in_h1 = h1.present && hist_has(h1, c1);
-    size = h1.n + (c1_in_h1 ? 0u : 1u);
+    uint32_t size = h1.n + (hbit(h1, c1) ? 0u : 1u);
     *cc1_out = cc1;
     if (a == 2) {
         const uint32_t c2 = c.kpos[q0 + 1];
-        const bool skip = (c2 == c1) || (h1.present && hist_has(h1, c2));   // case 1
+        const bool skip = (c2 == c1) || hbit(h1, c2);   // case 1: already paid for
         *skip2_out = skip;
         if (!skip) {
             const Hist h2 = child_hist(c, c2);
             double cc2;
             if (h2.present) {
+                // case 2: overlap of h2's constituents with the running history H1 = h1 + {c1}
                 double m = 0.0;
-                uint32_t ov = 0, i = 0, j = 0;
-                while (i < h1.n && j < h2.n) {        // overlap with h1
-                    const uint32_t a1 = h1.key[i], a2 = h2.key[j];
-                    if (a1 == a2) { m = pymax(m, h2.val[j]); ov++; i++; j++; }
-                    else if (a1 < a2) i++;
-                    else j++;
-                }
-                if (!c1_in_h1) {                      // key c1 of the running history
-                    const int at = hist_find(h2.key, h2.n, c1);
-                    if (at >= 0) { m = pymax(m, h2.val[at]); ov++; }
+                uint32_t ov = 0, rank2 = 0;
+                const uint4* b2v = reinterpret_cast<const uint4*>(h2.bits);
+                const uint4* b1v = reinterpret_cast<const uint4*>(h1.bits);
+                for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) {
+                    const uint4 q2 = b2v[w4];
+                    if (!(q2.x | q2.y | q2.z | q2.w)) continue;
+                    const uint4 q1 = h1.present ? b1v[w4] : make_uint4(0, 0, 0, 0);
+                    const uint32_t w2[4] = {q2.x, q2.y, q2.z, q2.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const uint32_t w = 4 * w4 + t;
+                        uint32_t o = w2[t] & (w1[t] | bit_of(c1, w));
+                        while (o) {
+                            const int bpos = __ffs(o) - 1;
+                            m = pymax(m, h2.vals[rank2 + __popc(w2[t] & ((1u << bpos) - 1u))]);
+                            ov++;
+                            o &= o - 1;
+                        }
+                        rank2 += __popc(w2[t]);
+                    }
                 }
                 cc2 = pymax(child_cost(c, c2) - m, 0.0);
-                size += h2.n - ov + (hist_has(h2, c2) ? 0u : 1u);
+                size += h2.n - ov + (hbit(h2, c2) ? 0u : 1u);
             } else {
-                cc2 = child_cost(c, c2);
+                cc2 = child_cost(c, c2);   // case 3
                 size += 1;
             }
             *cc2_out = cc2;
@@ -130,92 +129,112 @@ __device__ __forceinline__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint3
     return v;
 }
 
-// Materialise the history of an arity <= 2 node into dst (sorted by key).
-__device__ void ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2, bool skip2,
-                           uint32_t* dk, double* dv) {
+// Materialise the history of an arity <= 2 node: bitset at ob (NW words), values at ovals.
+__device__ void ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2, bool skip2, uint32_t* ob,
+                           double* ovals) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
-    if (a == 0) return;
+    uint4* obv = reinterpret_cast<uint4*>(ob);
+    if (a == 0) {
+        for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) obv[w4] = make_uint4(0, 0, 0, 0);
+        return;
+    }
     const uint32_t c1 = c.kpos[q0];
     const Hist h1 = child_hist(c, c1);
     Hist h2{nullptr, nullptr, 0u, false};
     uint32_t c2 = NONE;
     if (a == 2 && !skip2) { c2 = c.kpos[q0 + 1]; h2 = child_hist(c, c2); }
-    // union of keys {h1, h2, c1, c2}; value: c1 -> cc1, c2 -> cc2, h1 wins over h2
-    uint32_t i = 0, j = 0, o = 0;
-    bool d1 = false, d2 = (c2 == NONE);
-    for (;;) {
-        uint32_t k1 = i < h1.n ? h1.key[i] : NONE;
-        uint32_t k2 = j < h2.n ? h2.key[j] : NONE;
-        uint32_t ks = d1 ? NONE : c1;
-        uint32_t kt = d2 ? NONE : c2;
-        uint32_t m = k1;
-        if (k2 < m) m = k2;
-        if (ks < m) m = ks;
-        if (kt < m) m = kt;
-        if (m == NONE) break;
-        double vv;
-        if (m == c1) vv = cc1;
-        else if (m == c2) vv = cc2;
-        else if (m == k1) vv = h1.val[i];
-        else vv = h2.val[j];
-        if (m == k1) i++;
-        if (m == k2) j++;
-        if (m == ks) d1 = true;
-        if (m == kt) d2 = true;
-        dk[o] = m;
-        dv[o] = vv;
-        o++;
+    // keys {h1, c1, h2, c2}; values: c1 -> cc1, c2 -> cc2, h1 wins over h2 (first writer)
+    uint32_t o = 0, rank1 = 0, rank2 = 0;
+    const uint4* b1v = reinterpret_cast<const uint4*>(h1.bits);
+    const uint4* b2v = reinterpret_cast<const uint4*>(h2.bits);
+    for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) {
+        const uint4 q1 = h1.present ? b1v[w4] : make_uint4(0, 0, 0, 0);
+        const uint4 q2 = h2.present ? b2v[w4] : make_uint4(0, 0, 0, 0);
+        const uint32_t w1[4] = {q1.x, q1.y, q1.z, q1.w}, w2[4] = {q2.x, q2.y, q2.z, q2.w};
+        uint32_t wo[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const uint32_t w = 4 * w4 + t;
+            uint32_t ow = w1[t] | w2[t] | bit_of(c1, w) | (c2 != NONE ? bit_of(c2, w) : 0u);
+            wo[t] = ow;
+            while (ow) {
+                const int bpos = __ffs(ow) - 1;
+                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
+                double val;
+                if (key == c1) val = cc1;
+                else if (key == c2) val = cc2;
+                else if ((w1[t] >> bpos) & 1u) val = h1.vals[rank1 + __popc(w1[t] & below)];
+                else val = h2.vals[rank2 + __popc(w2[t] & below)];
+                ovals[o++] = val;
+                ow &= ow - 1;
+            }
+            rank1 += __popc(w1[t]);
+            rank2 += __popc(w2[t]);
+        }
+        obv[w4] = make_uint4(wo[0], wo[1], wo[2], wo[3]);
     }
 }
 
-// Generic-arity OCF node (n-ary sink): builds the running history in the pool (current
-// parity) child by child, exactly as Alg. 2 mutates enode_hist. Returns the node cost;
-// the final history is at (*off_out, *n_out).
-__device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* top, uint64_t pcap, uint32_t* pk,
-                              double* pv, uint32_t* off_out, uint32_t* n_out, uint32_t* over) {
-    const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
+// Generic-arity OCF node (n-ary sink): the running history is rebuilt in the pool child by
+// child, exactly as Alg. 2 mutates enode_hist. Returns the node cost; the final history is at
+// (*boff, *voff, *n_out) (boff == NONE for an empty history).
+__device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uint32_t* topv, uint64_t capk,
+                              uint64_t capv, uint32_t* pk, double* pv, uint32_t* boff, uint32_t* voff,
+                              uint32_t* n_out, uint32_t* over) {
+    const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0, NW = c.NW;
     double v = c.ncost[nd];
-    uint32_t hoff = 0, hn = 0;
+    uint32_t hb = NONE, hv = 0, hn = 0;   // running history H (none yet)
     for (uint32_t t = 0; t < a; t++) {
         const uint32_t ck = c.kpos[q0 + t];
-        if (hn && hist_find(pk + hoff, hn, ck) >= 0) continue;       // case 1
+        if (hb != NONE && ((pk[hb + (ck >> 5)] >> (ck & 31)) & 1u)) continue;   // case 1
         const Hist h = child_hist(c, ck);
         double m = 0.0;
-        if (h.present) {                                             // overlap max (case 2)
-            uint32_t i = 0, j = 0;
-            while (i < hn && j < h.n) {
-                const uint32_t a1 = pk[hoff + i], a2 = h.key[j];
-                if (a1 == a2) { m = pymax(m, h.val[j]); i++; j++; }
-                else if (a1 < a2) i++;
-                else j++;
+        uint32_t add = 0;
+        if (h.present) {
+            uint32_t rank = 0;
+            for (uint32_t w = 0; w < NW; w++) {
+                const uint32_t bw = h.bits[w], Hw = hb != NONE ? pk[hb + w] : 0u;
+                uint32_t o = bw & Hw;
+                while (o) {
+                    const int bpos = __ffs(o) - 1;
+                    m = pymax(m, h.vals[rank + __popc(bw & ((1u << bpos) - 1u))]);
+                    o &= o - 1;
+                }
+                add += __popc(bw & ~Hw);
+                rank += __popc(bw);
             }
         }
         const double cc = h.present ? pymax(child_cost(c, ck) - m, 0.0) : child_cost(c, ck);
-        const uint32_t need = hn + h.n + 1;
-        const uint32_t noff = atomicAdd(top, need);
-        if ((uint64_t)noff + need > pcap) { *over = 1; *off_out = 0; *n_out = 0; return v + cc; }
-        uint32_t i = 0, j = 0, o = 0;
-        bool dc = false;
-        for (;;) {                                                   // keys {H, h, ck}; H wins, ck -> cc
-            const uint32_t k1 = i < hn ? pk[hoff + i] : NONE;
-            const uint32_t k2 = j < h.n ? h.key[j] : NONE;
-            const uint32_t k3 = dc ? NONE : ck;
-            uint32_t mk = k1 < k2 ? k1 : k2;
-            mk = k3 < mk ? k3 : mk;
-            if (mk == NONE) break;
-            double vv = (mk == k3) ? cc : (mk == k1 ? pv[hoff + i] : h.val[j]);
-            if (mk == k1) i++;
-            if (mk == k2) j++;
-            if (mk == k3) dc = true;
-            pk[noff + o] = mk;
-            pv[noff + o] = vv;
-            o++;
+        const bool ck_new = !hbit(h, ck);
+        const uint32_t nn = hn + add + (ck_new ? 1u : 0u);
+        const uint32_t nb = atomicAdd(topk, NW), nv = atomicAdd(topv, nn);
+        if ((uint64_t)nb + NW > capk || (uint64_t)nv + nn > capv) {
+            *over = 1; *boff = NONE; *voff = 0; *n_out = 0;
+            return v + cc;
         }
-        hoff = noff;
-        hn = o;
+        uint32_t o = 0, r0 = 0, r1 = 0;
+        for (uint32_t w = 0; w < NW; w++) {
+            const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u, bw = h.present ? h.bits[w] : 0u;
+            uint32_t ow = Hw | bw | bit_of(ck, w);
+            pk[nb + w] = ow;
+            while (ow) {
+                const int bpos = __ffs(ow) - 1;
+                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
+                double val;
+                if (key == ck) val = cc;                                                 // enode_hist[child]
+                else if ((Hw >> bpos) & 1u) val = pv[hv + r0 + __popc(Hw & below)];      // H wins (first writer)
+                else val = h.vals[r1 + __popc(bw & below)];
+                pv[nv + o++] = val;
+                ow &= ow - 1;
+            }
+            r0 += __popc(Hw);
+            r1 += __popc(bw);
+        }
+        hb = nb; hv = nv; hn = nn;
         v = v + cc;
     }
-    *off_out = hoff;
+    *boff = hb;
+    *voff = hv;
     *n_out = hn;
     return v;
 }
@@ -230,6 +249,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
     const uint32_t* coff = d.cls_off + b + l;
     LeafCtx c;
     c.C = C;
+    c.NW = ((C + 31) / 32 + 3) & ~3u;
     c.nko = d.nd_koff + b + l;
     c.kpos = d.nd_kpos + k0;
     c.ncost = d.nd_cost + b;
@@ -242,25 +262,30 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
     uint32_t* order = x.order + b;
     uint32_t* lvcnt = x.lvcnt + b + l;   // C+1 entries
     const bool ocf = x.method == 1;
-    uint64_t pb = 0, pcap = 0;
+    uint64_t capk = 0, capv = 0;
     uint32_t* hoffw[2] = {nullptr, nullptr};
+    uint32_t* hvoffw[2] = {nullptr, nullptr};
     uint32_t* hlenw[2] = {nullptr, nullptr};
-    uint32_t* pkw[2] = {nullptr, nullptr};
-    double* pvw[2] = {nullptr, nullptr};
+    uint32_t* pkw = nullptr;
+    double* pvw = nullptr;
     if (ocf) {
-        pb = x.pool_base[l];
-        pcap = x.pool_base[l + 1] - pb;
+        const uint64_t pbk = x.pool_kbase[l], pbv = x.pool_base[l];
+        capk = x.pool_kbase[l + 1] - pbk;
+        capv = x.pool_base[l + 1] - pbv;
+        pkw = x.pool_key + pbk;
+        pvw = x.pool_val + pbv;
+        c.pk = pkw;
+        c.pv = pvw;
         for (int p = 0; p < 2; p++) {
-            pkw[p] = x.pool_key + p * x.pool_stride + pb;
-            pvw[p] = x.pool_val + p * x.pool_stride + pb;
             hoffw[p] = x.hoff + p * x.slot_stride + b;
+            hvoffw[p] = x.hvoff + p * x.slot_stride + b;
             hlenw[p] = x.hlen + p * x.slot_stride + b;
-            c.pk[p] = pkw[p]; c.pv[p] = pvw[p]; c.hoff[p] = hoffw[p]; c.hlen[p] = hlenw[p];
+            c.hoff[p] = hoffw[p]; c.hvoff[p] = hvoffw[p]; c.hlen[p] = hlenw[p];
         }
     }
 
     __shared__ uint32_t sh_scan[33];
-    __shared__ uint32_t sh_flag, sh_maxlv, sh_top, sh_over;
+    __shared__ uint32_t sh_flag, sh_maxlv, sh_topk, sh_topv, sh_over;
 
     for (uint32_t k = tid; k < C; k += T) {
         cost[k] = __longlong_as_double(0x7ff0000000000000ll);
@@ -269,23 +294,22 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
         level[k] = 0;
         x.reach[b + k] = 0;
     }
-    if (tid == 0) sh_over = 0;
+    if (tid == 0) { sh_over = 0; sh_topk = 0; sh_topv = 0; }
     __syncthreads();
     // ---- K7: wavefront levels over lower-position children ----
     // level[k] = 1 + max level of k's lower-position children. Warp 0 walks the classes in
     // position order 32 at a time: children below the chunk are final; dependencies inside the
     // chunk are resolved by re-evaluating the chunk until no lane changes (chain length + 1 rounds).
-    __syncthreads();
     if (tid < 32) {
         uint32_t mx = 0;
-        for (uint32_t k0 = 0; k0 < C; k0 += 32) {
-            const uint32_t k = k0 + tid;
+        for (uint32_t kb0 = 0; kb0 < C; kb0 += 32) {
+            const uint32_t k = kb0 + tid;
             uint32_t base = 0;
             if (k < C)
                 for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
                     for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
                         const uint32_t j = c.kpos[q];
-                        if (j < k0) { const uint32_t t = level[j] + 1; base = t > base ? t : base; }
+                        if (j < kb0) { const uint32_t t = level[j] + 1; base = t > base ? t : base; }
                     }
             if (k < C) level[k] = base;
             __syncwarp();
@@ -295,7 +319,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
                         for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
                             const uint32_t j = c.kpos[q];
-                            if (j >= k0 && j < k) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
+                            if (j >= kb0 && j < k) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
                         }
                 const bool upd = k < C && lv != level[k];
                 __syncwarp();
@@ -331,12 +355,13 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
 
     // ---- K8/K9: Gauss-Seidel passes as level sweeps ----
     const uint64_t cap = 4ull * C + 8;
+    const uint32_t NW = c.NW;
     uint32_t st = X_NOT_CONVERGED, passes = 0;
     for (uint64_t it = 0; it < cap; it++) {
         const int pass = (int)it;
         c.pass = pass;
         for (uint32_t k = tid; k < C; k += T) prev[k] = cost[k];
-        if (tid == 0) { sh_flag = 0; if (pass == 0) sh_top = 0; }
+        if (tid == 0) sh_flag = 0;
         __syncthreads();
         const int par = pass & 1, ppar = par ^ 1;
         uint8_t* chg_cur = x.chg + par * x.slot_stride + b;
@@ -357,7 +382,11 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                     }
                 if (!need) {
                     chg_cur[k] = 0;
-                    if (ocf && C > 1) { hoffw[par][k] = hoffw[ppar][k]; hlenw[par][k] = hlenw[ppar][k]; }
+                    if (ocf && C > 1) {
+                        hoffw[par][k] = hoffw[ppar][k];
+                        hvoffw[par][k] = hvoffw[ppar][k];
+                        hlenw[par][k] = hlenw[ppar][k];
+                    }
                     continue;
                 }
                 double bv = __longlong_as_double(0x7ff0000000000000ll);
@@ -372,7 +401,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                 } else {
                     // first strict-min node by ocf_enode_cost; its history is flushed for class k
                     double hb = __longlong_as_double(0x7ff0000000000000ll);
-                    uint32_t hn = NONE, hsize = 0, hgoff = 0;
+                    uint32_t hn = NONE, hsize = 0, gb = NONE, gv = 0;
                     double h_cc1 = 0, h_cc2 = 0;
                     bool h_skip2 = true, h_gen = false;
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++) {
@@ -384,31 +413,44 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                             v = ocf_walk2(c, nd, &size, &cc1, &cc2, &skip2);
                             if (v < hb) { hb = v; hn = nd; hsize = size; h_cc1 = cc1; h_cc2 = cc2; h_skip2 = skip2; h_gen = false; }
                         } else {
-                            uint32_t goff, gn;
-                            v = ocf_generic(c, nd, &sh_top, pcap, pkw[0], pvw[0], &goff, &gn, &sh_over);
-                            if (v < hb) { hb = v; hn = nd; hsize = gn; hgoff = goff; h_gen = true; }
+                            uint32_t ob, ovf, on;
+                            v = ocf_generic(c, nd, &sh_topk, &sh_topv, capk, capv, pkw, pvw, &ob, &ovf, &on, &sh_over);
+                            if (v < hb) { hb = v; hn = nd; hsize = on; gb = ob; gv = ovf; h_gen = true; }
                         }
                         if (bn == NONE || v < bv) { bv = v; bn = nd; }
                     }
                     if (C > 1) {
-                        uint32_t off = 0;
-                        if (hn == NONE || hsize == 0) {
-                            hsize = 0;
-                        } else if (h_gen) {
-                            off = hgoff;
-                        } else {
-                            off = atomicAdd(&sh_top, hsize);
-                            if ((uint64_t)off + hsize > pcap) { sh_over = 1; hsize = 0; off = 0; }
-                            else ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw[0] + off, pvw[0] + off);
+                        uint32_t offk = NONE, offv = 0;
+                        if (hn != NONE && h_gen && gb != NONE) {
+                            offk = gb; offv = gv;
+                        } else if (!(hn != NONE && h_gen)) {
+                            if (hn == NONE) hsize = 0;
+                            offk = atomicAdd(&sh_topk, NW);
+                            offv = atomicAdd(&sh_topv, hsize);
+                            if ((uint64_t)offk + NW > capk || (uint64_t)offv + hsize > capv) {
+                                sh_over = 1; offk = NONE;
+                            } else if (hn == NONE) {
+                                uint4* ob = reinterpret_cast<uint4*>(pkw + offk);
+                                for (uint32_t w4 = 0; w4 < NW / 4; w4++) ob[w4] = make_uint4(0, 0, 0, 0);
+                            } else {
+                                ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw + offk, pvw + offv);
+                            }
                         }
-                        hoffw[par][k] = off;
+                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; sh_over = 1; }   // status reports it
+                        hoffw[par][k] = offk;
+                        hvoffw[par][k] = offv;
                         hlenw[par][k] = hsize;
                         if (!changed) {  // did the flushed history change w.r.t. last pass?
-                            const uint32_t o2 = hoffw[ppar][k], n2 = hlenw[ppar][k];
+                            const uint32_t ok2 = hoffw[ppar][k], ov2 = hvoffw[ppar][k], n2 = hlenw[ppar][k];
                             if (n2 != hsize) changed = true;
+                            const uint4* a4 = reinterpret_cast<const uint4*>(pkw + offk);
+                            const uint4* b4 = reinterpret_cast<const uint4*>(pkw + ok2);
+                            for (uint32_t w4 = 0; w4 < NW / 4 && !changed; w4++) {
+                                const uint4 p = a4[w4], q = b4[w4];
+                                changed = p.x != q.x || p.y != q.y || p.z != q.z || p.w != q.w;
+                            }
                             for (uint32_t i = 0; i < hsize && !changed; i++)
-                                changed = pkw[0][off + i] != pkw[0][o2 + i] ||
-                                          __double_as_longlong(pvw[0][off + i]) != __double_as_longlong(pvw[0][o2 + i]);
+                                changed = __double_as_longlong(pvw[offv + i]) != __double_as_longlong(pvw[ov2 + i]);
                         }
                     }
                 }
