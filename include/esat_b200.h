@@ -119,6 +119,15 @@ int esat_join(esat_batch* b, uint32_t n_rules, const uint32_t* src_off, const ui
  * per-leaf pool of entries_per_node * n entries per pass parity (ESAT_X_CAPACITY -> grow, retry) */
 int esat_batch_set_pool(esat_batch* b, double entries_per_node);
 int esat_extract(esat_batch* b, int method);
+/* the same on the context's side stream: extraction only reads the rebuilt view, so it overlaps
+ * esat_ematch / esat_join on the main stream; esat_wait_async joins it back (downloads and
+ * esat_copy_results join implicitly) */
+int esat_extract_async(esat_batch* b, int method);
+/* mark the current point of the main stream as the side stream's start (so work issued on the
+ * main stream after esat_fork overlaps a later esat_extract_async) */
+int esat_fork(esat_ctx* ctx);
+int esat_wait_async(esat_ctx* ctx);
+float esat_last_async_ms(const esat_ctx* ctx);
 
 /* downloads (host buffers sized from the batch bases) */
 int esat_download_rebuild(esat_batch* b, uint32_t* n_out, uint32_t* merges, uint32_t* hc_sym, uint32_t* hc_koff,

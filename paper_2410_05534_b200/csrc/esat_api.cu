@@ -21,6 +21,10 @@ struct esat_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = true;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // side stream: extraction overlaps e-matching (both only read the rebuilt view)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_done = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+    bool side_timed = false, side_pending = false, fork_armed = false;
     bool timed = false;
     char err[512] = {0};
     // symbol table
@@ -33,6 +37,7 @@ struct esat_ctx {
     std::vector<int32_t> pat_words;
     int32_t* d_pat = nullptr;
     uint32_t* d_pat_off = nullptr;
+    uint32_t pat_gen = 0, sym_gen = 0;
 };
 
 namespace {
@@ -90,6 +95,12 @@ struct esat_batch {
     uint32_t* d_jspec = nullptr;
     uint64_t jspec_cap = 0;
     uint32_t* d_raw = nullptr;
+    // optimistic (lazily verified) re-launch of a verified e-match / join call
+    uint32_t upload_gen = 0, m_mode = 0, m_Pcap = 0, j_Rcap = 0, m_smem = 0;
+    uint32_t j_nsrc = 0, j_nmap_v = 0, j_nmap_q = 0;
+    bool m_verified = false, m_pending = false, j_verified = false, j_pending = false;
+    bool j_relaunch_needed = false, m_sig_matches_join = false;
+    std::vector<uint32_t> m_sig, j_sig;
 };
 
 namespace {
@@ -133,6 +144,11 @@ int esat_ctx_create(int device, esat_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev_s0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev_s1);
     if (e != cudaSuccess) {
         *out = nullptr;
         delete c;
@@ -147,6 +163,11 @@ int esat_ctx_destroy(esat_ctx* c) {
     cudaSetDevice(c->device);
     cudaFree(c->sym_name); cudaFree(c->sym_arity); cudaFree(c->sym_rank); cudaFree(c->sym_poff);
     cudaFree(c->sym_par); cudaFree(c->d_pat); cudaFree(c->d_pat_off);
+    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
+    if (c->ev_s0) cudaEventDestroy(c->ev_s0);
+    if (c->ev_s1) cudaEventDestroy(c->ev_s1);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream && c->own_stream) cudaStreamDestroy(c->stream);
@@ -185,6 +206,7 @@ int esat_symtab_upload(esat_ctx* c, uint32_t n, const uint32_t* name, const uint
     if (np) CK(c, cudaMemcpyAsync(c->sym_par, par, 4ull * np, cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     c->n_syms = n;
+    c->sym_gen++;
     return ESAT_OK;
 }
 
@@ -199,6 +221,7 @@ int esat_patterns_upload(esat_ctx* c, uint32_t n, const uint32_t* off, uint32_t 
     CK(c, cudaMemcpyAsync(c->d_pat_off, off, 4ull * (n + 1), cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     c->n_pat = n;
+    c->pat_gen++;
     return ESAT_OK;
 }
 
@@ -289,6 +312,7 @@ int esat_batch_upload(esat_batch* b, const uint32_t* sym, const uint32_t* koff, 
     CK(c, cudaMemcpyAsync((void*)b->d.root, root, 4 * L, cudaMemcpyHostToDevice, s));
     b->uploaded = true;
     b->rebuilt = false;
+    b->upload_gen++;
     return ESAT_OK;
 }
 
@@ -342,11 +366,8 @@ static int ensure_pool(esat_batch* b) {
     return ESAT_OK;
 }
 
-int esat_extract(esat_batch* b, int method) {
-    if (!b || (method != ESAT_METHOD_DEFAULT && method != ESAT_METHOD_OCF)) return ESAT_E_ARG;
+static int launch_extract(esat_batch* b, int method, cudaStream_t s) {
     esat_ctx* c = b->ctx;
-    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "extraction requires a rebuilt e-graph");
-    cudaSetDevice(c->device);
     XArgs x = b->x;
     x.method = method;
     if (method == ESAT_METHOD_OCF) {
@@ -358,15 +379,69 @@ int esat_extract(esat_batch* b, int method) {
         x.pool_val = b->pool_val;
         x.pool_stride = 0;   // one cumulative region per leaf
     }
-    tic(c);
     static const int xt = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 32;
     if (b->L) {
-        if (xt == 128) k_extract<128><<<b->L, 128, 0, c->stream>>>(b->d, x);
-        else if (xt == 64) k_extract<64><<<b->L, 64, 0, c->stream>>>(b->d, x);
-        else k_extract<32><<<b->L, 32, 0, c->stream>>>(b->d, x);
+        if (xt == 128) k_extract<128><<<b->L, 128, 0, s>>>(b->d, x);
+        else if (xt == 64) k_extract<64><<<b->L, 64, 0, s>>>(b->d, x);
+        else k_extract<32><<<b->L, 32, 0, s>>>(b->d, x);
     }
-    toc(c);
     return launch_check(c, "k_extract");
+}
+
+int esat_extract(esat_batch* b, int method) {
+    if (!b || (method != ESAT_METHOD_DEFAULT && method != ESAT_METHOD_OCF)) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "extraction requires a rebuilt e-graph");
+    cudaSetDevice(c->device);
+    tic(c);
+    int r = launch_extract(b, method, c->stream);
+    toc(c);
+    return r;
+}
+
+int esat_extract_async(esat_batch* b, int method) {
+    if (!b || (method != ESAT_METHOD_DEFAULT && method != ESAT_METHOD_OCF)) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "extraction requires a rebuilt e-graph");
+    cudaSetDevice(c->device);
+    if (method == ESAT_METHOD_OCF) {
+        int r = ensure_pool(b);   // allocation is synchronous; do it before forking
+        if (r) return r;
+    }
+    if (!c->fork_armed) CK(c, cudaEventRecord(c->ev_fork, c->stream));
+    c->fork_armed = false;
+    CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    CK(c, cudaEventRecord(c->ev_s0, c->side));
+    int r = launch_extract(b, method, c->side);
+    CK(c, cudaEventRecord(c->ev_s1, c->side));
+    CK(c, cudaEventRecord(c->ev_done, c->side));
+    c->side_timed = true;
+    c->side_pending = true;
+    return r;
+}
+
+int esat_fork(esat_ctx* c) {
+    if (!c) return ESAT_E_ARG;
+    CK(c, cudaEventRecord(c->ev_fork, c->stream));
+    c->fork_armed = true;
+    return ESAT_OK;
+}
+
+int esat_wait_async(esat_ctx* c) {
+    if (!c) return ESAT_E_ARG;
+    if (c->side_pending) {
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_done, 0));
+        c->side_pending = false;
+    }
+    return ESAT_OK;
+}
+
+float esat_last_async_ms(const esat_ctx* c) {
+    if (!c || !c->side_timed) return -1.f;
+    float ms = -1.f;
+    if (cudaEventSynchronize(c->ev_s1) != cudaSuccess) return -1.f;
+    cudaEventElapsedTime(&ms, c->ev_s0, c->ev_s1);
+    return ms;
 }
 
 int esat_download_rebuild(esat_batch* b, uint32_t* n_out, uint32_t* merges, uint32_t* sym, uint32_t* koff,
@@ -413,6 +488,7 @@ int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, 
                           double* class_cost, uint32_t* choice, uint8_t* reachable, uint32_t* passes) {
     if (!b) return ESAT_E_ARG;
     esat_ctx* c = b->ctx;
+    esat_wait_async(c);
     cudaSetDevice(c->device);
     cudaStream_t s = c->stream;
     const uint64_t N = b->N, L = b->L;
@@ -441,6 +517,7 @@ int esat_ctx_set_stream(esat_ctx* c, void* stream) {
 int esat_copy_results(esat_batch* b, void* dev_root_cost, void* dev_status) {
     if (!b) return ESAT_E_ARG;
     esat_ctx* c = b->ctx;
+    esat_wait_async(c);
     cudaSetDevice(c->device);
     if (dev_root_cost)
         CK(c, cudaMemcpyAsync(dev_root_cost, b->x.root_cost, 8ull * b->L, cudaMemcpyDeviceToDevice, c->stream));
@@ -484,6 +561,70 @@ int ensure_match_meta(esat_batch* b) {
 
 extern "C" {
 
+// Launch k_ematch for the call recorded in b (pattern ids / mode already on device).
+static int ematch_launch(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    const uint64_t L = b->L;
+    const uint32_t P = b->m_P;
+    int r;
+    CK(c, cudaMemsetAsync(b->d_tops, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(c, cudaMemsetAsync(b->d_over, 0, sizeof(uint32_t), c->stream));
+    MArgs a{};
+    a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = b->m_mode;
+    a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw;
+    a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
+    Dev d = b->d;
+    d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
+    d.sym_par = c->sym_par; d.n_syms = c->n_syms;
+    a.smem_bytes = b->m_smem;
+    static uint32_t attr_set = 0;
+    const uint32_t cap_bytes = 100 * 1024;
+    if (a.smem_bytes > attr_set) {
+        CK(c, cudaFuncSetAttribute(k_ematch<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_bytes));
+        attr_set = cap_bytes;
+    }
+    tic(c);
+    if (L && P) k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, a);
+    toc(c);
+    if ((r = launch_check(c, "k_ematch"))) return r;
+    return ESAT_OK;
+}
+
+// Synchronous check of the last k_ematch: regrow and relaunch on overflow.
+static int ematch_settle(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    int r;
+    for (int attempt = 0; attempt < 4; attempt++) {
+        uint32_t over = 0;
+        unsigned long long tops[2];
+        CK(c, cudaMemcpyAsync(&over, b->d_over, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(tops, b->d_tops, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (!over) { b->m_verified = true; b->m_pending = false; return ESAT_OK; }
+        if ((r = regrow(c, &b->stage, &b->stage_cap, tops[0]))) return r;
+        if ((r = regrow(c, &b->m_out, &b->m_cap, tops[1] > tops[0] ? tops[1] : tops[0]))) return r;
+        if ((r = ematch_launch(b))) return r;
+    }
+    return fail(c, ESAT_E_CAPACITY, "ematch output did not fit after regrowing");
+}
+
+static int join_launch(esat_batch* b);
+static int join_settle(esat_batch* b);
+
+// Resolve optimistic (unchecked) e-match / join launches: verify capacities, redo on overflow.
+static int verify_matches(esat_batch* b) {
+    int r;
+    if (b->m_pending) {
+        const bool redo_join = b->j_pending || b->j_R;
+        if ((r = ematch_settle(b))) return r;
+        if (redo_join && b->j_R && b->j_relaunch_needed) { if ((r = join_launch(b))) return r; }
+    }
+    if (b->j_pending) {
+        if ((r = join_settle(b))) return r;
+    }
+    return ESAT_OK;
+}
+
 int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     if (!b || (P && !pat_ids) || (mode != ESAT_MATCH_LIST && mode != ESAT_MATCH_EXISTS)) return ESAT_E_ARG;
     if (P > 32) return fail(b->ctx, ESAT_E_ARG, "at most 32 patterns per esat_ematch call (got %u)", P);
@@ -495,93 +636,121 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     const uint64_t L = b->L;
     int r;
     if ((r = ensure_match_meta(b))) return r;
-    cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_off); cudaFree(b->d_m_W);
-    b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
-    CK(c, cudaMalloc((void**)&b->d_pat_ids, 4ull * (P ? P : 1)));
-    CK(c, cudaMalloc((void**)&b->d_m_count, 4ull * (P * L ? P * L : 1)));
-    CK(c, cudaMalloc((void**)&b->d_m_off, 8ull * (P * L ? P * L : 1)));
-    CK(c, cudaMalloc((void**)&b->d_m_W, 4ull * (P ? P : 1)));
-    b->m_W.resize(P);
-    for (uint32_t i = 0; i < P; i++) {
-        const int32_t* pg = c->pat_words.data() + c->pat_off[pat_ids[i]];
-        b->m_W[i] = 1 + pg[1] + pg[2];
-        if (pg[0] > MAX_PN || pg[1] > MAX_V || pg[2] > MAX_V || (int)b->m_W[i] > MAX_W)
-            return fail(c, ESAT_E_ARG, "pattern %u exceeds device limits", pat_ids[i]);
-    }
-    CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
-    b->m_P = P;
-    if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts
-    if (!b->stage_cap) {
-        if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
-        if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
-    }
-    for (int attempt = 0; attempt < 4; attempt++) {
-        CK(c, cudaMemsetAsync(b->d_tops, 0, 8 * sizeof(unsigned long long), c->stream));
-        CK(c, cudaMemsetAsync(b->d_over, 0, 2 * sizeof(uint32_t), c->stream));
-        MArgs a{};
-        a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = mode;
-        a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw;
-        a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
-        Dev d = b->d;
-        d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
-        d.sym_par = c->sym_par; d.n_syms = c->n_syms;
-        // dynamic SMEM for staging the largest leaf's view (bounded; bigger leaves read global memory)
+    // Re-issuing a verified call on the same upload, patterns and symbol table reproduces the same
+    // output sizes (the clean view is a pure function of the upload), so it runs without a host
+    // round-trip; any other call is checked synchronously and regrown on overflow.
+    std::vector<uint32_t> sig(pat_ids, pat_ids + P);
+    sig.push_back((uint32_t)mode);
+    sig.push_back(b->upload_gen);
+    sig.push_back(c->pat_gen);
+    sig.push_back(c->sym_gen);
+    const bool same = b->m_verified && sig == b->m_sig;
+    if (!same) b->m_sig_matches_join = false;
+    if (!same) {
+        if (P > b->m_Pcap) {
+            cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_off); cudaFree(b->d_m_W);
+            b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
+            CK(c, cudaMalloc((void**)&b->d_pat_ids, 4ull * 32));
+            CK(c, cudaMalloc((void**)&b->d_m_count, 4ull * 32 * (L ? L : 1)));
+            CK(c, cudaMalloc((void**)&b->d_m_off, 8ull * 32 * (L ? L : 1)));
+            CK(c, cudaMalloc((void**)&b->d_m_W, 4ull * 32));
+            b->m_Pcap = 32;
+        }
+        b->m_W.resize(P);
+        for (uint32_t i = 0; i < P; i++) {
+            const int32_t* pg = c->pat_words.data() + c->pat_off[pat_ids[i]];
+            b->m_W[i] = 1 + pg[1] + pg[2];
+            if (pg[0] > MAX_PN || pg[1] > MAX_V || pg[2] > MAX_V || (int)b->m_W[i] > MAX_W)
+                return fail(c, ESAT_E_ARG, "pattern %u exceeds device limits", pat_ids[i]);
+        }
+        CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
+        if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts
+        if (!b->stage_cap) {
+            if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
+            if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
+        }
+        // dynamic SMEM for staging the largest leaf's hot view (bounded; bigger leaves read global)
         uint64_t mx = 0;
         for (uint64_t l = 0; l < L; l++) {
-            const uint64_t n = b->nb[l + 1] - b->nb[l], k = b->kb[l + 1] - b->kb[l];
+            const uint64_t n = b->nb[l + 1] - b->nb[l];
             const uint64_t bytes = 4 * (2 * n + 1) + 2 * 32 + 4 * n + 32;   // cls_off + nd_sym + class op masks
             mx = bytes > mx ? bytes : mx;
         }
         const uint32_t cap_bytes = 100 * 1024;
-        a.smem_bytes = (uint32_t)(mx < cap_bytes ? mx : cap_bytes);
-        if (getenv("ESAT_EMATCH_NOSTAGE")) a.smem_bytes = 0;
-        static uint32_t attr_set = 0;
-        if (a.smem_bytes > attr_set) {
-            CK(c, cudaFuncSetAttribute(k_ematch<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_bytes));
-            attr_set = cap_bytes;
-        }
-        tic(c);
-        if (L && P) k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, a);
-        toc(c);
-        if ((r = launch_check(c, "k_ematch"))) return r;
-        if (mode == ESAT_MATCH_EXISTS) return ESAT_OK;
+        b->m_smem = (uint32_t)(mx < cap_bytes ? mx : cap_bytes);
+        if (getenv("ESAT_EMATCH_NOSTAGE")) b->m_smem = 0;
+    }
+    b->m_P = P;
+    b->m_mode = mode;
+    b->j_R = 0;   // a new match call invalidates earlier join results
+    if ((r = ematch_launch(b))) return r;
+    if (mode == ESAT_MATCH_EXISTS) { b->m_pending = false; return ESAT_OK; }
+    if (same) return ESAT_OK;   // deterministic re-issue of a verified call
+    b->m_verified = false;
+    if ((r = ematch_settle(b))) return r;
+    b->m_sig = sig;
+    return ESAT_OK;
+}
+
+static int join_launch(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    const uint64_t L = b->L;
+    const uint32_t R = b->j_R, nsrc = b->j_nsrc, nmap_v = b->j_nmap_v, nmap_q = b->j_nmap_q;
+    CK(c, cudaMemsetAsync(b->d_tops + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(c, cudaMemsetAsync(b->d_over + 1, 0, sizeof(uint32_t), c->stream));
+    const uint32_t* p = b->d_jspec;
+    JArgs a{};
+    a.R = R;
+    a.src_off = p; a.src = p + (R + 1); a.map_off = a.src + nsrc; a.vmap = a.map_off + 2 * (nsrc + 1);
+    a.qmap = a.vmap + nmap_v; a.nv = a.qmap + nmap_q; a.nq = a.nv + R;
+    a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
+    a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
+    a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
+    tic(c);
+    if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 0, c->stream>>>((uint32_t)L, a);
+    toc(c);
+    b->j_relaunch_needed = true;
+    return launch_check(c, "k_join");
+}
+
+static int join_settle(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    int r;
+    for (int attempt = 0; attempt < 4; attempt++) {
         uint32_t over = 0;
         unsigned long long tops[2];
-        CK(c, cudaMemcpyAsync(&over, b->d_over, 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaMemcpyAsync(tops, b->d_tops, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(&over, b->d_over + 1, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 16, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
-        if (!over) return ESAT_OK;
-        if ((r = regrow(c, &b->stage, &b->stage_cap, tops[0]))) return r;
-        if ((r = regrow(c, &b->m_out, &b->m_cap, tops[1] > tops[0] ? tops[1] : tops[0]))) return r;
+        if (!over) { b->j_verified = true; b->j_pending = false; return ESAT_OK; }
+        if ((r = regrow(c, &b->j_out, &b->j_cap, tops[1]))) return r;
+        if ((r = join_launch(b))) return r;
     }
-    return fail(c, ESAT_E_CAPACITY, "ematch output did not fit after regrowing");
+    return fail(c, ESAT_E_CAPACITY, "join output did not fit after regrowing");
 }
 
 int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t* src, const uint32_t* map_off,
               const uint32_t* vmap, const uint32_t* qmap, const uint32_t* nv, const uint32_t* nq) {
     if (!b || (R && (!src_off || !src || !map_off || !nv || !nq))) return ESAT_E_ARG;
     esat_ctx* c = b->ctx;
-    if (!b->m_P) return fail(c, ESAT_E_STATE, "esat_join needs the source matches of a LIST esat_ematch call");
+    if (!b->m_P || b->m_mode != ESAT_MATCH_LIST)
+        return fail(c, ESAT_E_STATE, "esat_join needs the source matches of a LIST esat_ematch call");
     cudaSetDevice(c->device);
     const uint64_t L = b->L;
     const uint32_t nsrc = src_off[R];
-    b->j_W.resize(R);
+    std::vector<uint32_t> jW(R);
     for (uint32_t r = 0; r < R; r++) {
         const uint32_t S = src_off[r + 1] - src_off[r];
         if (S < 1 || S > MAX_S) return fail(c, ESAT_E_ARG, "rule %u: %u sources (max %d)", r, S, MAX_S);
         for (uint32_t s = src_off[r]; s < src_off[r + 1]; s++)
             if (src[s] >= b->m_P) return fail(c, ESAT_E_ARG, "join source %u not in the last ematch call", src[s]);
-        b->j_W[r] = S + nv[r] + nq[r];
-        if (b->j_W[r] > (uint32_t)MAX_W || nv[r] > 64 || nq[r] > 64) return fail(c, ESAT_E_ARG, "rule %u too wide", r);
+        jW[r] = S + nv[r] + nq[r];
+        if (jW[r] > (uint32_t)MAX_W || nv[r] > 64 || nq[r] > 64) return fail(c, ESAT_E_ARG, "rule %u too wide", r);
     }
     const uint32_t nmap_v = map_off[2 * nsrc], nmap_q = map_off[2 * nsrc + 1];
     // spec words: src_off[R+1] src[nsrc] map_off[2*(nsrc+1)] vmap[nmap_v] qmap[nmap_q] nv[R] nq[R]
-    const uint64_t words = (R + 1) + nsrc + 2ull * (nsrc + 1) + nmap_v + nmap_q + 2ull * R;
-    int r_;
-    if ((r_ = regrow(c, &b->d_jspec, &b->jspec_cap, words))) return r_;
     std::vector<uint32_t> spec;
-    spec.reserve(words);
     spec.insert(spec.end(), src_off, src_off + R + 1);
     spec.insert(spec.end(), src, src + nsrc);
     spec.insert(spec.end(), map_off, map_off + 2 * (nsrc + 1));
@@ -589,43 +758,42 @@ int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t
     spec.insert(spec.end(), qmap, qmap + nmap_q);
     spec.insert(spec.end(), nv, nv + R);
     spec.insert(spec.end(), nq, nq + R);
-    CK(c, cudaMemcpyAsync(b->d_jspec, spec.data(), 4 * spec.size(), cudaMemcpyHostToDevice, c->stream));
-    cudaFree(b->d_j_count); cudaFree(b->d_j_off);
-    b->d_j_count = nullptr; b->d_j_off = nullptr;
-    CK(c, cudaMalloc((void**)&b->d_j_count, 4ull * (R * L ? R * L : 1)));
-    CK(c, cudaMalloc((void**)&b->d_j_off, 8ull * (R * L ? R * L : 1)));
-    b->j_R = R;
-    if (!b->j_cap && (r_ = regrow(c, &b->j_out, &b->j_cap, 4 * b->N + 4096))) return r_;
-    const uint32_t* p = b->d_jspec;
-    for (int attempt = 0; attempt < 4; attempt++) {
-        CK(c, cudaMemsetAsync(b->d_tops + 2, 0, 2 * sizeof(unsigned long long), c->stream));
-        CK(c, cudaMemsetAsync(b->d_over + 1, 0, sizeof(uint32_t), c->stream));
-        JArgs a{};
-        a.R = R;
-        a.src_off = p; a.src = p + (R + 1); a.map_off = a.src + nsrc; a.vmap = a.map_off + 2 * (nsrc + 1);
-        a.qmap = a.vmap + nmap_v; a.nv = a.qmap + nmap_q; a.nq = a.nv + R;
-        a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
-        a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
-        a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
-        tic(c);
-        if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 0, c->stream>>>((uint32_t)L, a);
-        toc(c);
-        if ((r_ = launch_check(c, "k_join"))) return r_;
-        uint32_t over = 0;
-        unsigned long long tops[2];
-        CK(c, cudaMemcpyAsync(&over, b->d_over + 1, 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 16, cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
-        if (!over) return ESAT_OK;
-        if ((r_ = regrow(c, &b->j_out, &b->j_cap, tops[1]))) return r_;
+    std::vector<uint32_t> sig = spec;
+    sig.push_back(b->upload_gen);
+    sig.push_back(c->sym_gen);
+    const bool same = b->j_verified && sig == b->j_sig && b->m_sig_matches_join;
+    int r_;
+    if (!same) {
+        // the source lists must be final before a checked join
+        if (b->m_pending && (r_ = ematch_settle(b))) return r_;
+        if ((r_ = regrow(c, &b->d_jspec, &b->jspec_cap, spec.size()))) return r_;
+        CK(c, cudaMemcpyAsync(b->d_jspec, spec.data(), 4 * spec.size(), cudaMemcpyHostToDevice, c->stream));
+        if (R > b->j_Rcap) {
+            cudaFree(b->d_j_count); cudaFree(b->d_j_off);
+            b->d_j_count = nullptr; b->d_j_off = nullptr;
+            CK(c, cudaMalloc((void**)&b->d_j_count, 4ull * R * (L ? L : 1)));
+            CK(c, cudaMalloc((void**)&b->d_j_off, 8ull * R * (L ? L : 1)));
+            b->j_Rcap = R;
+        }
+        if (!b->j_cap && (r_ = regrow(c, &b->j_out, &b->j_cap, 4 * b->N + 4096))) return r_;
     }
-    return fail(c, ESAT_E_CAPACITY, "join output did not fit after regrowing");
+    b->j_W = jW;
+    b->j_R = R; b->j_nsrc = nsrc; b->j_nmap_v = nmap_v; b->j_nmap_q = nmap_q;
+    if ((r_ = join_launch(b))) return r_;
+    if (same) return ESAT_OK;   // deterministic re-issue of a verified join
+    b->j_verified = false;
+    if ((r_ = join_settle(b))) return r_;
+    b->j_sig = sig;
+    b->m_sig_matches_join = true;
+    return ESAT_OK;
 }
 
 int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t* counts, uint64_t* word_off,
                           uint32_t* words, uint64_t words_cap) {
     if (!b || !counts || !word_off) return ESAT_E_ARG;
     esat_ctx* c = b->ctx;
+    int rv = verify_matches(b);
+    if (rv) return rv;
     const uint32_t n = from_join ? b->j_R : b->m_P;
     if (index >= n) return fail(c, ESAT_E_ARG, "match index %u out of range (%u)", index, n);
     cudaSetDevice(c->device);

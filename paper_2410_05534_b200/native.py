@@ -54,12 +54,14 @@ def lib():
         L.esat_last_error.argtypes = [vp]
         L.esat_last_kernel_ms.restype = C.c_float
         L.esat_last_kernel_ms.argtypes = [vp]
+        L.esat_last_async_ms.restype = C.c_float
+        L.esat_last_async_ms.argtypes = [vp]
         for name in ("esat_ctx_create", "esat_ctx_destroy", "esat_ctx_sync", "esat_symtab_upload",
                      "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
                      "esat_rebuild", "esat_ematch", "esat_join", "esat_extract", "esat_batch_set_pool",
                      "esat_download_rebuild", "esat_download_view", "esat_download_matches",
                      "esat_download_extract", "esat_result_device_ptrs", "esat_ctx_set_stream",
-                     "esat_copy_results"):
+                     "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork"):
             getattr(L, name).restype = C.c_int
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
         _lib = L
@@ -70,7 +72,8 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_patterns_upload", "esat_batch_create", "esat_batch_destroy", "esat_batch_upload",
             "esat_rebuild", "esat_ematch", "esat_join", "esat_batch_set_pool", "esat_extract",
             "esat_download_rebuild", "esat_download_view", "esat_download_matches", "esat_download_extract",
-            "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results")
+            "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results",
+            "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork")
 
 
 def _p(a):
@@ -113,6 +116,15 @@ class Context:
 
     def last_ms(self) -> float:
         return float(self.L.esat_last_kernel_ms(self.h))
+
+    def last_async_ms(self) -> float:
+        return float(self.L.esat_last_async_ms(self.h))
+
+    def fork(self):
+        self.check(self.L.esat_fork(self.h))
+
+    def wait_async(self):
+        self.check(self.L.esat_wait_async(self.h))
 
     def upload_symtab(self, arrays: dict):
         n = len(arrays["name"])
@@ -175,6 +187,10 @@ class DeviceBatch:
 
     def extract(self, method: str):
         self.ctx.check(self.L.esat_extract(self.h, C.c_int(METHODS[method])))
+
+    def extract_async(self, method: str):
+        """Extraction on the side stream, overlapping e-matching (join with ctx.wait_async())."""
+        self.ctx.check(self.L.esat_extract_async(self.h, C.c_int(METHODS[method])))
 
     def ematch(self, pattern_ids, mode: int = MATCH_LIST):
         ids = _u32(pattern_ids)

@@ -94,10 +94,16 @@ class LeafPipeline:
     def extract(self):
         self.batch.extract(self.method)
 
+    def extract_async(self):
+        self.batch.extract_async(self.method)
+
     def step(self):
+        """rebuild, then OCF extraction on the side stream concurrently with e-match + join."""
         self.rebuild()
+        self.ctx.fork()
         self.ematch()
-        self.extract()
+        self.extract_async()
+        self.ctx.wait_async()
 
     LAUNCHES_PER_STEP = 4  # k_rebuild, k_ematch, k_join, k_extract
 
