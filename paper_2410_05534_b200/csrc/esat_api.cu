@@ -707,8 +707,19 @@ static int join_launch(esat_batch* b) {
     a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
     a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
     a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
+    // run table in dynamic SMEM: one u32 per class id of the largest leaf (capped)
+    uint64_t umax = 0;
+    for (uint64_t l = 0; l < L; l++) umax = b->ub[l + 1] - b->ub[l] > umax ? b->ub[l + 1] - b->ub[l] : umax;
+    const uint32_t run_cap = (uint32_t)(umax < 16384 ? umax : 16384);
+    a.id_base = b->d.ub;
+    a.run_cap = run_cap;
+    static bool join_attr = false;
+    if (!join_attr) {
+        CK(c, cudaFuncSetAttribute(k_join<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4));
+        join_attr = true;
+    }
     tic(c);
-    if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 0, c->stream>>>((uint32_t)L, a);
+    if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 4 * run_cap, c->stream>>>((uint32_t)L, a);
     toc(c);
     b->j_relaunch_needed = true;
     return launch_check(c, "k_join");

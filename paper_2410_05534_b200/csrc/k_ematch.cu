@@ -479,7 +479,7 @@ __device__ uint32_t block_products(const Src* src, int S, const uint32_t* lo, co
 }
 
 
-constexpr uint32_t JOIN_SMEM_KEYS = 4096;   // source-1 index sorted in shared memory
+constexpr uint32_t JOIN_SMEM_KEYS = 2048;   // source-1 index sorted in shared memory
 
 // Block-wide bitonic sort of n (power of two) u64 keys in shared memory.
 __device__ void block_bitonic(unsigned long long* k, uint32_t n) {
@@ -628,25 +628,55 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         const uint32_t wlo = group_start_at_or_after(src[0], min(n0, warp * chw));
         const uint32_t whi = group_start_at_or_after(src[0], min(n0, (warp + 1) * chw));
         const JoinPlan& jp = sh_plan;
+        // run table: for join value x, its run of source-1 records in the sorted index is
+        // [run[x] & 0xFFFF, +run[x] >> 16) -- an O(1) lookup instead of two binary searches
+        extern __shared__ uint32_t jrun[];
+        const uint32_t U = a.id_base ? (uint32_t)(a.id_base[l + 1] - a.id_base[l]) : 0u;
+        const bool use_run = U > 0 && U <= a.run_cap && n1 <= 0xFFFF;
+        if (use_run) {
+            for (uint32_t x = tid; x < U; x += T) jrun[x] = 0;
+            __syncthreads();
+            for (uint32_t q = tid; q < n1; q += T) {
+                const uint32_t x = (uint32_t)(sh_keys[q] >> 32);
+                if (q == 0 || (uint32_t)(sh_keys[q - 1] >> 32) != x) {
+                    uint32_t e = q + 1;
+                    while (e < n1 && (uint32_t)(sh_keys[e] >> 32) == x) e++;
+                    jrun[x] = q | ((e - q) << 16);
+                }
+            }
+            __syncthreads();
+        }
+        __shared__ uint32_t sh_m1[NW][MAX_W];
         auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
             uint32_t n = 0;
+            uint32_t* m1s = sh_m1[warp];
             for (uint32_t g = wlo; g < whi;) {
                 const uint32_t ge = group_end(src[0], g);
                 const uint32_t gstart = n;
                 for (uint32_t i = g; i < ge; i++) {
                     const uint32_t* m1 = w0 + (uint64_t)i * W0;
-                    const uint32_t x = m1[1 + v0];
-                    const uint32_t p0 = lower_bound_key(sh_keys, n1, (unsigned long long)x << 32);
-                    const uint32_t p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
+                    __syncwarp();
+                    if (lane < W0) m1s[lane] = m1[lane];
+                    __syncwarp();
+                    const uint32_t x = m1s[1 + v0];
+                    uint32_t p0, p1;
+                    if (use_run) {
+                        const uint32_t rr = x < U ? jrun[x] : 0u;
+                        p0 = rr & 0xFFFFu;
+                        p1 = p0 + (rr >> 16);
+                    } else {
+                        p0 = lower_bound_key(sh_keys, n1, (unsigned long long)x << 32);
+                        p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
+                    }
                     for (uint32_t base = p0; base < p1; base += 32) {
                         const uint32_t p = base + lane;
                         bool ok = p < p1;
                         const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)sh_keys[p] * W1 : w1;
-                        for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1[jp.c0[c]] == m2[jp.c1[c]];
+                        for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.c1[c]];
                         const uint32_t mask = __ballot_sync(0xffffffffu, ok);
                         if (out && ok) {
                             uint32_t* o = out + (uint64_t)(n + __popc(mask & ((1u << lane) - 1u))) * W;
-                            for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.idx[w]] : m1[jp.idx[w]];
+                            for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.idx[w]] : m1s[jp.idx[w]];
                         }
                         n += __popc(mask);
                     }

@@ -43,6 +43,8 @@ struct JArgs {
     uint32_t* count;            // [R][L]
     uint64_t* off;
     uint32_t* overflow;
+    const uint64_t* id_base;    // per-leaf id bases (run-table size)
+    uint32_t run_cap;           // dynamic SMEM run-table entries
 };
 
 template <int T> __global__ void k_ematch(Dev, MArgs);
