@@ -106,13 +106,19 @@ __device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, d
                     for (int t = 0; t < 4; t++) {
                         const uint32_t w = 4 * w4 + t;
                         uint32_t o = w2[t] & (w1[t] | bit_of(c1, w));
-                        while (o) {
-                            const int bpos = __ffs(o) - 1;
-                            m = pymax(m, h2.vals[rank2 + __popc(w2[t] & ((1u << bpos) - 1u))]);
-                            ov++;
-                            o &= o - 1;
+                        const uint32_t pc = __popc(w2[t]);
+                        if (o == w2[t]) {   // the whole word overlaps: max over a contiguous value run
+                            for (uint32_t i = 0; i < pc; i++) m = pymax(m, h2.vals[rank2 + i]);
+                            ov += pc;
+                        } else {
+                            while (o) {
+                                const int bpos = __ffs(o) - 1;
+                                m = pymax(m, h2.vals[rank2 + __popc(w2[t] & ((1u << bpos) - 1u))]);
+                                ov++;
+                                o &= o - 1;
+                            }
                         }
-                        rank2 += __popc(w2[t]);
+                        rank2 += pc;
                     }
                 }
                 cc2 = pymax(child_cost(c, c2) - m, 0.0);
@@ -155,8 +161,20 @@ __device__ void ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2
 #pragma unroll
         for (int t = 0; t < 4; t++) {
             const uint32_t w = 4 * w4 + t;
-            uint32_t ow = w1[t] | w2[t] | bit_of(c1, w) | (c2 != NONE ? bit_of(c2, w) : 0u);
+            const uint32_t sp = bit_of(c1, w) | (c2 != NONE ? bit_of(c2, w) : 0u);
+            uint32_t ow = w1[t] | w2[t] | sp;
             wo[t] = ow;
+            if (!sp && !(w1[t] & w2[t]) && (!w1[t] || !w2[t])) {
+                // word owned by one source and no special key: contiguous value copy
+                const uint32_t n1w = __popc(w1[t]), n2w = __popc(w2[t]);
+                const double* src = n1w ? h1.vals + rank1 : h2.vals + rank2;
+                const uint32_t cnt = n1w ? n1w : n2w;
+                for (uint32_t i = 0; i < cnt; i++) ovals[o + i] = src[i];
+                o += cnt;
+                rank1 += n1w;
+                rank2 += n2w;
+                continue;
+            }
             while (ow) {
                 const int bpos = __ffs(ow) - 1;
                 const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
