@@ -99,7 +99,7 @@ struct esat_batch {
     uint32_t upload_gen = 0, m_mode = 0, m_Pcap = 0, j_Rcap = 0, m_smem = 0;
     uint32_t j_nsrc = 0, j_nmap_v = 0, j_nmap_q = 0;
     bool m_verified = false, m_pending = false, j_verified = false, j_pending = false;
-    bool j_relaunch_needed = false, m_sig_matches_join = false;
+    bool j_relaunch_needed = false, m_sig_matches_join = false, m_sized = false, j_sized = false;
     std::vector<uint32_t> m_sig, j_sig;
 };
 
@@ -612,16 +612,27 @@ static int join_launch(esat_batch* b);
 static int join_settle(esat_batch* b);
 
 // Resolve optimistic (unchecked) e-match / join launches: verify capacities, redo on overflow.
+// Called before any consumer of the match lists (downloads); a join issued after the e-match is
+// relaunched when the e-match had to be redone.
 static int verify_matches(esat_batch* b) {
     int r;
+    bool redo = false;
     if (b->m_pending) {
-        const bool redo_join = b->j_pending || b->j_R;
-        if ((r = ematch_settle(b))) return r;
-        if (redo_join && b->j_R && b->j_relaunch_needed) { if ((r = join_launch(b))) return r; }
+        esat_ctx* c = b->ctx;
+        uint32_t over = 0;
+        CK(c, cudaMemcpyAsync(&over, b->d_over, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+        b->m_pending = false;
+        if (over) {   // regrow from the recorded totals and relaunch until it fits
+            redo = true;
+            if ((r = ematch_settle(b))) return r;
+        }
     }
-    if (b->j_pending) {
+    if (b->j_R && (redo || b->j_pending)) {
+        if (redo && (r = join_launch(b))) return r;
         if ((r = join_settle(b))) return r;
     }
+    b->j_pending = false;
     return ESAT_OK;
 }
 
@@ -636,17 +647,14 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     const uint64_t L = b->L;
     int r;
     if ((r = ensure_match_meta(b))) return r;
-    // Re-issuing a verified call on the same upload, patterns and symbol table reproduces the same
-    // output sizes (the clean view is a pure function of the upload), so it runs without a host
-    // round-trip; any other call is checked synchronously and regrown on overflow.
+    // Pattern list / programs / symbols unchanged -> no host->device traffic. Capacities are
+    // sized by one checked launch per batch; later launches run without a host round-trip and
+    // are verified lazily (verify_matches) before any consumer reads the lists.
     std::vector<uint32_t> sig(pat_ids, pat_ids + P);
     sig.push_back((uint32_t)mode);
-    sig.push_back(b->upload_gen);
     sig.push_back(c->pat_gen);
     sig.push_back(c->sym_gen);
-    const bool same = b->m_verified && sig == b->m_sig;
-    if (!same) b->m_sig_matches_join = false;
-    if (!same) {
+    if (sig != b->m_sig) {
         if (P > b->m_Pcap) {
             cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_off); cudaFree(b->d_m_W);
             b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
@@ -680,16 +688,19 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
         const uint32_t cap_bytes = 100 * 1024;
         b->m_smem = (uint32_t)(mx < cap_bytes ? mx : cap_bytes);
         if (getenv("ESAT_EMATCH_NOSTAGE")) b->m_smem = 0;
+        b->m_sig = sig;
+        b->m_sized = false;
     }
     b->m_P = P;
     b->m_mode = mode;
     b->j_R = 0;   // a new match call invalidates earlier join results
+    b->j_pending = false;
     if ((r = ematch_launch(b))) return r;
     if (mode == ESAT_MATCH_EXISTS) { b->m_pending = false; return ESAT_OK; }
-    if (same) return ESAT_OK;   // deterministic re-issue of a verified call
-    b->m_verified = false;
+    if (b->m_sized) { b->m_pending = true; return ESAT_OK; }
     if ((r = ematch_settle(b))) return r;
-    b->m_sig = sig;
+    b->m_pending = false;
+    b->m_sized = true;
     return ESAT_OK;
 }
 
@@ -769,14 +780,8 @@ int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t
     spec.insert(spec.end(), qmap, qmap + nmap_q);
     spec.insert(spec.end(), nv, nv + R);
     spec.insert(spec.end(), nq, nq + R);
-    std::vector<uint32_t> sig = spec;
-    sig.push_back(b->upload_gen);
-    sig.push_back(c->sym_gen);
-    const bool same = b->j_verified && sig == b->j_sig && b->m_sig_matches_join;
     int r_;
-    if (!same) {
-        // the source lists must be final before a checked join
-        if (b->m_pending && (r_ = ematch_settle(b))) return r_;
+    if (spec != b->j_sig) {
         if ((r_ = regrow(c, &b->d_jspec, &b->jspec_cap, spec.size()))) return r_;
         CK(c, cudaMemcpyAsync(b->d_jspec, spec.data(), 4 * spec.size(), cudaMemcpyHostToDevice, c->stream));
         if (R > b->j_Rcap) {
@@ -787,15 +792,23 @@ int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t
             b->j_Rcap = R;
         }
         if (!b->j_cap && (r_ = regrow(c, &b->j_out, &b->j_cap, 4 * b->N + 4096))) return r_;
+        b->j_sig = spec;
+        b->j_sized = false;
     }
     b->j_W = jW;
     b->j_R = R; b->j_nsrc = nsrc; b->j_nmap_v = nmap_v; b->j_nmap_q = nmap_q;
+    if (!b->j_sized) {   // sizing launch: needs settled sources
+        b->j_R = 0;
+        if ((r_ = verify_matches(b))) return r_;
+        b->j_R = R;
+        if ((r_ = join_launch(b))) return r_;
+        if ((r_ = join_settle(b))) return r_;
+        b->j_sized = true;
+        b->j_pending = false;
+        return ESAT_OK;
+    }
     if ((r_ = join_launch(b))) return r_;
-    if (same) return ESAT_OK;   // deterministic re-issue of a verified join
-    b->j_verified = false;
-    if ((r_ = join_settle(b))) return r_;
-    b->j_sig = sig;
-    b->m_sig_matches_join = true;
+    b->j_pending = true;
     return ESAT_OK;
 }
 
