@@ -325,14 +325,22 @@ def main():
         stage_ms["ematch"] += e[1].elapsed_time(e[2])
         stage_ms["join"] += e[2].elapsed_time(e[3])
         stage_ms["extract_tail"] = stage_ms.get("extract_tail", 0.0) + e[3].elapsed_time(e[4])
-    # the overlapped extraction kernel alone, timed on its own launches (same inputs, untimed region)
-    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    x0.record(stream)
-    for _ in range(K_EXTRACT := max(3, args.steps // 2)):
-        pipe.extract()
-    x1.record(stream)
-    torch.cuda.synchronize()
-    stage_ms["extract"] = x0.elapsed_time(x1) / K_EXTRACT * args.steps
+    # every kernel alone on its own launches (same inputs, outside the timed region): the roofline
+    # and the dominant kernel use these; stage_ms above are the overlapped in-step intervals
+    def time_alone(fn, reps):
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        x0.record(stream)
+        for _ in range(reps):
+            fn()
+        x1.record(stream)
+        torch.cuda.synchronize()
+        return x0.elapsed_time(x1) / reps
+
+    reps = max(3, min(20, args.steps // 5))
+    kernel_ms = {"rebuild": time_alone(pipe.rebuild, reps), "ematch": time_alone(pipe.match, reps),
+                 "join": time_alone(pipe.join, reps), "extract": time_alone(pipe.extract, reps)}
+    stage_ms["extract"] = stage_ms.pop("extract_tail", 0.0)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -392,8 +400,8 @@ def main():
 
     peak, peak_kind = peaks()
     per_stage = {k: v / K for k, v in stage_ms.items()}
-    dom = max(("rebuild", "ematch", "join", "extract"), key=per_stage.get)
-    achieved = abytes[dom] / (per_stage[dom] / 1e3) / 1e9
+    dom = max(kernel_ms, key=kernel_ms.get)
+    achieved = abytes[dom] / (kernel_ms[dom] / 1e3) / 1e9
     traffic = None
     tr = ROOT / "profiles" / "traffic.json"
     if tr.exists():
@@ -416,10 +424,11 @@ def main():
                    "l2": f"inputs larger than L2 ({(packed['hc_sym'].nbytes * 7) / 1e6:.0f} MB leaf arena per rank)"},
         "matches_per_s": total_matches * world * K / (ms / 1e3),
         "matches_per_step": total_matches * world,
-        "rebuilds_per_s": B * world / (per_stage["rebuild"] / 1e3),
-        "extractions_per_s": B * world / (per_stage["extract"] / 1e3),
-        "ematch_matches_per_s": total_matches * world / ((per_stage["ematch"] + per_stage["join"]) / 1e3),
-        "stage_ms": per_stage,
+        "rebuilds_per_s": B * world / (kernel_ms["rebuild"] / 1e3),
+        "extractions_per_s": B * world / (kernel_ms["extract"] / 1e3),
+        "ematch_matches_per_s": total_matches * world / ((kernel_ms["ematch"] + kernel_ms["join"]) / 1e3),
+        "kernel_ms": kernel_ms,
+        "stage_ms_in_step": per_stage,
         "parity_vs_reference": parity_ok,
         "parity_detail": {"status_nonzero": int(np.sum(ext["status"] != 0)),
                           "cost_mismatch": int(np.sum(ext["root_cost"].view(np.uint64) != exp.view(np.uint64))),
@@ -427,8 +436,10 @@ def main():
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_step": abytes[dom]},
-        "roofline_by_stage": {k: {"achieved_gbs": abytes[k] / (per_stage[k] / 1e3) / 1e9,
-                                  "frac": abytes[k] / (per_stage[k] / 1e3) / 1e9 / peak} for k in abytes},
+        "roofline_by_kernel": {k: {"achieved_gbs": abytes[k] / (kernel_ms[k] / 1e3) / 1e9,
+                                   "frac": abytes[k] / (kernel_ms[k] / 1e3) / 1e9 / peak,
+                                   "traffic": (json.loads(tr.read_text()).get(k) if tr.exists() else None)}
+                               for k in abytes},
         "schedule": "k_rebuild -> [k_extract on a side stream || k_ematch -> k_join] -> join streams",
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": pipe.LAUNCHES_PER_STEP * K,

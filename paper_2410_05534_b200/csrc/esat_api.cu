@@ -577,6 +577,7 @@ static int ematch_launch(esat_batch* b) {
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
     d.sym_par = c->sym_par; d.n_syms = c->n_syms;
     a.smem_bytes = b->m_smem;
+    a.no_flat = getenv("ESAT_EMATCH_GENERIC") ? 1 : 0;
     static uint32_t attr_set = 0;
     const uint32_t cap_bytes = 100 * 1024;
     if (a.smem_bytes > attr_set) {

@@ -120,6 +120,116 @@ __device__ uint32_t match_class(const Matcher& m, uint32_t r, bool first_only, E
     return n;
 }
 
+
+// ---- specialised matcher for patterns of depth <= 2 (all TASO-style sources) -----------------
+// Root App whose children are Vars or Apps over Vars only; <= 4 vars, <= 4 pvars, arity <= 3.
+// No backtracking stack: an odometer over the e-nodes of the App-children classes, bindings
+// held in registers (constant-indexed), re-derived per combination. Same match set as
+// match_class (order differs; the per-root sort makes the output identical).
+struct Flat2 {
+    int32_t ok, name, arity, nslots, V, Q;
+    int32_t slots[4];
+    int32_t ck[3], cv[3], cname[3], car[3], cns[3];
+    int32_t cslots[3][4], gv[3][3];
+};
+
+__device__ void decode_flat2(const int32_t* pg, Flat2& f) {
+    f.ok = 0;
+    const int32_t P = pg[0], V = pg[1], Q = pg[2];
+    const int32_t* r0 = pg + 3;
+    if (r0[0] != 1 || V > 4 || Q > 4 || r0[2] > 3 || r0[3] > 4) return;
+    f.name = r0[1]; f.arity = r0[2]; f.nslots = r0[3]; f.V = V; f.Q = Q;
+    for (int i = 0; i < 4; i++) f.slots[i] = i < f.nslots ? pg[r0[4] + i] : 0;
+    const int32_t* kids = pg + r0[5];
+    for (int j = 0; j < 3; j++) { f.ck[j] = 0; f.cv[j] = 0; f.cname[j] = 0; f.car[j] = 0; f.cns[j] = -1; }
+    for (int j = 0; j < f.arity; j++) {
+        const int32_t* rc = pg + 3 + 6 * kids[j];
+        if (rc[0] == 0) { f.ck[j] = 0; f.cv[j] = rc[1]; continue; }
+        if (rc[2] > 3 || rc[3] > 4) return;
+        f.ck[j] = 1; f.cname[j] = rc[1]; f.car[j] = rc[2]; f.cns[j] = rc[3];
+        for (int i = 0; i < 4; i++) f.cslots[j][i] = i < rc[3] ? pg[rc[4] + i] : 0;
+        const int32_t* gk = pg + rc[5];
+        for (int g = 0; g < rc[2]; g++) {
+            const int32_t* rg = pg + 3 + 6 * gk[g];
+            if (rg[0] != 0) return;   // depth > 2
+            f.gv[j][g] = rg[1];
+        }
+    }
+    (void)P;
+    f.ok = 1;
+}
+
+__device__ __forceinline__ bool bind4(uint32_t (&a)[4], uint32_t& set, int idx, uint32_t val) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+        if (i == idx) {
+            if ((set >> i) & 1u) ok = a[i] == val;
+            else { a[i] = val; set |= 1u << i; }
+        }
+    return ok;
+}
+
+__device__ __forceinline__ bool slots_ok(const Matcher& m, uint32_t sym, int32_t nslots, const int32_t* slots,
+                                         uint32_t (&pv)[4], uint32_t& pset) {
+    if (nslots < 0) return true;
+    const uint32_t p0 = m.s_poff[sym];
+    if ((int32_t)(m.s_poff[sym + 1] - p0) != nslots) return false;
+    for (int j = 0; j < nslots; j++) {
+        const int32_t sl = slots[j], av = m.s_par[p0 + j];
+        if (sl >= 0) { if (sl != av) return false; }
+        else if (!bind4(pv, pset, -sl - 1, (uint32_t)av)) return false;
+    }
+    return true;
+}
+
+template <typename Emit>
+__device__ uint32_t match_class_flat2(const Matcher& m, const Flat2& f, uint32_t r, Emit emit) {
+    uint32_t n = 0;
+    const uint32_t rid = m.cls_id[r];
+    for (uint32_t nd = m.cls_off[r]; nd < m.cls_off[r + 1]; nd++) {
+        const uint32_t s = m.nd_sym[nd];
+        if ((int32_t)m.s_name[s] != f.name || (int32_t)m.s_arity[s] != f.arity) continue;
+        uint32_t pv0[4] = {0, 0, 0, 0}, ps0 = 0;
+        if (!slots_ok(m, s, f.nslots, f.slots, pv0, ps0)) continue;
+        uint32_t kc[3] = {0, 0, 0};
+        const uint32_t k0 = m.nd_koff[nd];
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            if (j < f.arity) kc[j] = m.nd_kpos[k0 + j];
+        // child j: a Var binds its class; an App iterates the matching e-nodes of its class.
+        // Nested loops with early rejection at each level; bindings copied per level (registers).
+        auto child = [&](int j, uint32_t (&vars)[4], uint32_t& vset, uint32_t (&pv)[4], uint32_t& pset,
+                         auto&& next) {
+            if (j >= f.arity) { next(vars, vset, pv, pset); return; }
+            if (!f.ck[j]) {
+                uint32_t v2[4] = {vars[0], vars[1], vars[2], vars[3]}, vs2 = vset;
+                if (bind4(v2, vs2, f.cv[j], m.cls_id[kc[j]])) next(v2, vs2, pv, pset);
+                return;
+            }
+            for (uint32_t cn = m.cls_off[kc[j]]; cn < m.cls_off[kc[j] + 1]; cn++) {
+                const uint32_t cs = m.nd_sym[cn];
+                if ((int32_t)m.s_name[cs] != f.cname[j] || (int32_t)m.s_arity[cs] != f.car[j]) continue;
+                uint32_t p2[4] = {pv[0], pv[1], pv[2], pv[3]}, ps2 = pset;
+                if (!slots_ok(m, cs, f.cns[j], f.cslots[j], p2, ps2)) continue;
+                uint32_t v2[4] = {vars[0], vars[1], vars[2], vars[3]}, vs2 = vset;
+                const uint32_t g0 = m.nd_koff[cn];
+                bool ok = true;
+#pragma unroll
+                for (int g = 0; g < 3; g++)
+                    if (ok && g < f.car[j]) ok = bind4(v2, vs2, f.gv[j][g], m.cls_id[m.nd_kpos[g0 + g]]);
+                if (ok) next(v2, vs2, p2, ps2);
+            }
+        };
+        uint32_t vars[4] = {0, 0, 0, 0}, vset = 0;
+        auto leafc = [&](uint32_t (&v)[4], uint32_t&, uint32_t (&p)[4], uint32_t&) { n++; emit(rid, v, p); };
+        auto lvl2 = [&](uint32_t (&v)[4], uint32_t& vs, uint32_t (&p)[4], uint32_t& ps) { child(2, v, vs, p, ps, leafc); };
+        auto lvl1 = [&](uint32_t (&v)[4], uint32_t& vs, uint32_t (&p)[4], uint32_t& ps) { child(1, v, vs, p, ps, lvl2); };
+        child(0, vars, vset, pv0, ps0, lvl1);
+    }
+    return n;
+}
+
 __device__ __forceinline__ int cmpw(const uint32_t* a, const uint32_t* b, uint32_t W) {
     for (uint32_t i = 0; i < W; i++)
         if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
@@ -276,6 +386,7 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     // reference's sort order by root); pass 2 writes each pair's records at its offset and
     // sorts + dedups them in place (rewrite.py:420-433).
     __shared__ uint32_t sp_off[MAXP], sp_W[MAXP], sp_rbit[MAXP], sp_dup[MAXP];
+    __shared__ Flat2 sp_flat[MAXP];
     __shared__ uint32_t sp_rbase[MAXP + 1];
     __shared__ unsigned long long sp_wbase[MAXP];
     const uint32_t P = a.P;
@@ -292,6 +403,11 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
             sp_dup[pi] = 0;
         }
     }
+    for (uint32_t pi = tid; pi < P; pi += T) {
+        const uint32_t pid = a.pat_ids[pi];
+        decode_flat2(a.prog + a.prog_off[pid], sp_flat[pi]);
+        if (a.no_flat) sp_flat[pi].ok = 0;
+    }
     __syncthreads();
     auto prog_ptr = [&](uint32_t pi) -> const int32_t* { return (progs_smem ? sprog : a.prog) + sp_off[pi]; };
     const uint32_t PC = P * C;
@@ -301,8 +417,12 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         uint32_t n = 0;
         const uint32_t rb = sp_rbit[pi];
         if (!rb || (cmask[r] & rb)) {
-            set_prog(prog_ptr(pi));
-            n = match_class(m, r, false, nothing);
+            if (sp_flat[pi].ok) {
+                n = match_class_flat2(m, sp_flat[pi], r, [](uint32_t, const uint32_t (&)[4], const uint32_t (&)[4]) {});
+            } else {
+                set_prog(prog_ptr(pi));
+                n = match_class(m, r, false, nothing);
+            }
         }
         pc[i] = n;
     }
@@ -358,13 +478,26 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
             set_prog(prog_ptr(pi));
             uint32_t* o0 = a.out + sp_wbase[pi] + (uint64_t)(beg - sp_rbase[pi]) * W;
             uint32_t cur = 0;
-            match_class(m, r, false, [&](uint32_t root, const uint32_t* vars, const int32_t* pv) {
-                uint32_t* o = o0 + (uint64_t)cur * W;
-                o[0] = root;
-                for (int v = 0; v < m.V; v++) o[1 + v] = vars[v];
-                for (int q = 0; q < m.Q; q++) o[1 + m.V + q] = (uint32_t)pv[q];
-                cur++;
-            });
+            if (sp_flat[pi].ok) {
+                const Flat2& f = sp_flat[pi];
+                match_class_flat2(m, f, r, [&](uint32_t root, const uint32_t (&vars)[4], const uint32_t (&pv)[4]) {
+                    uint32_t* o = o0 + (uint64_t)cur * W;
+                    o[0] = root;
+#pragma unroll
+                    for (int v = 0; v < 4; v++) if (v < f.V) o[1 + v] = vars[v];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) if (q < f.Q) o[1 + f.V + q] = pv[q];
+                    cur++;
+                });
+            } else {
+                match_class(m, r, false, [&](uint32_t root, const uint32_t* vars, const int32_t* pv) {
+                    uint32_t* o = o0 + (uint64_t)cur * W;
+                    o[0] = root;
+                    for (int v = 0; v < m.V; v++) o[1 + v] = vars[v];
+                    for (int q = 0; q < m.Q; q++) o[1 + m.V + q] = (uint32_t)pv[q];
+                    cur++;
+                });
+            }
             if (cur > 1) {
                 const uint32_t u = sort_unique(o0, cur, W);
                 if (u != cur) {   // duplicate bindings from different e-nodes: mark the gap
