@@ -275,7 +275,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
-    OWN(x.hoff, 2 * N); OWN(x.hvoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.chg, 2 * N);
+    OWN(x.hoff, 2 * N); OWN(x.hvoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N);
     OWN(x.need, N); OWN(x.lnode, N); OWN(x.lcls, N); OWN(x.lvn, NL); OWN(x.nval, N); OWN(x.naux, 2 * N);
     x.slot_stride = N;
     *out = b;

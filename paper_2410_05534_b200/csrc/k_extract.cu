@@ -28,9 +28,9 @@ namespace esat {
 namespace {
 
 struct Hist {
-    const uint32_t* bits;   // NW words (only when present)
+    const uint32_t* bits;   // NW words (only when present); words outside [4*lo4, 4*hi4) are zero
     const double* vals;     // n values in key order
-    uint32_t n;
+    uint32_t n, lo4, hi4;   // value count, occupied uint4-group range
     bool present;
 };
 
@@ -41,7 +41,7 @@ struct LeafCtx {
     const double *ncost, *cost, *prev;
     const uint32_t* pk;        // bitset pool (leaf base applied)
     const double* pv;          // value pool
-    const uint32_t *hoff[2], *hvoff[2], *hlen[2];
+    const uint32_t *hoff[2], *hvoff[2], *hlen[2], *hrng[2];
 };
 
 __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
@@ -49,7 +49,7 @@ __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
 }
 
 __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
-    Hist h{nullptr, nullptr, 0u, false};
+    Hist h{nullptr, nullptr, 0u, 0u, 0u, false};
     if (c.C == 1) return h;                       // no flush ever happens with one class
     int par;
     if (j < c.k) par = c.pass & 1;                // flushed earlier in this pass
@@ -58,12 +58,21 @@ __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
     h.bits = c.pk + c.hoff[par][j];
     h.vals = c.pv + c.hvoff[par][j];
     h.n = c.hlen[par][j];
+    const uint32_t rg = c.hrng[par][j];
+    h.lo4 = rg & 0xFFFFu;
+    h.hi4 = rg >> 16;
     h.present = true;
     return h;
 }
 
 __device__ __forceinline__ bool hbit(const Hist& h, uint32_t key) {
-    return h.present && ((h.bits[key >> 5] >> (key & 31)) & 1u);
+    const uint32_t g = key >> 7;
+    return h.present && g >= h.lo4 && g < h.hi4 && ((h.bits[key >> 5] >> (key & 31)) & 1u);
+}
+
+__device__ __forceinline__ uint4 hword4(const Hist& h, uint32_t w4) {
+    return (h.present && w4 >= h.lo4 && w4 < h.hi4) ? reinterpret_cast<const uint4*>(h.bits)[w4]
+                                                    : make_uint4(0, 0, 0, 0);
 }
 
 __device__ __forceinline__ uint32_t bit_of(uint32_t key, uint32_t w) {
@@ -96,11 +105,10 @@ __device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, d
                 double m = 0.0;
                 uint32_t ov = 0, rank2 = 0;
                 const uint4* b2v = reinterpret_cast<const uint4*>(h2.bits);
-                const uint4* b1v = reinterpret_cast<const uint4*>(h1.bits);
-                for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) {
+                for (uint32_t w4 = h2.lo4; w4 < h2.hi4; w4++) {
                     const uint4 q2 = b2v[w4];
                     if (!(q2.x | q2.y | q2.z | q2.w)) continue;
-                    const uint4 q1 = h1.present ? b1v[w4] : make_uint4(0, 0, 0, 0);
+                    const uint4 q1 = hword4(h1, w4);
                     const uint32_t w2[4] = {q2.x, q2.y, q2.z, q2.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
                     for (int t = 0; t < 4; t++) {
@@ -136,26 +144,26 @@ __device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, d
 }
 
 // Materialise the history of an arity <= 2 node: bitset at ob (NW words), values at ovals.
-__device__ void ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2, bool skip2, uint32_t* ob,
-                           double* ovals) {
+// Only the occupied uint4-group range is written; it is returned packed as lo4 | hi4 << 16.
+__device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2, bool skip2, uint32_t* ob,
+                               double* ovals) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
     uint4* obv = reinterpret_cast<uint4*>(ob);
-    if (a == 0) {
-        for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) obv[w4] = make_uint4(0, 0, 0, 0);
-        return;
-    }
+    if (a == 0) return 0u;
     const uint32_t c1 = c.kpos[q0];
     const Hist h1 = child_hist(c, c1);
-    Hist h2{nullptr, nullptr, 0u, false};
+    Hist h2{nullptr, nullptr, 0u, 0u, 0u, false};
     uint32_t c2 = NONE;
     if (a == 2 && !skip2) { c2 = c.kpos[q0 + 1]; h2 = child_hist(c, c2); }
+    uint32_t lo = c1 >> 7, hi = (c1 >> 7) + 1;
+    if (c2 != NONE) { lo = min(lo, c2 >> 7); hi = max(hi, (c2 >> 7) + 1); }
+    if (h1.present && h1.hi4 > h1.lo4) { lo = min(lo, h1.lo4); hi = max(hi, h1.hi4); }
+    if (h2.present && h2.hi4 > h2.lo4) { lo = min(lo, h2.lo4); hi = max(hi, h2.hi4); }
     // keys {h1, c1, h2, c2}; values: c1 -> cc1, c2 -> cc2, h1 wins over h2 (first writer)
     uint32_t o = 0, rank1 = 0, rank2 = 0;
-    const uint4* b1v = reinterpret_cast<const uint4*>(h1.bits);
-    const uint4* b2v = reinterpret_cast<const uint4*>(h2.bits);
-    for (uint32_t w4 = 0; w4 < c.NW / 4; w4++) {
-        const uint4 q1 = h1.present ? b1v[w4] : make_uint4(0, 0, 0, 0);
-        const uint4 q2 = h2.present ? b2v[w4] : make_uint4(0, 0, 0, 0);
+    for (uint32_t w4 = lo; w4 < hi; w4++) {
+        const uint4 q1 = hword4(h1, w4);
+        const uint4 q2 = hword4(h2, w4);
         const uint32_t w1[4] = {q1.x, q1.y, q1.z, q1.w}, w2[4] = {q2.x, q2.y, q2.z, q2.w};
         uint32_t wo[4];
 #pragma unroll
@@ -191,6 +199,7 @@ __device__ void ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2
         }
         obv[w4] = make_uint4(wo[0], wo[1], wo[2], wo[3]);
     }
+    return lo | (hi << 16);
 }
 
 // Generic-arity OCF node (n-ary sink): the running history is rebuilt in the pool child by
@@ -211,7 +220,8 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
         if (h.present) {
             uint32_t rank = 0;
             for (uint32_t w = 0; w < NW; w++) {
-                const uint32_t bw = h.bits[w], Hw = hb != NONE ? pk[hb + w] : 0u;
+                const uint32_t bw = (w >> 2) >= h.lo4 && (w >> 2) < h.hi4 ? h.bits[w] : 0u;
+                const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u;
                 uint32_t o = bw & Hw;
                 while (o) {
                     const int bpos = __ffs(o) - 1;
@@ -232,7 +242,8 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
         }
         uint32_t o = 0, r0 = 0, r1 = 0;
         for (uint32_t w = 0; w < NW; w++) {
-            const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u, bw = h.present ? h.bits[w] : 0u;
+            const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u;
+            const uint32_t bw = (h.present && (w >> 2) >= h.lo4 && (w >> 2) < h.hi4) ? h.bits[w] : 0u;
             uint32_t ow = Hw | bw | bit_of(ck, w);
             pk[nb + w] = ow;
             while (ow) {
@@ -284,6 +295,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
     uint32_t* hoffw[2] = {nullptr, nullptr};
     uint32_t* hvoffw[2] = {nullptr, nullptr};
     uint32_t* hlenw[2] = {nullptr, nullptr};
+    uint32_t* hrngw[2] = {nullptr, nullptr};
     uint32_t* pkw = nullptr;
     double* pvw = nullptr;
     if (ocf) {
@@ -298,7 +310,8 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
             hoffw[p] = x.hoff + p * x.slot_stride + b;
             hvoffw[p] = x.hvoff + p * x.slot_stride + b;
             hlenw[p] = x.hlen + p * x.slot_stride + b;
-            c.hoff[p] = hoffw[p]; c.hvoff[p] = hvoffw[p]; c.hlen[p] = hlenw[p];
+            hrngw[p] = x.hrng + p * x.slot_stride + b;
+            c.hoff[p] = hoffw[p]; c.hvoff[p] = hvoffw[p]; c.hlen[p] = hlenw[p]; c.hrng[p] = hrngw[p];
         }
     }
 
@@ -404,6 +417,7 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                         hoffw[par][k] = hoffw[ppar][k];
                         hvoffw[par][k] = hvoffw[ppar][k];
                         hlenw[par][k] = hlenw[ppar][k];
+                        hrngw[par][k] = hrngw[ppar][k];
                     }
                     continue;
                 }
@@ -438,33 +452,36 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                         if (bn == NONE || v < bv) { bv = v; bn = nd; }
                     }
                     if (C > 1) {
-                        uint32_t offk = NONE, offv = 0;
+                        uint32_t offk = NONE, offv = 0, rng = 0;
                         if (hn != NONE && h_gen && gb != NONE) {
-                            offk = gb; offv = gv;
+                            offk = gb; offv = gv; rng = (NW / 4) << 16;
                         } else if (!(hn != NONE && h_gen)) {
                             if (hn == NONE) hsize = 0;
                             offk = atomicAdd(&sh_topk, NW);
                             offv = atomicAdd(&sh_topv, hsize);
                             if ((uint64_t)offk + NW > capk || (uint64_t)offv + hsize > capv) {
                                 sh_over = 1; offk = NONE;
-                            } else if (hn == NONE) {
-                                uint4* ob = reinterpret_cast<uint4*>(pkw + offk);
-                                for (uint32_t w4 = 0; w4 < NW / 4; w4++) ob[w4] = make_uint4(0, 0, 0, 0);
-                            } else {
-                                ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw + offk, pvw + offv);
+                            } else if (hn != NONE) {
+                                rng = ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw + offk, pvw + offv);
                             }
                         }
-                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; sh_over = 1; }   // status reports it
+                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; rng = 0; sh_over = 1; }   // status reports it
                         hoffw[par][k] = offk;
                         hvoffw[par][k] = offv;
                         hlenw[par][k] = hsize;
+                        hrngw[par][k] = rng;
                         if (!changed) {  // did the flushed history change w.r.t. last pass?
                             const uint32_t ok2 = hoffw[ppar][k], ov2 = hvoffw[ppar][k], n2 = hlenw[ppar][k];
+                            const uint32_t r2 = hrngw[ppar][k];
                             if (n2 != hsize) changed = true;
+                            // same value count; compare the occupied words of both ranges
+                            const uint32_t la = rng & 0xFFFFu, ha = rng >> 16, lb = r2 & 0xFFFFu, hb2 = r2 >> 16;
+                            const uint32_t lo = min(la, lb), hi = max(ha, hb2);
                             const uint4* a4 = reinterpret_cast<const uint4*>(pkw + offk);
                             const uint4* b4 = reinterpret_cast<const uint4*>(pkw + ok2);
-                            for (uint32_t w4 = 0; w4 < NW / 4 && !changed; w4++) {
-                                const uint4 p = a4[w4], q = b4[w4];
+                            for (uint32_t w4 = lo; w4 < hi && !changed; w4++) {
+                                const uint4 p = (w4 >= la && w4 < ha) ? a4[w4] : make_uint4(0, 0, 0, 0);
+                                const uint4 q = (w4 >= lb && w4 < hb2) ? b4[w4] : make_uint4(0, 0, 0, 0);
                                 changed = p.x != q.x || p.y != q.y || p.z != q.z || p.w != q.w;
                             }
                             for (uint32_t i = 0; i < hsize && !changed; i++)
