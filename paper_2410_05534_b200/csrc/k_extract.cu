@@ -21,6 +21,8 @@
 // word operations: membership is a bit test, the overlap of a child's constituents with the
 // node's running history is an AND, the inherited (non-overlapping) constituents an OR, and
 // values are located by popcount ranks -- no searching, no data-dependent merge walks.
+#include <cstdio>
+
 #include "esat_internal.cuh"
 
 namespace esat {
@@ -160,6 +162,8 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
     if (h1.present && h1.hi4 > h1.lo4) { lo = min(lo, h1.lo4); hi = max(hi, h1.hi4); }
     if (h2.present && h2.hi4 > h2.lo4) { lo = min(lo, h2.lo4); hi = max(hi, h2.hi4); }
     // keys {h1, c1, h2, c2}; values: c1 -> cc1, c2 -> cc2, h1 wins over h2 (first writer)
+    const double* v1 = h1.vals;
+    const double* v2 = h2.vals;
     uint32_t o = 0, rank1 = 0, rank2 = 0;
     for (uint32_t w4 = lo; w4 < hi; w4++) {
         const uint4 q1 = hword4(h1, w4);
@@ -175,7 +179,7 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
             if (!sp && !(w1[t] & w2[t]) && (!w1[t] || !w2[t])) {
                 // word owned by one source and no special key: contiguous value copy
                 const uint32_t n1w = __popc(w1[t]), n2w = __popc(w2[t]);
-                const double* src = n1w ? h1.vals + rank1 : h2.vals + rank2;
+                const double* src = n1w ? v1 + rank1 : v2 + rank2;
                 const uint32_t cnt = n1w ? n1w : n2w;
                 for (uint32_t i = 0; i < cnt; i++) ovals[o + i] = src[i];
                 o += cnt;
@@ -189,8 +193,8 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
                 double val;
                 if (key == c1) val = cc1;
                 else if (key == c2) val = cc2;
-                else if ((w1[t] >> bpos) & 1u) val = h1.vals[rank1 + __popc(w1[t] & below)];
-                else val = h2.vals[rank2 + __popc(w2[t] & below)];
+                else if ((w1[t] >> bpos) & 1u) val = v1[rank1 + __popc(w1[t] & below)];
+                else val = v2[rank2 + __popc(w2[t] & below)];
                 ovals[o++] = val;
                 ow &= ow - 1;
             }
@@ -271,7 +275,7 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
 }  // namespace
 
 template <int T>
-__global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
+__global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // <= 64 regs: 32 resident leaves per SM
     const uint32_t l = blockIdx.x, tid = threadIdx.x;
     const uint64_t b = d.nb[l], k0 = d.kb[l];
     const uint32_t C = d.v_C[l];
@@ -326,44 +330,43 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
         x.reach[b + k] = 0;
     }
     if (tid == 0) { sh_over = 0; sh_topk = 0; sh_topv = 0; }
+#ifdef ESAT_DEBUG
+    long long t_start = clock64(), t_lv = 0, t_sort = 0;
+    long long t_pass[8] = {0};
+#endif
     __syncthreads();
     // ---- K7: wavefront levels over lower-position children ----
     // level[k] = 1 + max level of k's lower-position children. Warp 0 walks the classes in
-    // position order 32 at a time: children below the chunk are final; dependencies inside the
-    // chunk are resolved by re-evaluating the chunk until no lane changes (chain length + 1 rounds).
+    // position order 32 at a time: children below the chunk are final (read from memory); a child
+    // inside the chunk is always at a lower lane, so one in-register sweep over the lanes in order
+    // (shuffle-broadcast of each lane's finished level) resolves every in-chunk chain exactly.
     if (tid < 32) {
         uint32_t mx = 0;
         for (uint32_t kb0 = 0; kb0 < C; kb0 += 32) {
             const uint32_t k = kb0 + tid;
-            uint32_t base = 0;
+            uint32_t lv = 0, dep = 0;   // dep: in-chunk children as a lane mask
             if (k < C)
                 for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
                     for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
                         const uint32_t j = c.kpos[q];
-                        if (j < kb0) { const uint32_t t = level[j] + 1; base = t > base ? t : base; }
+                        if (j < kb0) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
+                        else if (j < k) dep |= 1u << (j - kb0);
                     }
-            if (k < C) level[k] = base;
-            __syncwarp();
-            for (;;) {
-                uint32_t lv = base;
-                if (k < C)
-                    for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++)
-                        for (uint32_t q = c.nko[nd]; q < c.nko[nd + 1]; q++) {
-                            const uint32_t j = c.kpos[q];
-                            if (j >= kb0 && j < k) { const uint32_t t = level[j] + 1; lv = t > lv ? t : lv; }
-                        }
-                const bool upd = k < C && lv != level[k];
-                __syncwarp();
-                if (upd) level[k] = lv;
-                __syncwarp();
-                if (!__any_sync(0xffffffffu, upd)) break;
+#pragma unroll 4
+            for (uint32_t i = 0; i < 31; i++) {
+                const uint32_t li = __shfl_sync(0xffffffffu, lv, i);
+                if ((dep >> i) & 1u) lv = li + 1 > lv ? li + 1 : lv;
             }
-            const uint32_t lk = k < C ? level[k] : 0u;
-            mx = max(mx, __reduce_max_sync(0xffffffffu, lk));
+            if (k < C) level[k] = lv;
+            mx = max(mx, __reduce_max_sync(0xffffffffu, k < C ? lv : 0u));
+            __syncwarp();
         }
         if (tid == 0) sh_maxlv = mx;
     }
     __syncthreads();
+#ifdef ESAT_DEBUG
+    t_lv = clock64();
+#endif
     // counting sort of classes by level
     for (uint32_t k = tid; k <= C; k += T) lvcnt[k] = 0;
     __syncthreads();
@@ -384,6 +387,9 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
     __syncthreads();
     // lvcnt[lv] now holds the END of level lv; level lv spans [lv ? lvcnt[lv-1] : 0, lvcnt[lv])
 
+#ifdef ESAT_DEBUG
+    t_sort = clock64();
+#endif
     // ---- K8/K9: Gauss-Seidel passes as level sweeps ----
     const uint64_t cap = 4ull * C + 8;
     const uint32_t NW = c.NW;
@@ -495,6 +501,9 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
             __syncthreads();
         }
         passes++;
+#ifdef ESAT_DEBUG
+        if (passes <= 8) t_pass[passes - 1] = clock64();
+#endif
         const bool any_change = sh_flag != 0;
         __syncthreads();   // everyone has read the flag before thread 0 resets it for the next pass
         if (!any_change) { st = X_OK; break; }
@@ -526,13 +535,23 @@ __global__ void __launch_bounds__(T) k_extract(Dev d, XArgs x) {
                 state[kid] = 1;
                 vs[dpt] = kid; vi[dpt] = 0; dpt++;
             }
-            if (st == X_OK)
-                for (uint32_t k = 0; k < C; k++) state[k] = state[k] == 2 ? 1 : 0;
         }
+#ifdef ESAT_DEBUG
+        if (l < 4 || C > 800 && l < 64)
+            printf("leaf %u C %u nlv %u passes %u: levels %lld sort %lld pass0 %lld pass1 %lld pass2 %lld k10 %lld cyc\n", l, C,
+                   nlv, passes, t_lv - t_start, t_sort - t_lv, t_pass[0] - t_sort, passes > 1 ? t_pass[1] - t_pass[0] : 0ll,
+                   passes > 2 ? t_pass[2] - t_pass[1] : 0ll, clock64() - t_pass[passes > 8 ? 7 : passes - 1]);
+#endif
         x.status[l] = st;
         x.err_class[l] = err;
         x.root_cost[l] = rc;
         x.passes[l] = passes;
+        sh_flag = st;
+    }
+    __syncthreads();
+    if (sh_flag == X_OK) {   // DFS states (2 = visited) -> reachable flags
+        uint8_t* state = x.reach + b;
+        for (uint32_t k = tid; k < C; k += T) state[k] = state[k] == 2 ? 1 : 0;
     }
 }
 
