@@ -118,6 +118,8 @@ int esat_join(esat_batch* b, uint32_t n_rules, const uint32_t* src_off, const ui
 /* greedy extraction (method DEFAULT or OCF) over every leaf; OCF constituent histories live in a
  * per-leaf pool of entries_per_node * n entries per pass parity (ESAT_X_CAPACITY -> grow, retry) */
 int esat_batch_set_pool(esat_batch* b, double entries_per_node);
+/* separate sizing of the f64 contribution pool and the bitset pool (ceil(C/32) words per history) */
+int esat_batch_set_pool2(esat_batch* b, double values_per_node, double bitsets_per_node);
 int esat_extract(esat_batch* b, int method);
 /* the same on the context's side stream: extraction only reads the rebuilt view, so it overlaps
  * esat_ematch / esat_join on the main stream; esat_wait_async joins it back (downloads and

@@ -79,6 +79,7 @@ struct esat_batch {
     std::vector<void*> owned;
     // OCF pool
     double pool_factor = 32.0;   // f64 history entries per e-node
+    double pool_kfactor = 0.0;   // history bitsets per e-node (0: derived from pool_factor)
     std::vector<uint64_t> pb, pbk;
     uint64_t pool_total = 0, pool_ktotal = 0;
     uint64_t *d_pb = nullptr, *d_pbk = nullptr;
@@ -337,7 +338,18 @@ int esat_rebuild(esat_batch* b) {
 int esat_batch_set_pool(esat_batch* b, double entries_per_node) {
     if (!b || !(entries_per_node > 0)) return ESAT_E_ARG;
     b->pool_factor = entries_per_node;
+    b->pool_kfactor = 0.0;
     b->pool_total = 0;  // force re-allocation on the next OCF extraction
+    return ESAT_OK;
+}
+
+int esat_batch_set_pool2(esat_batch* b, double values_per_node, double bitsets_per_node) {
+    if (!b || !(values_per_node > 0) || !(bitsets_per_node > 0)) return ESAT_E_ARG;
+    if (b->pool_factor != values_per_node || b->pool_kfactor != bitsets_per_node) {
+        b->pool_factor = values_per_node;
+        b->pool_kfactor = bitsets_per_node;
+        b->pool_total = 0;
+    }
     return ESAT_OK;
 }
 
@@ -346,7 +358,8 @@ static int ensure_pool(esat_batch* b) {
     if (b->pool_total) return ESAT_OK;
     b->pb.assign(b->L + 1, 0);
     b->pbk.assign(b->L + 1, 0);
-    const double kf = b->pool_factor / 8.0 > 3.0 ? b->pool_factor / 8.0 : 3.0;
+    const double kf = b->pool_kfactor > 0 ? b->pool_kfactor
+                                          : (b->pool_factor / 8.0 > 3.0 ? b->pool_factor / 8.0 : 3.0);
     for (uint32_t l = 0; l < b->L; l++) {
         const uint64_t n = b->nb[l + 1] - b->nb[l];
         const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)

@@ -61,9 +61,11 @@ def lib():
                      "esat_rebuild", "esat_ematch", "esat_join", "esat_extract", "esat_batch_set_pool",
                      "esat_download_rebuild", "esat_download_view", "esat_download_matches",
                      "esat_download_extract", "esat_result_device_ptrs", "esat_ctx_set_stream",
-                     "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork"):
+                     "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork",
+                     "esat_batch_set_pool2"):
             getattr(L, name).restype = C.c_int
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
+        L.esat_batch_set_pool2.argtypes = [vp, C.c_double, C.c_double]
         _lib = L
     return _lib
 
@@ -73,7 +75,8 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_rebuild", "esat_ematch", "esat_join", "esat_batch_set_pool", "esat_extract",
             "esat_download_rebuild", "esat_download_view", "esat_download_matches", "esat_download_extract",
             "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results",
-            "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork")
+            "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork",
+            "esat_batch_set_pool2")
 
 
 def _p(a):
@@ -182,8 +185,12 @@ class DeviceBatch:
     def rebuild(self):
         self.ctx.check(self.L.esat_rebuild(self.h))
 
-    def set_pool(self, entries_per_node: float):
-        self.ctx.check(self.L.esat_batch_set_pool(self.h, C.c_double(entries_per_node)))
+    def set_pool(self, entries_per_node: float, bitsets_per_node: float | None = None):
+        if bitsets_per_node is None:
+            self.ctx.check(self.L.esat_batch_set_pool(self.h, C.c_double(entries_per_node)))
+        else:
+            self.ctx.check(self.L.esat_batch_set_pool2(self.h, C.c_double(entries_per_node),
+                                                       C.c_double(bitsets_per_node)))
 
     def extract(self, method: str):
         self.ctx.check(self.L.esat_extract(self.h, C.c_int(METHODS[method])))
@@ -271,14 +278,18 @@ class DeviceBatch:
         return words, off, cnt
 
 
-def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max_factor: float = 4096.0) -> dict:
-    """Run extraction, growing the OCF history pool on ESAT_X_CAPACITY (host regrow path)."""
+def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max_factor: float = 1 << 16,
+                       bitsets: float = 4.0) -> dict:
+    """Run extraction, growing the OCF history pools on ESAT_X_CAPACITY (host regrow path):
+    contributions x4 and bitset histories x2 per retry."""
+    batch.set_pool(factor, bitsets)
     while True:
         batch.extract(method)
         out = batch.download_extract()
         if method.startswith("ocf") and np.any(out["status"] == X_CAPACITY) and factor < max_factor:
             factor *= 4
-            batch.set_pool(factor)
+            bitsets *= 2
+            batch.set_pool(factor, bitsets)
             continue
         return out
 
