@@ -267,9 +267,7 @@ def main():
         pipe.step()
     torch.cuda.synchronize()
     ext = batch.download_extract()
-    while np.any(ext["status"] == native.X_CAPACITY):   # size the OCF history pool once, outside timing
-        pipe.pool *= 2
-        batch.set_pool(pipe.pool)
+    while pipe.grow_pool(ext):   # size the OCF history pools once, outside timing
         pipe.step()
         ext = batch.download_extract()
     exp = np.asarray(ref_ocf)[src_idx]
@@ -368,7 +366,8 @@ def main():
     # two device batches alternate so step i+1's H2D upload (copy engine) overlaps step i's
     # kernels; every step still uploads its own inputs and reads back its own results
     ctx2 = native.Context(local)
-    pipe2 = LeafPipeline(ctx2, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=pipe.pool)
+    pipe2 = LeafPipeline(ctx2, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=pipe.pool,
+                         pool_bitsets_per_node=pipe.pool_bitsets)
     batch2 = pipe2.load(packed)
     pipe2.step()
     torch.cuda.synchronize()
@@ -432,7 +431,8 @@ def main():
         "parity_vs_reference": parity_ok,
         "parity_detail": {"status_nonzero": int(np.sum(ext["status"] != 0)),
                           "cost_mismatch": int(np.sum(ext["root_cost"].view(np.uint64) != exp.view(np.uint64))),
-                          "ocf_pool_entries_per_node": pipe.pool},
+                          "ocf_pool_entries_per_node": pipe.pool,
+                          "ocf_pool_bitsets_per_node": pipe.pool_bitsets},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_step": abytes[dom]},

@@ -70,7 +70,8 @@ extern "C" {
 #define ESAT_X_CHILD_NOT_CHOSEN 4  /* ExtractionError("child e-class %u required but not chosen") */
 #define ESAT_X_ROOT_NOT_CHOSEN 5   /* ExtractionError("root e-class not chosen") */
 #define ESAT_X_NO_ROOT 6           /* StructuralError("e-graph has no root") */
-#define ESAT_X_CAPACITY 7          /* OCF history pool too small: grow and retry */
+#define ESAT_X_CAPACITY 7          /* OCF history pool too small: grow and retry; err_class holds the
+                                      overflow mask (1: bitset pool, 2: value pool) */
 
 #define ESAT_METHOD_DEFAULT 0
 #define ESAT_METHOD_OCF 1

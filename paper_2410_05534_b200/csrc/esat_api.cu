@@ -364,7 +364,7 @@ static int ensure_pool(esat_batch* b) {
         const uint64_t n = b->nb[l + 1] - b->nb[l];
         const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)
         b->pb[l + 1] = b->pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
-        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * nw + 4 * nw + 64;
+        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * 3 * nw + 12 * nw + 64;   // bits | wmax
     }
     b->pool_total = b->pb[b->L];
     b->pool_ktotal = b->pbk[b->L];

@@ -20,7 +20,12 @@
 // 16-B aligned) plus the f64 contributions in key order. Alg. 2's dictionary operations become
 // word operations: membership is a bit test, the overlap of a child's constituents with the
 // node's running history is an AND, the inherited (non-overlapping) constituents an OR, and
-// values are located by popcount ranks -- no searching, no data-dependent merge walks.
+// values are located by popcount ranks -- no searching, no data-dependent merge walks. Each
+// history block also carries, per bitset word, the Python-max of that word's values (from +0.0):
+// an overlap that covers a whole word then costs one load instead of one per key (the max of
+// Alg. 2's overlap is order-independent: it only ever moves on a strictly greater value).
+//
+// History block layout (3*NW words): bits[NW] | wmax[NW] (f64).
 #include <cstdio>
 
 #include "esat_internal.cuh"
@@ -31,6 +36,7 @@ namespace {
 
 struct Hist {
     const uint32_t* bits;   // NW words (only when present); words outside [4*lo4, 4*hi4) are zero
+    const double* wmax;     // NW per-word value maxima (valid inside the occupied range)
     const double* vals;     // n values in key order
     uint32_t n, lo4, hi4;   // value count, occupied uint4-group range
     bool present;
@@ -51,13 +57,14 @@ __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
 }
 
 __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
-    Hist h{nullptr, nullptr, 0u, 0u, 0u, false};
+    Hist h{nullptr, nullptr, nullptr, 0u, 0u, 0u, false};
     if (c.C == 1) return h;                       // no flush ever happens with one class
     int par;
     if (j < c.k) par = c.pass & 1;                // flushed earlier in this pass
     else if (c.pass == 0) return h;               // not flushed yet
     else par = (c.pass - 1) & 1;                  // last pass's flush
     h.bits = c.pk + c.hoff[par][j];
+    h.wmax = reinterpret_cast<const double*>(h.bits + c.NW);
     h.vals = c.pv + c.hvoff[par][j];
     h.n = c.hlen[par][j];
     const uint32_t rg = c.hrng[par][j];
@@ -117,8 +124,8 @@ __device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, d
                         const uint32_t w = 4 * w4 + t;
                         uint32_t o = w2[t] & (w1[t] | bit_of(c1, w));
                         const uint32_t pc = __popc(w2[t]);
-                        if (o == w2[t]) {   // the whole word overlaps: max over a contiguous value run
-                            for (uint32_t i = 0; i < pc; i++) m = pymax(m, h2.vals[rank2 + i]);
+                        if (o == w2[t]) {   // the whole word overlaps: its stored maximum
+                            m = pymax(m, h2.wmax[w]);
                             ov += pc;
                         } else {
                             while (o) {
@@ -151,10 +158,11 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
                                double* ovals) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
     uint4* obv = reinterpret_cast<uint4*>(ob);
+    double* owm = reinterpret_cast<double*>(ob + c.NW);
     if (a == 0) return 0u;
     const uint32_t c1 = c.kpos[q0];
     const Hist h1 = child_hist(c, c1);
-    Hist h2{nullptr, nullptr, 0u, 0u, 0u, false};
+    Hist h2{nullptr, nullptr, nullptr, 0u, 0u, 0u, false};
     uint32_t c2 = NONE;
     if (a == 2 && !skip2) { c2 = c.kpos[q0 + 1]; h2 = child_hist(c, c2); }
     uint32_t lo = c1 >> 7, hi = (c1 >> 7) + 1;
@@ -182,11 +190,13 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
                 const double* src = n1w ? v1 + rank1 : v2 + rank2;
                 const uint32_t cnt = n1w ? n1w : n2w;
                 for (uint32_t i = 0; i < cnt; i++) ovals[o + i] = src[i];
+                owm[w] = n1w ? h1.wmax[w] : (n2w ? h2.wmax[w] : 0.0);
                 o += cnt;
                 rank1 += n1w;
                 rank2 += n2w;
                 continue;
             }
+            double wm = 0.0;
             while (ow) {
                 const int bpos = __ffs(ow) - 1;
                 const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
@@ -196,8 +206,10 @@ __device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double
                 else if ((w1[t] >> bpos) & 1u) val = v1[rank1 + __popc(w1[t] & below)];
                 else val = v2[rank2 + __popc(w2[t] & below)];
                 ovals[o++] = val;
+                wm = pymax(wm, val);
                 ow &= ow - 1;
             }
+            owm[w] = wm;
             rank1 += __popc(w1[t]);
             rank2 += __popc(w2[t]);
         }
@@ -239,9 +251,10 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
         const double cc = h.present ? pymax(child_cost(c, ck) - m, 0.0) : child_cost(c, ck);
         const bool ck_new = !hbit(h, ck);
         const uint32_t nn = hn + add + (ck_new ? 1u : 0u);
-        const uint32_t nb = atomicAdd(topk, NW), nv = atomicAdd(topv, nn);
-        if ((uint64_t)nb + NW > capk || (uint64_t)nv + nn > capv) {
-            *over = 1; *boff = NONE; *voff = 0; *n_out = 0;
+        const uint32_t nb = atomicAdd(topk, 3 * NW), nv = atomicAdd(topv, nn);
+        if ((uint64_t)nb + 3 * NW > capk || (uint64_t)nv + nn > capv) {
+            atomicOr(over, ((uint64_t)nb + 3 * NW > capk ? 1u : 0u) | ((uint64_t)nv + nn > capv ? 2u : 0u));
+            *boff = NONE; *voff = 0; *n_out = 0;
             return v + cc;
         }
         uint32_t o = 0, r0 = 0, r1 = 0;
@@ -250,6 +263,7 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
             const uint32_t bw = (h.present && (w >> 2) >= h.lo4 && (w >> 2) < h.hi4) ? h.bits[w] : 0u;
             uint32_t ow = Hw | bw | bit_of(ck, w);
             pk[nb + w] = ow;
+            double wm = 0.0;
             while (ow) {
                 const int bpos = __ffs(ow) - 1;
                 const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
@@ -258,8 +272,10 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
                 else if ((Hw >> bpos) & 1u) val = pv[hv + r0 + __popc(Hw & below)];      // H wins (first writer)
                 else val = h.vals[r1 + __popc(bw & below)];
                 pv[nv + o++] = val;
+                wm = pymax(wm, val);
                 ow &= ow - 1;
             }
+            reinterpret_cast<double*>(pk + nb + NW)[w] = wm;
             r0 += __popc(Hw);
             r1 += __popc(bw);
         }
@@ -463,15 +479,17 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                             offk = gb; offv = gv; rng = (NW / 4) << 16;
                         } else if (!(hn != NONE && h_gen)) {
                             if (hn == NONE) hsize = 0;
-                            offk = atomicAdd(&sh_topk, NW);
+                            offk = atomicAdd(&sh_topk, 3 * NW);
                             offv = atomicAdd(&sh_topv, hsize);
-                            if ((uint64_t)offk + NW > capk || (uint64_t)offv + hsize > capv) {
-                                sh_over = 1; offk = NONE;
+                            if ((uint64_t)offk + 3 * NW > capk || (uint64_t)offv + hsize > capv) {
+                                atomicOr(&sh_over, ((uint64_t)offk + 3 * NW > capk ? 1u : 0u) |
+                                                   ((uint64_t)offv + hsize > capv ? 2u : 0u));
+                                offk = NONE;
                             } else if (hn != NONE) {
                                 rng = ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw + offk, pvw + offv);
                             }
                         }
-                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; rng = 0; sh_over = 1; }   // status reports it
+                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
                         hoffw[par][k] = offk;
                         hvoffw[par][k] = offv;
                         hlenw[par][k] = hsize;
@@ -511,18 +529,64 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     if (sh_over) st = X_CAPACITY;
 
     // ---- K10: root check, validation DFS and reachable set (extraction.py:67-115, 149-153) ----
+    // Fast path (warp 0): if every chosen edge reachable from the root points to a lower class
+    // position and every reachable class is chosen, the selection is acyclic and the DFS can
+    // neither fail nor visit anything else -- the reachable set is then one descending sweep of
+    // 32-class chunks (in-chunk parent -> child pushes resolved by a shuffle sweep from the top
+    // lane down). Anything else (an upward or self edge, an unchosen child) falls back to the
+    // sequential DFS, which reports the reference's error class in the reference's order.
+    const uint32_t root = d.v_root[l];
+    if (st == X_OK && root == NONE) st = X_NO_ROOT;
+    if (st == X_OK && !(cost[root] < __longlong_as_double(0x7ff0000000000000ll))) st = X_INFEASIBLE;
+    uint8_t* state = x.reach + b;   // 0 unvisited, 1 on stack, 2 done
+    bool fast = false;
+    if (st == X_OK && tid < 32) {
+        if (tid == 0) state[root] = 2;
+        __syncwarp();
+        bool bad = false;
+        for (int kb0 = (int)((C - 1) & ~31u); kb0 >= 0; kb0 -= 32) {
+            const uint32_t k = (uint32_t)kb0 + tid;
+            uint32_t r = k < C ? state[k] : 0u, cmask = 0;
+            bool up = false;
+            uint32_t q0 = 0, q1 = 0;
+            if (k < C) {
+                const uint32_t nd = ch[k];
+                if (nd != NONE) { q0 = c.nko[nd]; q1 = c.nko[nd + 1]; }
+            }
+            for (uint32_t q = q0; q < q1; q++) {
+                const uint32_t j = c.kpos[q];
+                if (j >= k) up = true;
+                else if (j >= (uint32_t)kb0) cmask |= 1u << (j - kb0);
+            }
+            for (int i = 31; i >= 0; i--) {
+                const uint32_t ri = __shfl_sync(0xffffffffu, r, i), mi = __shfl_sync(0xffffffffu, cmask, i);
+                if (ri && ((mi >> tid) & 1u)) r = 2;
+            }
+            if (r) {
+                if (up) bad = true;
+                for (uint32_t q = q0; q < q1 && !bad; q++) {
+                    const uint32_t j = c.kpos[q];
+                    if (ch[j] == NONE) bad = true;
+                    else if (j < (uint32_t)kb0) state[j] = 2;
+                }
+                state[k] = 2;
+            }
+            __syncwarp();
+        }
+        fast = !__any_sync(0xffffffffu, bad);
+        if (!fast) {
+            for (uint32_t k = tid; k < C; k += 32) state[k] = 0;
+            __syncwarp();
+        }
+    }
     if (tid == 0) {
-        const uint32_t root = d.v_root[l];
         uint32_t err = NONE;
         double rc = __longlong_as_double(0x7ff8000000000000ll);
-        if (st == X_OK && root == NONE) st = X_NO_ROOT;
-        if (st == X_OK && !(cost[root] < __longlong_as_double(0x7ff0000000000000ll))) st = X_INFEASIBLE;
         if (st == X_OK) {
             rc = cost[root];
-            uint8_t* state = x.reach + b;   // 0 unvisited, 1 on stack, 2 done
             uint32_t *vs = x.stk + b, *vi = x.stki + b;
-            uint32_t dpt = 1;
-            vs[0] = root; vi[0] = 0; state[root] = 1;
+            uint32_t dpt = fast ? 0u : 1u;
+            if (!fast) { vs[0] = root; vi[0] = 0; state[root] = 1; }
             while (dpt) {
                 const uint32_t cc = vs[dpt - 1], nd = ch[cc];
                 const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
@@ -542,6 +606,7 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                    nlv, passes, t_lv - t_start, t_sort - t_lv, t_pass[0] - t_sort, passes > 1 ? t_pass[1] - t_pass[0] : 0ll,
                    passes > 2 ? t_pass[2] - t_pass[1] : 0ll, clock64() - t_pass[passes > 8 ? 7 : passes - 1]);
 #endif
+        if (st == X_CAPACITY) err = sh_over;   // 1: bitset pool, 2: value pool
         x.status[l] = st;
         x.err_class[l] = err;
         x.root_cost[l] = rc;

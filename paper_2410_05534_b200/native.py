@@ -280,15 +280,20 @@ class DeviceBatch:
 
 def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max_factor: float = 1 << 16,
                        bitsets: float = 4.0) -> dict:
-    """Run extraction, growing the OCF history pools on ESAT_X_CAPACITY (host regrow path):
-    contributions x4 and bitset histories x2 per retry."""
+    """Run extraction, growing the OCF history pools on ESAT_X_CAPACITY (host regrow path).
+    err_class of an overflowed leaf is the overflow mask: 1 grows the bitset pool x2, 2 grows the
+    contribution pool x4."""
     batch.set_pool(factor, bitsets)
     while True:
         batch.extract(method)
         out = batch.download_extract()
-        if method.startswith("ocf") and np.any(out["status"] == X_CAPACITY) and factor < max_factor:
-            factor *= 4
-            bitsets *= 2
+        over = out["status"] == X_CAPACITY
+        if method.startswith("ocf") and np.any(over) and factor < max_factor:
+            mask = int(np.bitwise_or.reduce(out["err_class"][over]))
+            if mask & 1 or not mask & 3:
+                bitsets *= 2
+            if mask & 2 or not mask & 3:
+                factor *= 4
             batch.set_pool(factor, bitsets)
             continue
         return out

@@ -54,10 +54,11 @@ def compile_rules(rules, name_id, code):
 
 class LeafPipeline:
     def __init__(self, ctx: native.Context, symtab_arrays: dict, rules, name_id, code,
-                 method: str = "ocf", pool_entries_per_node: float = 8.0):
+                 method: str = "ocf", pool_entries_per_node: float = 8.0, pool_bitsets_per_node: float = 2.0):
         self.ctx = ctx
         self.method = method
         self.pool = pool_entries_per_node
+        self.pool_bitsets = pool_bitsets_per_node
         ctx.upload_symtab(symtab_arrays)
         self.programs, self.rules = compile_rules(rules, name_id, code)
         ctx.upload_patterns(self.programs)
@@ -69,9 +70,23 @@ class LeafPipeline:
         if self.batch is not None:
             self.batch.close()
         self.batch = native.DeviceBatch(self.ctx, packed)
-        self.batch.set_pool(self.pool)
+        self.batch.set_pool(self.pool, self.pool_bitsets)
         self.batch.upload(packed)
         return self.batch
+
+    def grow_pool(self, ext: dict) -> bool:
+        """After an extraction that overflowed (ESAT_X_CAPACITY), grow the pool(s) named by the
+        overflow mask in err_class. Returns False when nothing overflowed."""
+        over = ext["status"] == native.X_CAPACITY
+        if not np.any(over):
+            return False
+        mask = int(np.bitwise_or.reduce(ext["err_class"][over]))
+        if mask & 1 or not mask & 3:
+            self.pool_bitsets *= 2
+        if mask & 2 or not mask & 3:
+            self.pool *= 2
+        self.batch.set_pool(self.pool, self.pool_bitsets)
+        return True
 
     # the four stages -------------------------------------------------------------
     def rebuild(self):
