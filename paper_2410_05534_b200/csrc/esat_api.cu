@@ -276,7 +276,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
-    OWN(x.hoff, 2 * N); OWN(x.hvoff, 2 * N); OWN(x.hlen, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N);
+    OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N);
     OWN(x.need, N); OWN(x.lnode, N); OWN(x.lcls, N); OWN(x.lvn, NL); OWN(x.nval, N); OWN(x.naux, 2 * N);
     x.slot_stride = N;
     *out = b;
@@ -364,7 +364,7 @@ static int ensure_pool(esat_batch* b) {
         const uint64_t n = b->nb[l + 1] - b->nb[l];
         const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)
         b->pb[l + 1] = b->pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
-        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * 3 * nw + 12 * nw + 64;   // bits | wmax
+        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * 4 * nw + 16 * nw + 64;   // bits|wptr|wmax
     }
     b->pool_total = b->pb[b->L];
     b->pool_ktotal = b->pbk[b->L];

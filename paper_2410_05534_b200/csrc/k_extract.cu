@@ -17,15 +17,20 @@
 // is skipped (exact dirty skip).
 //
 // Constituent histories are stored as a dense bitset over class positions (ceil(C/32) words,
-// 16-B aligned) plus the f64 contributions in key order. Alg. 2's dictionary operations become
-// word operations: membership is a bit test, the overlap of a child's constituents with the
-// node's running history is an AND, the inherited (non-overlapping) constituents an OR, and
-// values are located by popcount ranks -- no searching, no data-dependent merge walks. Each
-// history block also carries, per bitset word, the Python-max of that word's values (from +0.0):
-// an overlap that covers a whole word then costs one load instead of one per key (the max of
-// Alg. 2's overlap is order-independent: it only ever moves on a strictly greater value).
+// 16-B aligned). Alg. 2's dictionary operations become word operations: membership is a bit
+// test, the overlap of a child's constituents with the node's running history is an AND, the
+// inherited (non-overlapping) constituents an OR, and values are located by popcount ranks.
 //
-// History block layout (3*NW words): bits[NW] | wmax[NW] (f64).
+// Values are shared at word granularity instead of copied: each bitset word w carries a pointer
+// wptr[w] to the f64 values of its keys (key order) in the value pool, and the Python-max of
+// those values wmax[w] (folded from +0.0). A merged history whose word w holds exactly one
+// source's keys (the later source's keys all shadowed by the earlier one, no new key) reuses
+// that source's wptr/wmax; only words that mix sources or hold a new key get fresh values. An
+// overlap that covers a whole word costs one wmax load (the max of Alg. 2's overlap is
+// order-independent: it only ever moves on a strictly greater value, never on NaN).
+//
+// History block (4*NW words): bits[NW] | wptr[NW] | wmax[NW] (f64). An empty history is the
+// empty word range (no block).
 #include <cstdio>
 
 #include "esat_internal.cuh"
@@ -35,10 +40,8 @@ namespace esat {
 namespace {
 
 struct Hist {
-    const uint32_t* bits;   // NW words (only when present); words outside [4*lo4, 4*hi4) are zero
-    const double* wmax;     // NW per-word value maxima (valid inside the occupied range)
-    const double* vals;     // n values in key order
-    uint32_t n, lo4, hi4;   // value count, occupied uint4-group range
+    const uint32_t* bits;   // block base; words outside [4*lo4, 4*hi4) are zero (not stored)
+    uint32_t lo4, hi4;      // occupied uint4-group range
     bool present;
 };
 
@@ -47,9 +50,9 @@ struct LeafCtx {
     int pass;
     const uint32_t *nko, *kpos;
     const double *ncost, *cost, *prev;
-    const uint32_t* pk;        // bitset pool (leaf base applied)
+    const uint32_t* pk;        // history blocks (leaf base applied)
     const double* pv;          // value pool
-    const uint32_t *hoff[2], *hvoff[2], *hlen[2], *hrng[2];
+    const uint32_t *hoff[2], *hrng[2];
 };
 
 __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
@@ -57,21 +60,23 @@ __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
 }
 
 __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
-    Hist h{nullptr, nullptr, nullptr, 0u, 0u, 0u, false};
+    Hist h{nullptr, 0u, 0u, false};
     if (c.C == 1) return h;                       // no flush ever happens with one class
     int par;
     if (j < c.k) par = c.pass & 1;                // flushed earlier in this pass
     else if (c.pass == 0) return h;               // not flushed yet
     else par = (c.pass - 1) & 1;                  // last pass's flush
     h.bits = c.pk + c.hoff[par][j];
-    h.wmax = reinterpret_cast<const double*>(h.bits + c.NW);
-    h.vals = c.pv + c.hvoff[par][j];
-    h.n = c.hlen[par][j];
     const uint32_t rg = c.hrng[par][j];
     h.lo4 = rg & 0xFFFFu;
     h.hi4 = rg >> 16;
     h.present = true;
     return h;
+}
+
+__device__ __forceinline__ const uint32_t* wptr_of(const LeafCtx& c, const Hist& h) { return h.bits + c.NW; }
+__device__ __forceinline__ const double* wmax_of(const LeafCtx& c, const Hist& h) {
+    return reinterpret_cast<const double*>(h.bits + 2 * c.NW);
 }
 
 __device__ __forceinline__ bool hbit(const Hist& h, uint32_t key) {
@@ -84,23 +89,118 @@ __device__ __forceinline__ uint4 hword4(const Hist& h, uint32_t w4) {
                                                     : make_uint4(0, 0, 0, 0);
 }
 
+__device__ __forceinline__ uint32_t hword(const Hist& h, uint32_t w) {
+    const uint32_t g = w >> 2;
+    return (h.present && g >= h.lo4 && g < h.hi4) ? h.bits[w] : 0u;
+}
+
 __device__ __forceinline__ uint32_t bit_of(uint32_t key, uint32_t w) {
     return (key >> 5) == w ? (1u << (key & 31)) : 0u;
 }
 
-// Read-only OCF walk for arity <= 2 (extraction.py:205-221): node cost and exact history size.
-__device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, double* cc1_out, double* cc2_out,
-                            bool* skip2_out) {
+// Python-max over hB's values at the keys hB shares with (hA + {sA}) (extraction.py:205-221,
+// PAPER.md Alg. 2 case 2). sA may be NONE.
+__device__ double overlap_max(const LeafCtx& c, const Hist& hA, uint32_t sA, const Hist& hB) {
+    double m = 0.0;
+    const uint4* bB = reinterpret_cast<const uint4*>(hB.bits);
+    const uint32_t* pB = wptr_of(c, hB);
+    const double* mB = wmax_of(c, hB);
+    for (uint32_t w4 = hB.lo4; w4 < hB.hi4; w4++) {
+        const uint4 qB = bB[w4];
+        if (!(qB.x | qB.y | qB.z | qB.w)) continue;
+        const uint4 qA = hword4(hA, w4);
+        const uint32_t wB[4] = {qB.x, qB.y, qB.z, qB.w}, wA[4] = {qA.x, qA.y, qA.z, qA.w};
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+            const uint32_t w = 4 * w4 + t;
+            uint32_t o = wB[t] & (wA[t] | bit_of(sA, w));
+            if (!o) continue;
+            if (o == wB[t]) {   // the whole word overlaps: its stored maximum
+                m = pymax(m, mB[w]);
+            } else {
+                const double* vb = c.pv + pB[w];
+                while (o) {
+                    const int bpos = __ffs(o) - 1;
+                    m = pymax(m, vb[__popc(wB[t] & ((1u << bpos) - 1u))]);
+                    o &= o - 1;
+                }
+            }
+        }
+    }
+    return m;
+}
+
+// Merged history hA + {sA: vA} + hB + {sB: vB} with precedence sA, sB, hA, hB (first writer of a
+// key wins; Alg. 2's enode_hist[child] = cc overrides an inherited value). Writes the block at
+// ob and fresh values into the value pool; returns the packed range lo4 | hi4 << 16, or NONE
+// when the value pool is exhausted (*over gets bit 2).
+__device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, double vA, const Hist& hB,
+                                uint32_t sB, double vB, uint32_t* ob, uint32_t* topv, uint64_t capv, double* pv,
+                                uint32_t* over) {
+    const uint32_t NW = c.NW;
+    uint32_t lo = 0xFFFFu, hi = 0;
+    if (sA != NONE) { lo = min(lo, sA >> 7); hi = max(hi, (sA >> 7) + 1); }
+    if (sB != NONE) { lo = min(lo, sB >> 7); hi = max(hi, (sB >> 7) + 1); }
+    if (hA.present && hA.hi4 > hA.lo4) { lo = min(lo, hA.lo4); hi = max(hi, hA.hi4); }
+    if (hB.present && hB.hi4 > hB.lo4) { lo = min(lo, hB.lo4); hi = max(hi, hB.hi4); }
+    if (hi <= lo) return 0u;
+    // pass 1: fresh value count (words that mix sources or hold a new key)
+    uint32_t fresh = 0;
+    for (uint32_t w = 4 * lo; w < 4 * hi; w++) {
+        const uint32_t wA = hword(hA, w), wB = hword(hB, w), sp = bit_of(sA, w) | bit_of(sB, w);
+        const bool share = !sp && (wA ? !(wB & ~wA) : true);
+        if (!share) fresh += __popc(wA | wB | sp);
+    }
+    const uint32_t base = atomicAdd(topv, fresh);
+    if ((uint64_t)base + fresh > capv) { atomicOr(over, 2u); return NONE; }
+    // pass 2: bits, word pointers, word maxima, fresh values
+    const uint32_t *pA = hA.present ? wptr_of(c, hA) : nullptr, *pB = hB.present ? wptr_of(c, hB) : nullptr;
+    const double *mA = hA.present ? wmax_of(c, hA) : nullptr, *mB = hB.present ? wmax_of(c, hB) : nullptr;
+    uint32_t* optr = ob + NW;
+    double* omax = reinterpret_cast<double*>(ob + 2 * NW);
+    uint32_t o = base;
+    for (uint32_t w = 4 * lo; w < 4 * hi; w++) {
+        const uint32_t wA = hword(hA, w), wB = hword(hB, w), sp = bit_of(sA, w) | bit_of(sB, w);
+        uint32_t ow = wA | wB | sp;
+        ob[w] = ow;
+        if (!sp && wA && !(wB & ~wA)) { optr[w] = pA[w]; omax[w] = mA[w]; continue; }   // hA's word
+        if (!sp && !wA) {                                                                // hB's word (or empty)
+            optr[w] = wB ? pB[w] : 0u;
+            omax[w] = wB ? mB[w] : 0.0;
+            continue;
+        }
+        const double* va = wA ? c.pv + pA[w] : nullptr;
+        const double* vb = wB ? c.pv + pB[w] : nullptr;
+        optr[w] = o;
+        double mx = 0.0;
+        while (ow) {
+            const int bpos = __ffs(ow) - 1;
+            const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
+            double val;
+            if (key == sA) val = vA;
+            else if (key == sB) val = vB;
+            else if ((wA >> bpos) & 1u) val = va[__popc(wA & below)];
+            else val = vb[__popc(wB & below)];
+            pv[o++] = val;
+            mx = pymax(mx, val);
+            ow &= ow - 1;
+        }
+        omax[w] = mx;
+    }
+    return lo | (hi << 16);
+}
+
+// OCF cost of an arity <= 2 node (extraction.py:205-221), read-only.
+__device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, double* cc1_out, double* cc2_out, bool* skip2_out) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
     double v = c.ncost[nd];
     *skip2_out = true;
-    if (a == 0) { *size_out = 0; return v; }
+    if (a == 0) return v;
     const uint32_t c1 = c.kpos[q0];
     const Hist h1 = child_hist(c, c1);
     // case 2 with an empty running history (max_cost = 0), or case 3 without a history
     const double cc1 = h1.present ? pymax(child_cost(c, c1) - 0.0, 0.0) : child_cost(c, c1);
     v = v + cc1;
-    uint32_t size = h1.n + (hbit(h1, c1) ? 0u : 1u);
     *cc1_out = cc1;
     if (a == 2) {
         const uint32_t c2 = c.kpos[q0 + 1];
@@ -108,183 +208,44 @@ __device__ double ocf_walk2(const LeafCtx& c, uint32_t nd, uint32_t* size_out, d
         *skip2_out = skip;
         if (!skip) {
             const Hist h2 = child_hist(c, c2);
-            double cc2;
-            if (h2.present) {
-                // case 2: overlap of h2's constituents with the running history H1 = h1 + {c1}
-                double m = 0.0;
-                uint32_t ov = 0, rank2 = 0;
-                const uint4* b2v = reinterpret_cast<const uint4*>(h2.bits);
-                for (uint32_t w4 = h2.lo4; w4 < h2.hi4; w4++) {
-                    const uint4 q2 = b2v[w4];
-                    if (!(q2.x | q2.y | q2.z | q2.w)) continue;
-                    const uint4 q1 = hword4(h1, w4);
-                    const uint32_t w2[4] = {q2.x, q2.y, q2.z, q2.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-                    for (int t = 0; t < 4; t++) {
-                        const uint32_t w = 4 * w4 + t;
-                        uint32_t o = w2[t] & (w1[t] | bit_of(c1, w));
-                        const uint32_t pc = __popc(w2[t]);
-                        if (o == w2[t]) {   // the whole word overlaps: its stored maximum
-                            m = pymax(m, h2.wmax[w]);
-                            ov += pc;
-                        } else {
-                            while (o) {
-                                const int bpos = __ffs(o) - 1;
-                                m = pymax(m, h2.vals[rank2 + __popc(w2[t] & ((1u << bpos) - 1u))]);
-                                ov++;
-                                o &= o - 1;
-                            }
-                        }
-                        rank2 += pc;
-                    }
-                }
-                cc2 = pymax(child_cost(c, c2) - m, 0.0);
-                size += h2.n - ov + (hbit(h2, c2) ? 0u : 1u);
-            } else {
-                cc2 = child_cost(c, c2);   // case 3
-                size += 1;
-            }
+            // case 2: overlap of h2's constituents with the running history h1 + {c1}; case 3
+            const double cc2 = h2.present ? pymax(child_cost(c, c2) - overlap_max(c, h1, c1, h2), 0.0)
+                                          : child_cost(c, c2);
             *cc2_out = cc2;
             v = v + cc2;
         }
     }
-    *size_out = size;
     return v;
 }
 
-// Materialise the history of an arity <= 2 node: bitset at ob (NW words), values at ovals.
-// Only the occupied uint4-group range is written; it is returned packed as lo4 | hi4 << 16.
-__device__ uint32_t ocf_write2(const LeafCtx& c, uint32_t nd, double cc1, double cc2, bool skip2, uint32_t* ob,
-                               double* ovals) {
-    const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0;
-    uint4* obv = reinterpret_cast<uint4*>(ob);
-    double* owm = reinterpret_cast<double*>(ob + c.NW);
-    if (a == 0) return 0u;
-    const uint32_t c1 = c.kpos[q0];
-    const Hist h1 = child_hist(c, c1);
-    Hist h2{nullptr, nullptr, nullptr, 0u, 0u, 0u, false};
-    uint32_t c2 = NONE;
-    if (a == 2 && !skip2) { c2 = c.kpos[q0 + 1]; h2 = child_hist(c, c2); }
-    uint32_t lo = c1 >> 7, hi = (c1 >> 7) + 1;
-    if (c2 != NONE) { lo = min(lo, c2 >> 7); hi = max(hi, (c2 >> 7) + 1); }
-    if (h1.present && h1.hi4 > h1.lo4) { lo = min(lo, h1.lo4); hi = max(hi, h1.hi4); }
-    if (h2.present && h2.hi4 > h2.lo4) { lo = min(lo, h2.lo4); hi = max(hi, h2.hi4); }
-    // keys {h1, c1, h2, c2}; values: c1 -> cc1, c2 -> cc2, h1 wins over h2 (first writer)
-    const double* v1 = h1.vals;
-    const double* v2 = h2.vals;
-    uint32_t o = 0, rank1 = 0, rank2 = 0;
-    for (uint32_t w4 = lo; w4 < hi; w4++) {
-        const uint4 q1 = hword4(h1, w4);
-        const uint4 q2 = hword4(h2, w4);
-        const uint32_t w1[4] = {q1.x, q1.y, q1.z, q1.w}, w2[4] = {q2.x, q2.y, q2.z, q2.w};
-        uint32_t wo[4];
-#pragma unroll
-        for (int t = 0; t < 4; t++) {
-            const uint32_t w = 4 * w4 + t;
-            const uint32_t sp = bit_of(c1, w) | (c2 != NONE ? bit_of(c2, w) : 0u);
-            uint32_t ow = w1[t] | w2[t] | sp;
-            wo[t] = ow;
-            if (!sp && !(w1[t] & w2[t]) && (!w1[t] || !w2[t])) {
-                // word owned by one source and no special key: contiguous value copy
-                const uint32_t n1w = __popc(w1[t]), n2w = __popc(w2[t]);
-                const double* src = n1w ? v1 + rank1 : v2 + rank2;
-                const uint32_t cnt = n1w ? n1w : n2w;
-                for (uint32_t i = 0; i < cnt; i++) ovals[o + i] = src[i];
-                owm[w] = n1w ? h1.wmax[w] : (n2w ? h2.wmax[w] : 0.0);
-                o += cnt;
-                rank1 += n1w;
-                rank2 += n2w;
-                continue;
-            }
-            double wm = 0.0;
-            while (ow) {
-                const int bpos = __ffs(ow) - 1;
-                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
-                double val;
-                if (key == c1) val = cc1;
-                else if (key == c2) val = cc2;
-                else if ((w1[t] >> bpos) & 1u) val = v1[rank1 + __popc(w1[t] & below)];
-                else val = v2[rank2 + __popc(w2[t] & below)];
-                ovals[o++] = val;
-                wm = pymax(wm, val);
-                ow &= ow - 1;
-            }
-            owm[w] = wm;
-            rank1 += __popc(w1[t]);
-            rank2 += __popc(w2[t]);
-        }
-        obv[w4] = make_uint4(wo[0], wo[1], wo[2], wo[3]);
-    }
-    return lo | (hi << 16);
-}
-
-// Generic-arity OCF node (n-ary sink): the running history is rebuilt in the pool child by
-// child, exactly as Alg. 2 mutates enode_hist. Returns the node cost; the final history is at
-// (*boff, *voff, *n_out) (boff == NONE for an empty history).
+// Generic-arity OCF node (n-ary sink): the running history is rebuilt child by child exactly as
+// Alg. 2 mutates enode_hist, each step one merge into a fresh block. Returns the node cost; the
+// final history block offset / range go to *boff / *rng (boff NONE on pool exhaustion).
 __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uint32_t* topv, uint64_t capk,
-                              uint64_t capv, uint32_t* pk, double* pv, uint32_t* boff, uint32_t* voff,
-                              uint32_t* n_out, uint32_t* over) {
+                              uint64_t capv, uint32_t* pk, double* pv, uint32_t* boff, uint32_t* rng,
+                              uint32_t* over) {
     const uint32_t q0 = c.nko[nd], a = c.nko[nd + 1] - q0, NW = c.NW;
     double v = c.ncost[nd];
-    uint32_t hb = NONE, hv = 0, hn = 0;   // running history H (none yet)
+    Hist H{nullptr, 0u, 0u, false};   // running history (none yet)
+    uint32_t hb = 0, hr = 0;
+    const Hist none{nullptr, 0u, 0u, false};
     for (uint32_t t = 0; t < a; t++) {
         const uint32_t ck = c.kpos[q0 + t];
-        if (hb != NONE && ((pk[hb + (ck >> 5)] >> (ck & 31)) & 1u)) continue;   // case 1
+        if (hbit(H, ck)) continue;   // case 1
         const Hist h = child_hist(c, ck);
-        double m = 0.0;
-        uint32_t add = 0;
-        if (h.present) {
-            uint32_t rank = 0;
-            for (uint32_t w = 0; w < NW; w++) {
-                const uint32_t bw = (w >> 2) >= h.lo4 && (w >> 2) < h.hi4 ? h.bits[w] : 0u;
-                const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u;
-                uint32_t o = bw & Hw;
-                while (o) {
-                    const int bpos = __ffs(o) - 1;
-                    m = pymax(m, h.vals[rank + __popc(bw & ((1u << bpos) - 1u))]);
-                    o &= o - 1;
-                }
-                add += __popc(bw & ~Hw);
-                rank += __popc(bw);
-            }
-        }
-        const double cc = h.present ? pymax(child_cost(c, ck) - m, 0.0) : child_cost(c, ck);
-        const bool ck_new = !hbit(h, ck);
-        const uint32_t nn = hn + add + (ck_new ? 1u : 0u);
-        const uint32_t nb = atomicAdd(topk, 3 * NW), nv = atomicAdd(topv, nn);
-        if ((uint64_t)nb + 3 * NW > capk || (uint64_t)nv + nn > capv) {
-            atomicOr(over, ((uint64_t)nb + 3 * NW > capk ? 1u : 0u) | ((uint64_t)nv + nn > capv ? 2u : 0u));
-            *boff = NONE; *voff = 0; *n_out = 0;
-            return v + cc;
-        }
-        uint32_t o = 0, r0 = 0, r1 = 0;
-        for (uint32_t w = 0; w < NW; w++) {
-            const uint32_t Hw = hb != NONE ? pk[hb + w] : 0u;
-            const uint32_t bw = (h.present && (w >> 2) >= h.lo4 && (w >> 2) < h.hi4) ? h.bits[w] : 0u;
-            uint32_t ow = Hw | bw | bit_of(ck, w);
-            pk[nb + w] = ow;
-            double wm = 0.0;
-            while (ow) {
-                const int bpos = __ffs(ow) - 1;
-                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
-                double val;
-                if (key == ck) val = cc;                                                 // enode_hist[child]
-                else if ((Hw >> bpos) & 1u) val = pv[hv + r0 + __popc(Hw & below)];      // H wins (first writer)
-                else val = h.vals[r1 + __popc(bw & below)];
-                pv[nv + o++] = val;
-                wm = pymax(wm, val);
-                ow &= ow - 1;
-            }
-            reinterpret_cast<double*>(pk + nb + NW)[w] = wm;
-            r0 += __popc(Hw);
-            r1 += __popc(bw);
-        }
-        hb = nb; hv = nv; hn = nn;
+        const double cc = h.present ? pymax(child_cost(c, ck) - overlap_max(c, H, NONE, h), 0.0)
+                                    : child_cost(c, ck);
+        const uint32_t nb = atomicAdd(topk, 4 * NW);
+        if ((uint64_t)nb + 4 * NW > capk) { atomicOr(over, 1u); *boff = NONE; *rng = 0; return v + cc; }
+        const uint32_t r = merge_write(c, H, ck, cc, h, NONE, 0.0, pk + nb, topv, capv, pv, over);
+        if (r == NONE) { *boff = NONE; *rng = 0; return v + cc; }
+        hb = nb; hr = r;
+        H.bits = pk + nb; H.lo4 = r & 0xFFFFu; H.hi4 = r >> 16; H.present = true;
         v = v + cc;
     }
+    (void)none;
     *boff = hb;
-    *voff = hv;
-    *n_out = hn;
+    *rng = hr;
     return v;
 }
 
@@ -313,8 +274,6 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     const bool ocf = x.method == 1;
     uint64_t capk = 0, capv = 0;
     uint32_t* hoffw[2] = {nullptr, nullptr};
-    uint32_t* hvoffw[2] = {nullptr, nullptr};
-    uint32_t* hlenw[2] = {nullptr, nullptr};
     uint32_t* hrngw[2] = {nullptr, nullptr};
     uint32_t* pkw = nullptr;
     double* pvw = nullptr;
@@ -328,10 +287,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
         c.pv = pvw;
         for (int p = 0; p < 2; p++) {
             hoffw[p] = x.hoff + p * x.slot_stride + b;
-            hvoffw[p] = x.hvoff + p * x.slot_stride + b;
-            hlenw[p] = x.hlen + p * x.slot_stride + b;
             hrngw[p] = x.hrng + p * x.slot_stride + b;
-            c.hoff[p] = hoffw[p]; c.hvoff[p] = hvoffw[p]; c.hlen[p] = hlenw[p]; c.hrng[p] = hrngw[p];
+            c.hoff[p] = hoffw[p]; c.hrng[p] = hrngw[p];
         }
     }
 
@@ -437,8 +394,6 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                     chg_cur[k] = 0;
                     if (ocf && C > 1) {
                         hoffw[par][k] = hoffw[ppar][k];
-                        hvoffw[par][k] = hvoffw[ppar][k];
-                        hlenw[par][k] = hlenw[ppar][k];
                         hrngw[par][k] = hrngw[ppar][k];
                     }
                     continue;
@@ -455,61 +410,67 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 } else {
                     // first strict-min node by ocf_enode_cost; its history is flushed for class k
                     double hb = __longlong_as_double(0x7ff0000000000000ll);
-                    uint32_t hn = NONE, hsize = 0, gb = NONE, gv = 0;
+                    uint32_t hn = NONE, gb = NONE, grng = 0;
                     double h_cc1 = 0, h_cc2 = 0;
                     bool h_skip2 = true, h_gen = false;
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++) {
                         double v;
                         if (c.nko[nd + 1] - c.nko[nd] <= 2) {
-                            uint32_t size;
                             double cc1 = 0, cc2 = 0;
                             bool skip2;
-                            v = ocf_walk2(c, nd, &size, &cc1, &cc2, &skip2);
-                            if (v < hb) { hb = v; hn = nd; hsize = size; h_cc1 = cc1; h_cc2 = cc2; h_skip2 = skip2; h_gen = false; }
+                            v = ocf_walk2(c, nd, &cc1, &cc2, &skip2);
+                            if (v < hb) { hb = v; hn = nd; h_cc1 = cc1; h_cc2 = cc2; h_skip2 = skip2; h_gen = false; }
                         } else {
-                            uint32_t ob, ovf, on;
-                            v = ocf_generic(c, nd, &sh_topk, &sh_topv, capk, capv, pkw, pvw, &ob, &ovf, &on, &sh_over);
-                            if (v < hb) { hb = v; hn = nd; hsize = on; gb = ob; gv = ovf; h_gen = true; }
+                            uint32_t ob, orng;
+                            v = ocf_generic(c, nd, &sh_topk, &sh_topv, capk, capv, pkw, pvw, &ob, &orng, &sh_over);
+                            if (v < hb) { hb = v; hn = nd; gb = ob; grng = orng; h_gen = true; }
                         }
                         if (bn == NONE || v < bv) { bv = v; bn = nd; }
                     }
                     if (C > 1) {
-                        uint32_t offk = NONE, offv = 0, rng = 0;
-                        if (hn != NONE && h_gen && gb != NONE) {
-                            offk = gb; offv = gv; rng = (NW / 4) << 16;
-                        } else if (!(hn != NONE && h_gen)) {
-                            if (hn == NONE) hsize = 0;
-                            offk = atomicAdd(&sh_topk, 3 * NW);
-                            offv = atomicAdd(&sh_topv, hsize);
-                            if ((uint64_t)offk + 3 * NW > capk || (uint64_t)offv + hsize > capv) {
-                                atomicOr(&sh_over, ((uint64_t)offk + 3 * NW > capk ? 1u : 0u) |
-                                                   ((uint64_t)offv + hsize > capv ? 2u : 0u));
-                                offk = NONE;
-                            } else if (hn != NONE) {
-                                rng = ocf_write2(c, hn, h_cc1, h_cc2, h_skip2, pkw + offk, pvw + offv);
+                        uint32_t offk = 0, rng = 0;
+                        bool ok = true;
+                        if (hn != NONE && h_gen) {
+                            ok = gb != NONE;
+                            offk = gb; rng = grng;
+                        } else if (hn != NONE && c.nko[hn + 1] > c.nko[hn]) {
+                            const uint32_t q0 = c.nko[hn], c1 = c.kpos[q0];
+                            const bool two = c.nko[hn + 1] - q0 == 2 && !h_skip2;
+                            const uint32_t c2 = two ? c.kpos[q0 + 1] : NONE;
+                            const Hist h1 = child_hist(c, c1);
+                            const Hist h2 = two ? child_hist(c, c2) : Hist{nullptr, 0u, 0u, false};
+                            offk = atomicAdd(&sh_topk, 4 * NW);
+                            if ((uint64_t)offk + 4 * NW > capk) {
+                                atomicOr(&sh_over, 1u);
+                                ok = false;
+                            } else {
+                                rng = merge_write(c, h1, c1, h_cc1, h2, c2, h_cc2, pkw + offk, &sh_topv, capv, pvw,
+                                                  &sh_over);
+                                ok = rng != NONE;
                             }
-                        }
-                        if (offk == NONE) { offk = 0; offv = 0; hsize = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
+                        }   // else: empty history (no node, or a leaf node): the empty range, no block
+                        if (!ok) { offk = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
                         hoffw[par][k] = offk;
-                        hvoffw[par][k] = offv;
-                        hlenw[par][k] = hsize;
                         hrngw[par][k] = rng;
                         if (!changed) {  // did the flushed history change w.r.t. last pass?
-                            const uint32_t ok2 = hoffw[ppar][k], ov2 = hvoffw[ppar][k], n2 = hlenw[ppar][k];
-                            const uint32_t r2 = hrngw[ppar][k];
-                            if (n2 != hsize) changed = true;
-                            // same value count; compare the occupied words of both ranges
+                            const uint32_t ok2 = hoffw[ppar][k], r2 = hrngw[ppar][k];
                             const uint32_t la = rng & 0xFFFFu, ha = rng >> 16, lb = r2 & 0xFFFFu, hb2 = r2 >> 16;
                             const uint32_t lo = min(la, lb), hi = max(ha, hb2);
-                            const uint4* a4 = reinterpret_cast<const uint4*>(pkw + offk);
-                            const uint4* b4 = reinterpret_cast<const uint4*>(pkw + ok2);
-                            for (uint32_t w4 = lo; w4 < hi && !changed; w4++) {
-                                const uint4 p = (w4 >= la && w4 < ha) ? a4[w4] : make_uint4(0, 0, 0, 0);
-                                const uint4 q = (w4 >= lb && w4 < hb2) ? b4[w4] : make_uint4(0, 0, 0, 0);
-                                changed = p.x != q.x || p.y != q.y || p.z != q.z || p.w != q.w;
+                            const uint32_t* a1 = pkw + offk;
+                            const uint32_t* b1 = pkw + ok2;
+                            for (uint32_t w = 4 * lo; w < 4 * hi && !changed; w++) {
+                                const uint32_t p = (w >= 4 * la && w < 4 * ha) ? a1[w] : 0u;
+                                const uint32_t q = (w >= 4 * lb && w < 4 * hb2) ? b1[w] : 0u;
+                                if (p != q) { changed = true; break; }
+                                if (!p) continue;
+                                const uint32_t pa = a1[NW + w], pb = b1[NW + w];
+                                if (pa == pb) continue;   // shared storage
+                                for (uint32_t i = 0; i < (uint32_t)__popc(p); i++)
+                                    if (__double_as_longlong(pvw[pa + i]) != __double_as_longlong(pvw[pb + i])) {
+                                        changed = true;
+                                        break;
+                                    }
                             }
-                            for (uint32_t i = 0; i < hsize && !changed; i++)
-                                changed = __double_as_longlong(pvw[offv + i]) != __double_as_longlong(pvw[ov2 + i]);
                         }
                     }
                 }
