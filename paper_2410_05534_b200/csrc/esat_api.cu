@@ -738,13 +738,16 @@ static int join_launch(esat_batch* b) {
     const uint32_t run_cap = (uint32_t)(umax < 16384 ? umax : 16384);
     a.id_base = b->d.ub;
     a.run_cap = run_cap;
+    a.s1_cap = JOIN_SMEM_S1;
     static bool join_attr = false;
     if (!join_attr) {
-        CK(c, cudaFuncSetAttribute(k_join<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384 * 4));
+        CK(c, cudaFuncSetAttribute(k_join<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   4 * (16384 + JOIN_SMEM_S1)));
         join_attr = true;
     }
     tic(c);
-    if (L && R) k_join<128><<<dim3((unsigned)L, R), 128, 4 * run_cap, c->stream>>>((uint32_t)L, a);
+    if (L && R)
+        k_join<128><<<dim3((unsigned)L, R), 128, 4 * (run_cap + JOIN_SMEM_S1), c->stream>>>((uint32_t)L, a);
     toc(c);
     b->j_relaunch_needed = true;
     return launch_check(c, "k_join");

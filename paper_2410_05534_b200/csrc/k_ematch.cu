@@ -567,6 +567,17 @@ __device__ __forceinline__ uint32_t group_end(const Src& s, uint32_t i) {
     return j;
 }
 
+// group_end for a converged warp: 32 records tested per step
+__device__ __forceinline__ uint32_t group_end_warp(const Src& s, uint32_t i, uint32_t lane) {
+    const uint32_t root = s.w[(uint64_t)i * s.W];
+    for (uint32_t j = i + 1;; j += 32) {
+        const uint32_t q = j + lane;
+        const bool stop = q >= s.n || s.w[(uint64_t)q * s.W] != root;
+        const uint32_t m = __ballot_sync(0xffffffffu, stop);
+        if (m) return j + __ffs(m) - 1;
+    }
+}
+
 __device__ __forceinline__ uint32_t group_start_at_or_after(const Src& s, uint32_t p) {
     if (p == 0 || p >= s.n) return p >= s.n ? s.n : 0;
     while (p < s.n && s.w[(uint64_t)p * s.W] == s.w[(uint64_t)(p - 1) * s.W]) p++;
@@ -645,7 +656,18 @@ struct JoinPlan {
     uint8_t src[MAX_W], idx[MAX_W];
     uint8_t c0[2 * MAX_V], c1[2 * MAX_V];
     uint32_t nchk, W;
+    // source-1 fields the join reads (output words from source 1, consistency checks), staged in
+    // SMEM in sorted-index order: record p's field f at s1[p * F + f]
+    uint8_t f1[MAX_W + 2 * MAX_V], s1idx[MAX_W], s1chk[2 * MAX_V];
+    uint32_t F;
 };
+
+__device__ uint8_t plan_slot(JoinPlan& p, uint8_t field) {
+    for (uint32_t f = 0; f < p.F; f++)
+        if (p.f1[f] == field) return (uint8_t)f;
+    p.f1[p.F] = field;
+    return (uint8_t)p.F++;
+}
 
 __device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ) {
     p.W = 2 + NV + NQ;
@@ -667,6 +689,9 @@ __device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ) {
         if (p.src[o] == 0) { p.c0[p.nchk] = p.idx[o]; p.c1[p.nchk] = 1 + s[1].V + q; p.nchk++; }
         else { p.src[o] = 1; p.idx[o] = 1 + s[1].V + q; }
     }
+    p.F = 0;
+    for (uint32_t c = 0; c < p.nchk; c++) p.s1chk[c] = plan_slot(p, p.c1[c]);
+    for (uint32_t w = 0; w < p.W; w++) p.s1idx[w] = p.src[w] == 1 ? plan_slot(p, p.idx[w]) : 0;
 }
 
 // Products of the source-0 records [g, ge) (one root group) with the source-1 records sharing the
@@ -750,6 +775,17 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     __shared__ JoinPlan sh_plan;
     if (indexed && tid == 0) make_plan(sh_plan, src, NV, NQ);
     __syncthreads();
+    extern __shared__ uint32_t jrun[];
+    uint32_t* s1 = jrun + a.run_cap;
+    const bool staged = indexed && src[1].n * sh_plan.F <= a.s1_cap;
+    if (staged) {   // source-1 fields in sorted-index order: the walk reads SMEM, not scattered global words
+        const uint32_t F = sh_plan.F, W1s = src[1].W;
+        for (uint32_t e = tid; e < src[1].n * F; e += T) {
+            const uint32_t p = e / F, f = e - p * F;
+            s1[e] = src[1].w[(uint64_t)(uint32_t)sh_keys[p] * W1s + sh_plan.f1[f]];
+        }
+        __syncthreads();
+    }
     if (indexed) {
         // ---- warp-cooperative sort-join: a warp owns whole root groups of source 0; the lanes
         // walk the index run of each source-0 record 32 products at a time, compact consistent
@@ -763,7 +799,6 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         const JoinPlan& jp = sh_plan;
         // run table: for join value x, its run of source-1 records in the sorted index is
         // [run[x] & 0xFFFF, +run[x] >> 16) -- an O(1) lookup instead of two binary searches
-        extern __shared__ uint32_t jrun[];
         const uint32_t U = a.id_base ? (uint32_t)(a.id_base[l + 1] - a.id_base[l]) : 0u;
         const bool use_run = U > 0 && U <= a.run_cap && n1 <= 0xFFFF;
         if (use_run) {
@@ -784,7 +819,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             uint32_t n = 0;
             uint32_t* m1s = sh_m1[warp];
             for (uint32_t g = wlo; g < whi;) {
-                const uint32_t ge = group_end(src[0], g);
+                const uint32_t ge = group_end_warp(src[0], g, lane);
                 const uint32_t gstart = n;
                 for (uint32_t i = g; i < ge; i++) {
                     const uint32_t* m1 = w0 + (uint64_t)i * W0;
@@ -801,9 +836,21 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                         p0 = lower_bound_key(sh_keys, n1, (unsigned long long)x << 32);
                         p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
                     }
+                    if (!out && jp.nchk == 0) { n += p1 - p0; continue; }   // every product is consistent
                     for (uint32_t base = p0; base < p1; base += 32) {
                         const uint32_t p = base + lane;
                         bool ok = p < p1;
+                        if (staged) {
+                            const uint32_t* m2 = s1 + (ok ? p : 0u) * jp.F;
+                            for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.s1chk[c]];
+                            const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+                            if (out && ok) {
+                                uint32_t* o = out + (uint64_t)(n + __popc(mask & ((1u << lane) - 1u))) * W;
+                                for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.s1idx[w]] : m1s[jp.idx[w]];
+                            }
+                            n += __popc(mask);
+                            continue;
+                        }
                         const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)sh_keys[p] * W1 : w1;
                         for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.c1[c]];
                         const uint32_t mask = __ballot_sync(0xffffffffu, ok);

@@ -46,7 +46,10 @@ struct JArgs {
     uint32_t* overflow;
     const uint64_t* id_base;    // per-leaf id bases (run-table size)
     uint32_t run_cap;           // dynamic SMEM run-table entries
+    uint32_t s1_cap;            // dynamic SMEM words for the staged source-1 fields (after the run table)
 };
+
+constexpr uint32_t JOIN_SMEM_S1 = 4096;   // SMEM words for staged source-1 join fields
 
 template <int T> __global__ void k_ematch(Dev, MArgs);
 template <int T> __global__ void k_join(uint32_t, JArgs);
