@@ -723,6 +723,47 @@ __device__ uint32_t indexed_products(const uint32_t* w0, uint32_t W0, const uint
 
 }  // namespace
 
+// Products of one source-0 record (fields in m1s) with its staged source-1 run [p0, p1): 32 per
+// step, consistent ones compacted by ballot and written as consecutive records from row n.
+// WC > 0 fixes the record width at compile time (plan columns and the source-0 values live in
+// registers); WC == 0 is the runtime-width path.
+template <int WC>
+__device__ __forceinline__ uint32_t staged_products(const JoinPlan& jp, const uint32_t* s1, const uint32_t* m1s,
+                                                    uint32_t p0, uint32_t p1, uint32_t lane, uint32_t* out,
+                                                    uint32_t n) {
+    const uint32_t F = jp.F, nchk = jp.nchk, W = WC ? (uint32_t)WC : jp.W;
+    constexpr int R = WC ? WC : 1;
+    uint32_t v0[R], sl[R];
+    bool from1[R];
+    if (WC) {
+#pragma unroll
+        for (int w = 0; w < R; w++) {
+            from1[w] = jp.src[w] != 0;
+            sl[w] = jp.s1idx[w];
+            v0[w] = m1s[jp.idx[w]];
+        }
+    }
+    for (uint32_t base = p0; base < p1; base += 32) {
+        const uint32_t p = base + lane;
+        bool ok = p < p1;
+        const uint32_t* m2 = s1 + (ok ? p : 0u) * F;
+        if (nchk)
+            for (uint32_t c = 0; c < nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.s1chk[c]];
+        const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+        if (out && ok) {
+            uint32_t* o = out + (uint64_t)(n + __popc(mask & ((1u << lane) - 1u))) * W;
+            if (WC) {
+#pragma unroll
+                for (int w = 0; w < R; w++) o[w] = from1[w] ? m2[sl[w]] : v0[w];
+            } else {
+                for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.s1idx[w]] : m1s[jp.idx[w]];
+            }
+        }
+        n += __popc(mask);
+    }
+    return n;
+}
+
 template <int T>
 __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     const uint32_t l = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
@@ -815,11 +856,34 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             __syncthreads();
         }
         __shared__ uint32_t sh_m1[NW][MAX_W];
+        // source-0 root-group starts as a bitmask (bit i: record i starts a group), built once
+        constexpr uint32_t GB_WORDS = 1024;
+        __shared__ uint32_t sh_gbits[GB_WORDS];
+        const bool gtab = n0 <= 32 * GB_WORDS;
+        if (gtab) {
+            for (uint32_t i0 = warp * 32; i0 < n0; i0 += T) {
+                const uint32_t i = i0 + lane;
+                const bool st = i < n0 && (i == 0 || w0[(uint64_t)i * W0] != w0[(uint64_t)(i - 1) * W0]);
+                const uint32_t m = __ballot_sync(0xffffffffu, st);
+                if (lane == 0) sh_gbits[i0 >> 5] = m;
+            }
+            __syncthreads();
+        }
+        auto gend = [&](uint32_t g) -> uint32_t {
+            if (!gtab) return group_end_warp(src[0], g, lane);
+            uint32_t j = g + 1;
+            while (j < n0) {
+                const uint32_t bits = sh_gbits[j >> 5] & (0xFFFFFFFFu << (j & 31));
+                if (bits) return min(n0, (j & ~31u) + __ffs(bits) - 1);
+                j = (j & ~31u) + 32;
+            }
+            return n0;
+        };
         auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
             uint32_t n = 0;
             uint32_t* m1s = sh_m1[warp];
             for (uint32_t g = wlo; g < whi;) {
-                const uint32_t ge = group_end_warp(src[0], g, lane);
+                const uint32_t ge = gend(g);
                 const uint32_t gstart = n;
                 for (uint32_t i = g; i < ge; i++) {
                     const uint32_t* m1 = w0 + (uint64_t)i * W0;
@@ -837,20 +901,17 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                         p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
                     }
                     if (!out && jp.nchk == 0) { n += p1 - p0; continue; }   // every product is consistent
+                    if (staged) {
+                        switch (W) {
+                            case 5: n = staged_products<5>(jp, s1, m1s, p0, p1, lane, out, n); break;
+                            case 8: n = staged_products<8>(jp, s1, m1s, p0, p1, lane, out, n); break;
+                            default: n = staged_products<0>(jp, s1, m1s, p0, p1, lane, out, n); break;
+                        }
+                        continue;
+                    }
                     for (uint32_t base = p0; base < p1; base += 32) {
                         const uint32_t p = base + lane;
                         bool ok = p < p1;
-                        if (staged) {
-                            const uint32_t* m2 = s1 + (ok ? p : 0u) * jp.F;
-                            for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.s1chk[c]];
-                            const uint32_t mask = __ballot_sync(0xffffffffu, ok);
-                            if (out && ok) {
-                                uint32_t* o = out + (uint64_t)(n + __popc(mask & ((1u << lane) - 1u))) * W;
-                                for (uint32_t w = 0; w < W; w++) o[w] = jp.src[w] ? m2[jp.s1idx[w]] : m1s[jp.idx[w]];
-                            }
-                            n += __popc(mask);
-                            continue;
-                        }
                         const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)sh_keys[p] * W1 : w1;
                         for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.c1[c]];
                         const uint32_t mask = __ballot_sync(0xffffffffu, ok);
