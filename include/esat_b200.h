@@ -155,6 +155,36 @@ int esat_result_device_ptrs(esat_batch* b, void** root_cost, void** status);
 /* timing of the last compute call on the context stream, in milliseconds (CUDA events) */
 float esat_last_kernel_ms(const esat_ctx* ctx);
 
+/* ---- apply loop: apply_rule on every leaf of a rebuilt batch ----------------
+ * Replaces rewrite.py:526-570 (apply_rule: _target_refs 460-489, would_create_cycle 492-505,
+ * _instance_shape 508-514, _instantiate 517-523, EGraph.add/union egraph.py:175-201) and the
+ * language hooks make_symbol (rewrite.py:296-298, tensor_ir.py:253-265) / infer_shape
+ * (tensor_ir.py:64-126). Status per leaf: */
+#define ESAT_A_OK 0
+#define ESAT_A_NODE_LIMIT 1     /* StructuralError: node limit not above the node count (rewrite.py:532-537) */
+#define ESAT_A_NEED_SYMBOL 2    /* a new operator symbol must be interned on the host, then retry */
+#define ESAT_A_CAPACITY 3       /* the leaf's arena headroom is exhausted: re-pack with more, retry */
+#define ESAT_A_PROGRAM 4        /* target program beyond device limits */
+
+/* symbol identities (paper_2410_05534_b200/apply.py): per-symbol shape (ndim 255 = none, dims
+ * [n][4]), open-addressing key table (power-of-2 size), attribute integer values by code, the
+ * language (0 term, 1 tensor), cost model (0 term, 1 unit, 2 analytic x coeff) and the rule
+ * target programs (offsets [n_rules+1] into words) */
+int esat_apply_setup(esat_ctx* ctx, int lang, int cost_mode, double coeff, uint32_t n_syms, const uint8_t* sym_ndim,
+                     const uint32_t* sym_dims, uint32_t table_size, const uint32_t* sym_table, uint32_t n_values,
+                     const int32_t* val_int, uint32_t n_rules, const uint32_t* rule_off, const int32_t* words);
+/* live entry / id counts of an arena uploaded with headroom (spans larger than the leaves) */
+int esat_batch_set_counts(esat_batch* b, const uint32_t* n_cnt, const uint32_t* u_cnt);
+/* apply rule leaf_rule[l] (0xFFFFFFFF: none) to every leaf, using the match lists of the last
+ * esat_ematch / esat_join calls; the leaf's dirty state replaces the batch input (next: esat_rebuild) */
+int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit);
+/* status[L], report[L][4] = {matches_found, changed, cycles_filtered, shape_filtered}
+ * (ApplyReport, rewrite.py:440-448), missing[L][16] = descriptor of a symbol to intern */
+int esat_download_apply(esat_batch* b, uint32_t* status, uint32_t* report, uint32_t* missing);
+/* the batch input (dirty) arena with live counts: hashcons + union-find, spans as created */
+int esat_download_state(esat_batch* b, uint32_t* n_cnt, uint32_t* u_cnt, uint32_t* sym, uint32_t* koff,
+                        uint32_t* kids, uint32_t* cid, double* cost, uint32_t* parent, uint8_t* rank);
+
 #ifdef __cplusplus
 }
 #endif

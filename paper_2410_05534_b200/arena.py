@@ -165,3 +165,48 @@ class Batch:
             "uf_rank": cat("uf_rank", np.uint8),
             "root": np.array([lf.root for lf in self.leaves], np.uint32),
         }
+
+    def pack_with_headroom(self, nodes: int, kids: int | None = None, ids: int | None = None) -> dict:
+        """Pack with spare capacity per leaf for the device apply loop (esat_apply): leaf l's
+        spans are n+nodes entries, K+kids child slots, U+ids union-find ids. Unused slots are
+        zero; the live sizes travel as ``n_cnt`` / ``u_cnt`` (esat_batch_set_counts)."""
+        kids = 2 * nodes if kids is None else kids
+        ids = nodes if ids is None else ids
+        L = len(self.leaves)
+        nb = np.zeros(L + 1, np.uint64)
+        kb = np.zeros(L + 1, np.uint64)
+        ub = np.zeros(L + 1, np.uint64)
+        for i, lf in enumerate(self.leaves):
+            nb[i + 1] = nb[i] + lf.n + nodes
+            kb[i + 1] = kb[i] + lf.n_kids + kids
+            ub[i + 1] = ub[i] + lf.n_ids + ids
+        N, K, U = int(nb[-1]), int(kb[-1]), int(ub[-1])
+        out = {"n_leaves": L, "node_base": nb, "kid_base": kb, "id_base": ub,
+               "hc_sym": np.zeros(N, np.uint32), "hc_koff": np.zeros(N + L, np.uint32),
+               "hc_kids": np.zeros(K, np.uint32), "hc_cid": np.zeros(N, np.uint32),
+               "hc_cost": np.zeros(N, np.float64), "uf_parent": np.zeros(U, np.uint32),
+               "uf_rank": np.zeros(U, np.uint8), "root": np.array([lf.root for lf in self.leaves], np.uint32),
+               "n_cnt": np.array([lf.n for lf in self.leaves], np.uint32),
+               "u_cnt": np.array([lf.n_ids for lf in self.leaves], np.uint32)}
+        for i, lf in enumerate(self.leaves):
+            n0, k0, u0 = int(nb[i]), int(kb[i]), int(ub[i])
+            out["hc_sym"][n0:n0 + lf.n] = lf.hc_sym
+            out["hc_koff"][n0 + i:n0 + i + lf.n + 1] = lf.hc_koff
+            out["hc_kids"][k0:k0 + lf.n_kids] = lf.hc_kids
+            out["hc_cid"][n0:n0 + lf.n] = lf.hc_cid
+            out["hc_cost"][n0:n0 + lf.n] = lf.hc_cost
+            out["uf_parent"][u0:u0 + lf.n_ids] = lf.uf_parent
+            out["uf_rank"][u0:u0 + lf.n_ids] = lf.uf_rank
+        return out
+
+
+def unpack_state(packed: dict, state: dict, l: int) -> LeafState:
+    """Leaf l of a downloaded device arena with live counts (DeviceBatch.download_state)."""
+    n0, k0, u0 = (int(packed[k][l]) for k in ("node_base", "kid_base", "id_base"))
+    n, U = int(state["n"][l]), int(state["U"][l])
+    koff = state["hc_koff"][n0 + l:n0 + l + n + 1].copy()
+    K = int(koff[-1])
+    return LeafState(state["hc_sym"][n0:n0 + n].copy(), koff, state["hc_kids"][k0:k0 + K].copy(),
+                     state["hc_cid"][n0:n0 + n].copy(), state["hc_cost"][n0:n0 + n].copy(),
+                     state["uf_parent"][u0:u0 + U].copy(), state["uf_rank"][u0:u0 + U].copy(),
+                     int(packed["root"][l]))

@@ -13,6 +13,7 @@ template <int T> __global__ void k_rebuild(Dev);
 template <int T> __global__ void k_extract(Dev, XArgs);
 }  // namespace esat
 #include "k_ematch_args.cuh"
+#include "k_apply_args.cuh"
 
 using namespace esat;
 
@@ -38,6 +39,15 @@ struct esat_ctx {
     int32_t* d_pat = nullptr;
     uint32_t* d_pat_off = nullptr;
     uint32_t pat_gen = 0, sym_gen = 0;
+    // apply loop setup (esat_apply_setup)
+    bool apply_ready = false;
+    int lang = 0, cost_mode = 0;
+    double coeff = 0.0;
+    uint32_t a_nsyms = 0, a_tmask = 0, a_nvalues = 0, a_nrules = 0;
+    uint8_t* a_ndim = nullptr;
+    uint32_t *a_dims = nullptr, *a_table = nullptr, *a_rule_off = nullptr;
+    int32_t *a_vint = nullptr, *a_prog = nullptr;
+    std::vector<int32_t> a_head;   // per rule: from_join, list index, W
 };
 
 namespace {
@@ -102,6 +112,11 @@ struct esat_batch {
     bool m_verified = false, m_pending = false, j_verified = false, j_pending = false;
     bool j_relaunch_needed = false, m_sig_matches_join = false, m_sized = false, j_sized = false;
     std::vector<uint32_t> m_sig, j_sig;
+    // apply loop: live counts (valid once set by esat_batch_set_counts or an apply) + scratch
+    bool counts = false;
+    uint32_t *d_ncnt = nullptr, *d_ucnt = nullptr;
+    uint32_t *a_rule = nullptr, *a_status = nullptr, *a_report = nullptr, *a_missing = nullptr;
+    uint32_t *a_shead = nullptr, *a_stail = nullptr, *a_snext = nullptr, *a_sseen = nullptr, *a_sstack = nullptr;
 };
 
 namespace {
@@ -314,6 +329,9 @@ int esat_batch_upload(esat_batch* b, const uint32_t* sym, const uint32_t* koff, 
     b->uploaded = true;
     b->rebuilt = false;
     b->upload_gen++;
+    b->counts = false;   // a plain upload fills every arena span (esat_batch_set_counts for headroom)
+    b->d.n_cnt = nullptr;
+    b->d.u_cnt = nullptr;
     return ESAT_OK;
 }
 
@@ -857,6 +875,172 @@ int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t
             CK(c, cudaMemcpyAsync(words + word_off[l], src + off[l], 4ull * counts[l] * W, cudaMemcpyDeviceToHost,
                                   c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
+    return ESAT_OK;
+}
+
+
+// ---- apply loop (K11) ----------------------------------------------------------
+
+int esat_apply_setup(esat_ctx* c, int lang, int cost_mode, double coeff, uint32_t n_syms, const uint8_t* sym_ndim,
+                     const uint32_t* sym_dims, uint32_t table_size, const uint32_t* sym_table, uint32_t n_values,
+                     const int32_t* val_int, uint32_t n_rules, const uint32_t* rule_off, const int32_t* words) {
+    if (!c || !sym_ndim || !sym_dims || !sym_table || !rule_off || (n_rules && !words)) return ESAT_E_ARG;
+    if (table_size == 0 || (table_size & (table_size - 1))) return fail(c, ESAT_E_ARG, "table size must be a power of 2");
+    if (n_syms != c->n_syms) return fail(c, ESAT_E_STATE, "apply symbols (%u) != uploaded symbol table (%u)", n_syms, c->n_syms);
+    cudaSetDevice(c->device);
+    int r;
+    if ((r = dalloc(c, &c->a_ndim, n_syms))) return r;
+    if ((r = dalloc(c, &c->a_dims, 4ull * n_syms))) return r;
+    if ((r = dalloc(c, &c->a_table, table_size))) return r;
+    if ((r = dalloc(c, &c->a_vint, n_values ? n_values : 1))) return r;
+    if ((r = dalloc(c, &c->a_rule_off, n_rules + 1))) return r;
+    const uint32_t nw = rule_off[n_rules];
+    if ((r = dalloc(c, &c->a_prog, nw ? nw : 1))) return r;
+    CK(c, cudaMemcpy(c->a_ndim, sym_ndim, n_syms, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->a_dims, sym_dims, 16ull * n_syms, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->a_table, sym_table, 4ull * table_size, cudaMemcpyHostToDevice));
+    if (n_values) CK(c, cudaMemcpy(c->a_vint, val_int, 4ull * n_values, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->a_rule_off, rule_off, 4ull * (n_rules + 1), cudaMemcpyHostToDevice));
+    if (nw) CK(c, cudaMemcpy(c->a_prog, words, 4ull * nw, cudaMemcpyHostToDevice));
+    c->a_head.assign(3ull * n_rules, 0);
+    for (uint32_t i = 0; i < n_rules; i++)
+        for (int k = 0; k < 3; k++) c->a_head[3 * i + k] = words[rule_off[i] + k];
+    c->lang = lang; c->cost_mode = cost_mode; c->coeff = coeff;
+    c->a_nsyms = n_syms; c->a_tmask = table_size - 1; c->a_nvalues = n_values; c->a_nrules = n_rules;
+    c->apply_ready = true;
+    return ESAT_OK;
+}
+
+static int ensure_apply_buffers(esat_batch* b) {
+    if (b->d_ncnt) return ESAT_OK;
+    const uint64_t N = b->N, K = b->K, U = b->U, L = b->L;
+    OWN(b->d_ncnt, L); OWN(b->d_ucnt, L);
+    OWN(b->a_rule, L); OWN(b->a_status, L); OWN(b->a_report, 4 * L); OWN(b->a_missing, 16 * L);
+    OWN(b->a_shead, U); OWN(b->a_stail, U); OWN(b->a_sseen, U); OWN(b->a_snext, N); OWN(b->a_sstack, N + K);
+    return ESAT_OK;
+}
+
+int esat_batch_set_counts(esat_batch* b, const uint32_t* n_cnt, const uint32_t* u_cnt) {
+    if (!b || !n_cnt || !u_cnt) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    cudaSetDevice(c->device);
+    int r;
+    if ((r = ensure_apply_buffers(b))) return r;
+    for (uint32_t l = 0; l < b->L; l++)
+        if (n_cnt[l] > b->nb[l + 1] - b->nb[l] || u_cnt[l] > b->ub[l + 1] - b->ub[l])
+            return fail(c, ESAT_E_ARG, "leaf %u: counts exceed the arena capacity", l);
+    CK(c, cudaMemcpyAsync(b->d_ncnt, n_cnt, 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(b->d_ucnt, u_cnt, 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    b->counts = true;
+    b->d.n_cnt = b->d_ncnt;
+    b->d.u_cnt = b->d_ucnt;
+    b->rebuilt = false;
+    return ESAT_OK;
+}
+
+int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
+    if (!b || !leaf_rule) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!c->apply_ready) return fail(c, ESAT_E_STATE, "esat_apply_setup not called");
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "apply requires a rebuilt e-graph");
+    cudaSetDevice(c->device);
+    int r;
+    if ((r = ensure_apply_buffers(b))) return r;
+    if ((r = verify_matches(b))) return r;
+    for (uint32_t l = 0; l < b->L; l++) {
+        const uint32_t ru = leaf_rule[l];
+        if (ru == 0xFFFFFFFFu) continue;
+        if (ru >= c->a_nrules) return fail(c, ESAT_E_ARG, "leaf %u: rule %u out of range", l, ru);
+        const int32_t fj = c->a_head[3 * ru], li = c->a_head[3 * ru + 1], W = c->a_head[3 * ru + 2];
+        const uint32_t nl = fj ? b->j_R : b->m_P;
+        if ((uint32_t)li >= nl) return fail(c, ESAT_E_STATE, "rule %u: match list %d not computed", ru, li);
+        if ((uint32_t)W != (fj ? b->j_W[li] : b->m_W[li]))
+            return fail(c, ESAT_E_STATE, "rule %u: record width %d differs from the match list's", ru, W);
+    }
+    CK(c, cudaMemcpyAsync(b->a_rule, leaf_rule, 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
+    if (!b->counts) {   // first apply on a plain upload: counts are the arena spans
+        std::vector<uint32_t> nc(b->L), uc(b->L);
+        for (uint32_t l = 0; l < b->L; l++) {
+            nc[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]);
+            uc[l] = (uint32_t)(b->ub[l + 1] - b->ub[l]);
+        }
+        CK(c, cudaMemcpyAsync(b->d_ncnt, nc.data(), 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaMemcpyAsync(b->d_ucnt, uc.data(), 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
+    Dev d = b->d;
+    d.n_cnt = b->d_ncnt;
+    d.u_cnt = b->d_ucnt;
+    d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
+    d.sym_par = c->sym_par; d.n_syms = c->n_syms;
+    AArgs a{};
+    a.prog = c->a_prog; a.rule_off = c->a_rule_off; a.leaf_rule = b->a_rule;
+    a.sym_ndim = c->a_ndim; a.sym_dims = c->a_dims; a.sym_table = c->a_table; a.sym_tmask = c->a_tmask;
+    a.val_int = c->a_vint; a.n_values = c->a_nvalues;
+    a.lang = c->lang; a.cost_mode = c->cost_mode; a.coeff = c->coeff; a.node_limit = node_limit;
+    a.m_words = b->m_out; a.m_off = b->d_m_off; a.m_count = b->d_m_count;
+    a.j_words = b->j_out; a.j_off = b->d_j_off; a.j_count = b->d_j_count;
+    a.w_sym = const_cast<uint32_t*>(b->d.hc_sym); a.w_koff = const_cast<uint32_t*>(b->d.hc_koff);
+    a.w_kids = const_cast<uint32_t*>(b->d.hc_kids); a.w_cid = const_cast<uint32_t*>(b->d.hc_cid);
+    a.w_cost = const_cast<double*>(b->d.hc_cost);
+    a.w_parent = const_cast<uint32_t*>(b->d.uf_parent_in); a.w_rank = const_cast<uint8_t*>(b->d.uf_rank_in);
+    a.status = b->a_status; a.report = b->a_report; a.missing = b->a_missing;
+    a.s_head = b->a_shead; a.s_tail = b->a_stail; a.s_next = b->a_snext; a.s_seen = b->a_sseen;
+    a.s_stack = b->a_sstack;
+    tic(c);
+    if (b->L) k_apply<<<(b->L + 127) / 128, 128, 0, c->stream>>>(d, a);
+    toc(c);
+    if ((r = launch_check(c, "k_apply"))) return r;
+    b->counts = true;
+    b->d.n_cnt = b->d_ncnt;
+    b->d.u_cnt = b->d_ucnt;
+    b->rebuilt = false;
+    b->upload_gen++;
+    return ESAT_OK;
+}
+
+int esat_download_apply(esat_batch* b, uint32_t* status, uint32_t* report, uint32_t* missing) {
+    if (!b) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->a_status) return fail(c, ESAT_E_STATE, "no apply results");
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t L = b->L;
+    if (status) CK(c, cudaMemcpyAsync(status, b->a_status, 4 * L, cudaMemcpyDeviceToHost, s));
+    if (report) CK(c, cudaMemcpyAsync(report, b->a_report, 16 * L, cudaMemcpyDeviceToHost, s));
+    if (missing) CK(c, cudaMemcpyAsync(missing, b->a_missing, 64 * L, cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
+    return ESAT_OK;
+}
+
+int esat_download_state(esat_batch* b, uint32_t* n_cnt, uint32_t* u_cnt, uint32_t* sym, uint32_t* koff,
+                        uint32_t* kids, uint32_t* cid, double* cost, uint32_t* parent, uint8_t* rank) {
+    if (!b) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t N = b->N, K = b->K, U = b->U, L = b->L;
+    if (n_cnt || u_cnt) {
+        std::vector<uint32_t> nc(L), uc(L);
+        if (b->counts) {
+            CK(c, cudaMemcpyAsync(nc.data(), b->d_ncnt, 4 * L, cudaMemcpyDeviceToHost, s));
+            CK(c, cudaMemcpyAsync(uc.data(), b->d_ucnt, 4 * L, cudaMemcpyDeviceToHost, s));
+            CK(c, cudaStreamSynchronize(s));
+        } else {
+            for (uint64_t l = 0; l < L; l++) { nc[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]); uc[l] = (uint32_t)(b->ub[l + 1] - b->ub[l]); }
+        }
+        if (n_cnt) memcpy(n_cnt, nc.data(), 4 * L);
+        if (u_cnt) memcpy(u_cnt, uc.data(), 4 * L);
+    }
+    if (sym) CK(c, cudaMemcpyAsync(sym, b->d.hc_sym, 4 * N, cudaMemcpyDeviceToHost, s));
+    if (koff) CK(c, cudaMemcpyAsync(koff, b->d.hc_koff, 4 * (N + L), cudaMemcpyDeviceToHost, s));
+    if (kids) CK(c, cudaMemcpyAsync(kids, b->d.hc_kids, 4 * K, cudaMemcpyDeviceToHost, s));
+    if (cid) CK(c, cudaMemcpyAsync(cid, b->d.hc_cid, 4 * N, cudaMemcpyDeviceToHost, s));
+    if (cost) CK(c, cudaMemcpyAsync(cost, b->d.hc_cost, 8 * N, cudaMemcpyDeviceToHost, s));
+    if (parent) CK(c, cudaMemcpyAsync(parent, b->d.uf_parent_in, 4 * U, cudaMemcpyDeviceToHost, s));
+    if (rank) CK(c, cudaMemcpyAsync(rank, b->d.uf_rank_in, U, cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
     return ESAT_OK;
 }
 

@@ -27,6 +27,7 @@ struct Dev {
     uint32_t* uf_parent;              // working / output union-find
     uint8_t* uf_rank;
     const uint32_t* root;
+    uint32_t *n_cnt, *u_cnt;          // live hashcons entries / ids per leaf (null: the base spans; set after an apply)
     // rebuild output: compacted hashcons
     uint32_t *o_n, *o_merges, *o_sym, *o_koff, *o_kids, *o_cid;
     double* o_cost;

@@ -1,0 +1,503 @@
+// K11: the apply loop of one MCTS rollout step -- apply_rule (rewrite.py:526-570) on every leaf
+// of a rebuilt batch, each leaf with its own rule, writing the leaf's dirty state (the input of
+// the next rebuild) in place of the batch's previous input.
+//
+// Per leaf the reference is strictly sequential: every match of the rule, in the sorted
+// joint_match order, sees the adds and unions of the matches before it (hashcons hits, class
+// membership for the cycle test, union-find roots). So one thread owns one leaf and replays
+// that order exactly; leaves run in parallel. The leaf state lives in the batch arrays:
+//   read:  rebuild output hashcons (o_*), working union-find (uf_parent/uf_rank), match lists
+//   write: hc_* (insertion-ordered hashcons, new entries appended), uf_*_in, per-leaf counts
+// Class membership (EGraph.classes[c].nodes, needed by would_create_cycle, rewrite.py:492-505)
+// is a linked list of hashcons entries per class root; union concatenates lists (egraph.py:
+// 189-201). class_shape (rewrite.py:286-290) is the shape of the head entry's symbol (tensor
+// e-classes are shape-homogeneous). Symbols are looked up by their identity key (apply.py).
+#include "esat_internal.cuh"
+#include "k_apply_args.cuh"
+
+namespace esat {
+
+namespace {
+
+constexpr int INSTR = 20;
+constexpr int MAXI = 24;      // instructions per target
+constexpr uint32_t NO_SHAPE = 255;
+enum Op : int { OP_UNK = 0, OP_INPUT, OP_WEIGHT, OP_EWADD, OP_EWMUL, OP_MATMUL, OP_CONV2D, OP_RELU, OP_TANH,
+                OP_SIGMOID, OP_CONCAT, OP_SPLIT, OP_MAXPOOL, OP_TRANSPOSE, OP_NOOP };
+constexpr int32_t INT_NONE = (int32_t)0x80000000;
+
+struct Shape {
+    uint32_t nd;   // NO_SHAPE: None
+    uint32_t d[4];
+};
+
+struct Sym {            // a symbol under construction (make_symbol)
+    int32_t name;       // name id (-1: never interned)
+    uint32_t arity, np;
+    uint32_t code[3];   // attribute codes (NO_MATCH_CODE: value absent from the table)
+    int32_t ival[3];    // attribute integer values
+    Shape shape;
+};
+
+struct Leaf {
+    const Dev* d;
+    const AArgs* a;
+    uint32_t l, cap_n, cap_k, cap_u;
+    uint32_t n, K, U;                 // live sizes
+    uint32_t *sym, *koff, *kids, *cid;
+    double* cost;
+    uint32_t* parent;
+    uint8_t* rank;
+    uint32_t *head, *tail, *next, *seen, *stack, *tab;
+    uint32_t tmask, stamp;
+    bool changed;
+};
+
+__device__ __forceinline__ uint32_t find(Leaf& L, uint32_t x) { return uf_find(L.parent, x); }
+
+__device__ Shape sym_shape(const AArgs& a, uint32_t s) {
+    Shape sh;
+    sh.nd = a.sym_ndim[s];
+    for (int i = 0; i < 4; i++) sh.d[i] = a.sym_dims[4 * s + i];
+    return sh;
+}
+
+__device__ __forceinline__ Shape class_shape(Leaf& L, uint32_t c) {
+    const uint32_t e = L.head[find(L, c)];
+    Shape sh;
+    sh.nd = NO_SHAPE;
+    if (e == NONE) return sh;
+    return sym_shape(*L.a, L.sym[e]);
+}
+
+__device__ __forceinline__ bool shape_eq(const Shape& x, const Shape& y) {
+    if (x.nd != y.nd) return false;
+    if (x.nd == NO_SHAPE) return true;
+    for (uint32_t i = 0; i < x.nd; i++)
+        if (x.d[i] != y.d[i]) return false;
+    return true;
+}
+
+// infer_shape (tensor_ir.py:64-126); false = ShapeError
+__device__ bool infer_shape(int op, const Sym& s, const Shape* in, uint32_t nin, Shape& out) {
+    if (op == OP_UNK || op == OP_INPUT || op == OP_WEIGHT) return false;
+    const uint32_t expect = op == OP_NOOP ? (nin > 1 ? nin : 1u)
+                            : (op == OP_RELU || op == OP_TANH || op == OP_SIGMOID || op == OP_SPLIT ||
+                               op == OP_MAXPOOL || op == OP_TRANSPOSE)
+                                ? 1u : 2u;
+    if (nin != expect) return false;
+    for (uint32_t i = 0; i < nin; i++) {   // check_shape: 1..4 dims, all >= 1
+        if (in[i].nd == NO_SHAPE || in[i].nd < 1 || in[i].nd > 4) return false;
+        for (uint32_t j = 0; j < in[i].nd; j++)
+            if (in[i].d[j] < 1) return false;
+    }
+    out.nd = NO_SHAPE;
+    switch (op) {
+        case OP_EWADD: case OP_EWMUL:
+            if (!shape_eq(in[0], in[1])) return false;
+            out = in[0];
+            return true;
+        case OP_MATMUL:
+            if (in[0].nd != 2 || in[1].nd != 2 || in[0].d[1] != in[1].d[0]) return false;
+            out.nd = 2; out.d[0] = in[0].d[0]; out.d[1] = in[1].d[1];
+            return true;
+        case OP_CONV2D: {
+            if (in[0].nd != 4 || in[1].nd != 4) return false;
+            if (in[0].d[1] != in[1].d[1]) return false;
+            if (s.ival[0] == INT_NONE || s.ival[1] == INT_NONE) return false;
+            const int64_t stride = s.ival[0], pad = s.ival[1];
+            if (stride == 0) return false;
+            // Python floor division
+            auto fdiv = [](int64_t x, int64_t y) { int64_t q = x / y; if ((x % y != 0) && ((x < 0) != (y < 0))) q--; return q; };
+            const int64_t oh = fdiv((int64_t)in[0].d[2] + 2 * pad - in[1].d[2], stride) + 1;
+            const int64_t ow = fdiv((int64_t)in[0].d[3] + 2 * pad - in[1].d[3], stride) + 1;
+            if (oh < 1 || ow < 1) return false;
+            out.nd = 4; out.d[0] = in[0].d[0]; out.d[1] = in[1].d[0]; out.d[2] = (uint32_t)oh; out.d[3] = (uint32_t)ow;
+            return true;
+        }
+        case OP_RELU: case OP_TANH: case OP_SIGMOID: case OP_NOOP:
+            out = in[0];
+            return true;
+        case OP_TRANSPOSE:
+            if (in[0].nd != 2) return false;
+            out.nd = 2; out.d[0] = in[0].d[1]; out.d[1] = in[0].d[0];
+            return true;
+        case OP_CONCAT: {
+            if (s.ival[0] == INT_NONE) return false;
+            const int64_t ax = s.ival[0];
+            if (in[0].nd != in[1].nd || ax < 0 || ax >= (int64_t)in[0].nd) return false;
+            for (uint32_t j = 0; j < in[0].nd; j++)
+                if ((int64_t)j != ax && in[0].d[j] != in[1].d[j]) return false;
+            out = in[0];
+            out.d[ax] = in[0].d[ax] + in[1].d[ax];
+            return true;
+        }
+        case OP_SPLIT: {
+            if (s.ival[0] == INT_NONE || s.ival[1] == INT_NONE) return false;
+            const int64_t ax = s.ival[0], idx = s.ival[1];
+            if (ax < 0 || ax >= (int64_t)in[0].nd) return false;
+            if (idx != 0 && idx != 1) return false;
+            if (in[0].d[ax] % 2 != 0) return false;
+            out = in[0];
+            out.d[ax] = in[0].d[ax] / 2;
+            return true;
+        }
+        case OP_MAXPOOL: {
+            if (s.ival[0] == INT_NONE || s.ival[1] == INT_NONE) return false;
+            const int64_t k = s.ival[0], st = s.ival[1];
+            if (in[0].nd != 4 || st == 0) return false;
+            auto fdiv = [](int64_t x, int64_t y) { int64_t q = x / y; if ((x % y != 0) && ((x < 0) != (y < 0))) q--; return q; };
+            const int64_t oh = fdiv((int64_t)in[0].d[2] - k, st) + 1, ow = fdiv((int64_t)in[0].d[3] - k, st) + 1;
+            if (oh < 1 || ow < 1) return false;
+            out.nd = 4; out.d[0] = in[0].d[0]; out.d[1] = in[0].d[1]; out.d[2] = (uint32_t)oh; out.d[3] = (uint32_t)ow;
+            return true;
+        }
+        default:
+            return false;
+    }
+}
+
+__device__ __forceinline__ uint32_t fnv(uint32_t h, uint32_t w) {
+    for (int s = 0; s < 32; s += 8) { h ^= (w >> s) & 0xFFu; h *= 16777619u; }
+    return h;
+}
+
+// symbol id of s, NONE if it was never interned (apply.py symbol_key_words / key_hash)
+__device__ uint32_t sym_lookup(const Dev& d, const AArgs& a, const Sym& s) {
+    if (s.name < 0) return NONE;
+    for (uint32_t i = 0; i < s.np; i++)
+        if (s.code[i] == NO_MATCH_CODE_U) return NONE;
+    uint32_t h = 2166136261u;
+    h = fnv(h, (uint32_t)s.name); h = fnv(h, s.arity); h = fnv(h, s.np);
+    for (uint32_t i = 0; i < s.np; i++) h = fnv(h, s.code[i]);
+    h = fnv(h, s.shape.nd);
+    if (s.shape.nd != NO_SHAPE)
+        for (uint32_t i = 0; i < s.shape.nd; i++) h = fnv(h, s.shape.d[i]);
+    for (uint32_t slot = h & a.sym_tmask;; slot = (slot + 1) & a.sym_tmask) {
+        const uint32_t c = a.sym_table[slot];
+        if (c == NONE) return NONE;
+        if (d.sym_name[c] != (uint32_t)s.name || d.sym_arity[c] != s.arity) continue;
+        const uint32_t p0 = d.sym_poff[c], pn = d.sym_poff[c + 1] - p0;
+        if (pn != s.np) continue;
+        bool ok = true;
+        for (uint32_t i = 0; i < pn && ok; i++) ok = (uint32_t)d.sym_par[p0 + i] == s.code[i];
+        if (!ok) continue;
+        const Shape cs = sym_shape(a, c);
+        if (!shape_eq(cs, s.shape)) continue;
+        return c;
+    }
+}
+
+// make_symbol (rewrite.py:296-298 / tensor_ir.py:253-265); false = InstantiationError
+__device__ bool make_symbol(const AArgs& a, const int32_t* ins, const uint32_t* rec, const Shape* cs, uint32_t nin,
+                            Sym& s) {
+    s.name = ins[1];
+    s.arity = nin;
+    s.np = 0;
+    s.shape.nd = NO_SHAPE;
+    if (a.lang == 0) return true;   // TermLanguage: payload is a function of the name
+    const int op = ins[2];
+    if (op == OP_UNK || op == OP_INPUT || op == OP_WEIGHT) return false;
+    static constexpr int NPARAM[15] = {0, 1, 1, 0, 0, 0, 3, 0, 0, 0, 1, 2, 2, 0, 0};
+    const int32_t np = ins[4] < 0 ? 0 : ins[4];
+    if (np != NPARAM[op]) return false;
+    s.np = (uint32_t)np;
+    for (int p = 0; p < np; p++) {
+        const int32_t tag = ins[9 + 3 * p], v = ins[10 + 3 * p];
+        if (tag == 1) {   // pvar: the code bound by the match
+            const uint32_t c = rec[v];
+            s.code[p] = c;
+            s.ival[p] = c < a.n_values ? a.val_int[c] : INT_NONE;
+        } else {
+            s.code[p] = tag == 0 ? (uint32_t)v : NO_MATCH_CODE_U;
+            s.ival[p] = ins[11 + 3 * p];
+        }
+    }
+    for (uint32_t i = 0; i < nin; i++)
+        if (cs[i].nd == NO_SHAPE) return false;   // missing child shape
+    return infer_shape(op, s, cs, nin, s.shape);
+}
+
+// node_cost (cost_model.py): f64, left-to-right products as in Python
+__device__ double node_cost(const AArgs& a, int op, const Sym& s, const Shape* in) {
+    if (a.cost_mode == 0) return 1.0;
+    const bool leaf = op == OP_INPUT || op == OP_WEIGHT || op == OP_NOOP;
+    if (a.cost_mode == 1) return leaf ? 0.0 : 1.0;
+    if (leaf) return a.coeff * 0.0;
+    double f;
+    if (op == OP_MATMUL) {
+        f = 2.0 * (double)in[0].d[0];
+        f = f * (double)in[0].d[1];
+        f = f * (double)in[1].d[1];
+    } else if (op == OP_CONV2D) {
+        f = 2.0 * (double)s.shape.d[0];
+        f = f * (double)in[1].d[1];
+        f = f * (double)in[1].d[2];
+        f = f * (double)in[1].d[3];
+        f = f * (double)s.shape.d[2];
+        f = f * (double)s.shape.d[3];
+        f = f * (double)in[1].d[0];
+    } else {
+        unsigned long long p = 1;
+        for (uint32_t i = 0; i < s.shape.nd; i++) p *= s.shape.d[i];
+        if (op == OP_MAXPOOL) p = p * (unsigned long long)s.ival[0] * (unsigned long long)s.ival[0];
+        f = (double)p;
+    }
+    return a.coeff * f;
+}
+
+__device__ __forceinline__ uint32_t node_hash(uint32_t sym, const uint32_t* k, uint32_t ar) {
+    uint64_t h = mix64(0x9e3779b97f4a7c15ull ^ sym);
+    for (uint32_t i = 0; i < ar; i++) h = mix64(h ^ ((uint64_t)k[i] + 0x632be59bd9b4e019ull * (i + 1)));
+    return (uint32_t)h;
+}
+
+// hashcons.get(node): the entry whose stored key equals (sym, kids), NONE if absent
+__device__ uint32_t hc_get(Leaf& L, uint32_t sym, const uint32_t* k, uint32_t ar) {
+    for (uint32_t s = node_hash(sym, k, ar) & L.tmask;; s = (s + 1) & L.tmask) {
+        const uint32_t e = L.tab[s];
+        if (e == NONE) return NONE;
+        if (L.sym[e] != sym || L.koff[e + 1] - L.koff[e] != ar) continue;
+        bool ok = true;
+        for (uint32_t i = 0; i < ar && ok; i++) ok = L.kids[L.koff[e] + i] == k[i];
+        if (ok) return e;
+    }
+}
+
+__device__ void hc_insert(Leaf& L, uint32_t e) {
+    const uint32_t ar = L.koff[e + 1] - L.koff[e];
+    uint32_t s = node_hash(L.sym[e], L.kids + L.koff[e], ar) & L.tmask;
+    while (L.tab[s] != NONE) s = (s + 1) & L.tmask;
+    L.tab[s] = e;
+}
+
+__device__ __forceinline__ void list_push(Leaf& L, uint32_t c, uint32_t e) {
+    L.next[e] = NONE;
+    if (L.head[c] == NONE) { L.head[c] = e; L.tail[c] = e; }
+    else { L.next[L.tail[c]] = e; L.tail[c] = e; }
+}
+
+// would_create_cycle (rewrite.py:492-505): is goal reachable from refs through child edges?
+__device__ bool reaches(Leaf& L, const uint32_t* refs, uint32_t nrefs, uint32_t goal, bool* overflow) {
+    const uint32_t st = ++L.stamp;
+    uint32_t sp = 0;
+    const uint32_t cap = L.cap_k + L.cap_n;
+    for (uint32_t i = 0; i < nrefs; i++) L.stack[sp++] = find(L, refs[i]);
+    while (sp) {
+        const uint32_t c = L.stack[--sp];
+        if (c == goal) return true;
+        if (L.seen[c] == st) continue;
+        L.seen[c] = st;
+        for (uint32_t e = L.head[c]; e != NONE; e = L.next[e])
+            for (uint32_t q = L.koff[e]; q < L.koff[e + 1]; q++) {
+                if (sp >= cap) { *overflow = true; return false; }
+                L.stack[sp++] = find(L, L.kids[q]);
+            }
+    }
+    return false;
+}
+
+// add (egraph.py:175-187); returns the class or NONE on failure (*err set)
+__device__ uint32_t add_node(Leaf& L, const Sym& s, int op, const uint32_t* k, const Shape* cs, uint32_t* err) {
+    const uint32_t sid = sym_lookup(*L.d, *L.a, s);
+    if (sid != NONE) {
+        const uint32_t e = hc_get(L, sid, k, s.arity);
+        if (e != NONE) return find(L, L.cid[e]);
+    }
+    if (sid == NONE) { *err = A_NEED_SYMBOL; return NONE; }
+    if (L.n + 1 > L.cap_n || L.K + s.arity > L.cap_k || L.U + 1 > L.cap_u) { *err = A_CAPACITY; return NONE; }
+    const uint32_t id = L.U++;
+    L.parent[id] = id;
+    L.rank[id] = 0;
+    L.head[id] = NONE;
+    L.seen[id] = 0;
+    const uint32_t e = L.n++;
+    L.sym[e] = sid;
+    for (uint32_t i = 0; i < s.arity; i++) L.kids[L.K + i] = k[i];
+    L.K += s.arity;
+    L.koff[e + 1] = L.K;
+    L.cid[e] = id;
+    L.cost[e] = node_cost(*L.a, op, s, cs);
+    hc_insert(L, e);
+    list_push(L, id, e);
+    L.changed = true;
+    return id;
+}
+
+__device__ void union_classes(Leaf& L, uint32_t a, uint32_t b) {
+    const uint32_t ra = find(L, a), rb = find(L, b);
+    if (ra == rb) return;
+    const uint32_t win = uf_union(L.parent, L.rank, ra, rb), lose = win == ra ? rb : ra;
+    if (L.head[lose] != NONE) {
+        if (L.head[win] == NONE) { L.head[win] = L.head[lose]; L.tail[win] = L.tail[lose]; }
+        else { L.next[L.tail[win]] = L.head[lose]; L.tail[win] = L.tail[lose]; }
+        L.head[lose] = NONE;
+    }
+    L.changed = true;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
+    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= d.L) return;
+    const uint32_t rule = a.leaf_rule[l];
+    uint32_t* rep = a.report + 4 * (uint64_t)l;
+    const uint64_t b = d.nb[l], k0 = d.kb[l], u0 = d.ub[l], t0 = d.tb[l];
+    Leaf L;
+    L.d = &d; L.a = &a; L.l = l;
+    L.cap_n = (uint32_t)(d.nb[l + 1] - b);
+    L.cap_k = (uint32_t)(d.kb[l + 1] - k0);
+    L.cap_u = (uint32_t)(d.ub[l + 1] - u0);
+    L.n = d.o_n[l];
+    L.U = d.n_cnt ? d.u_cnt[l] : L.cap_u;
+    L.sym = a.w_sym + b; L.koff = a.w_koff + b + l; L.kids = a.w_kids + k0; L.cid = a.w_cid + b;
+    L.cost = a.w_cost + b;
+    L.parent = a.w_parent + u0; L.rank = a.w_rank + u0;
+    L.head = a.s_head + u0; L.tail = a.s_tail + u0; L.next = a.s_next + b; L.seen = a.s_seen + u0;
+    L.stack = a.s_stack + b + k0;
+    L.tab = d.s_tc + t0;
+    L.tmask = (uint32_t)(d.tb[l + 1] - t0) - 1;
+    L.stamp = 0;
+    L.changed = false;
+    // the rebuilt state becomes the working state: hashcons entries (canonical keys, class =
+    // find(c)), union-find, class membership lists, lookup table
+    const uint32_t* okoff = d.o_koff + b + l;
+    L.koff[0] = 0;
+    for (uint32_t e = 0; e < L.n; e++) {
+        L.sym[e] = d.o_sym[b + e];
+        L.cid[e] = d.o_cid[b + e];
+        L.cost[e] = d.o_cost[b + e];
+        L.koff[e + 1] = okoff[e + 1];
+    }
+    L.K = okoff[L.n];
+    for (uint32_t q = 0; q < L.K; q++) L.kids[q] = d.o_kids[k0 + q];
+    for (uint32_t x = 0; x < L.U; x++) {
+        L.parent[x] = d.uf_parent[u0 + x];
+        L.rank[x] = d.uf_rank[u0 + x];
+        L.head[x] = NONE;
+        L.seen[x] = 0;
+    }
+    for (uint32_t s = 0; s <= L.tmask; s++) L.tab[s] = NONE;
+    for (uint32_t e = 0; e < L.n; e++) {
+        list_push(L, find(L, L.cid[e]), e);
+        hc_insert(L, e);
+    }
+    uint32_t st = A_OK, found = 0, cyc = 0, shp = 0;
+    if (rule != NONE && a.node_limit && L.n >= a.node_limit) st = A_NODE_LIMIT;   // rewrite.py:532-537
+    if (rule != NONE && st == A_OK) {
+        const int32_t* rp = a.prog + a.rule_off[rule];
+        const int32_t from_join = rp[0], li = rp[1], W = rp[2], NT = rp[6];
+        const uint64_t mi = (uint64_t)li * d.L + l;
+        const uint32_t* words = from_join ? a.j_words + a.j_off[mi] : a.m_words + a.m_off[mi];
+        const uint32_t cnt = from_join ? a.j_count[mi] : a.m_count[mi];
+        found = cnt;
+        for (uint32_t m = 0; m < cnt && st == A_OK; m++) {
+            const uint32_t* rec = words + (uint64_t)m * W;
+            for (int32_t t = 0; t < NT && st == A_OK; t++) {
+                const int32_t* tp = rp + rp[7 + t];
+                const uint32_t ni = (uint32_t)tp[0];
+                if (ni > MAXI) { st = A_PROGRAM; break; }
+                const uint32_t matched = find(L, rec[t]);
+                // _target_refs (rewrite.py:463-489): refs set, existing instance class
+                uint32_t cid[MAXI];          // class of instruction i (NONE: not existing)
+                uint32_t rbeg[MAXI], rend[MAXI];
+                uint32_t refs[64];
+                uint32_t nref = 0;
+                bool inst_err = false;
+                for (uint32_t i = 0; i < ni && !inst_err; i++) {
+                    const int32_t* ins = tp + 1 + INSTR * i;
+                    if (ins[0] == 0) {
+                        const uint32_t c = find(L, rec[ins[1]]);
+                        cid[i] = c;
+                        rbeg[i] = nref;
+                        if (nref < 64) refs[nref++] = c;
+                        rend[i] = nref;
+                        continue;
+                    }
+                    const uint32_t ar = (uint32_t)ins[3];
+                    uint32_t b0 = nref;
+                    bool all = true;
+                    uint32_t kc[4];
+                    for (uint32_t j = 0; j < ar; j++) {
+                        const uint32_t ci = (uint32_t)ins[5 + j];
+                        for (uint32_t r = rbeg[ci]; r < rend[ci]; r++)
+                            if (nref < 64) refs[nref++] = refs[r];
+                        if (cid[ci] == NONE) all = false;
+                        else kc[j] = cid[ci];
+                    }
+                    cid[i] = NONE;
+                    if (all) {
+                        Shape cs[4];
+                        for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, kc[j]);
+                        Sym s;
+                        if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
+                        const uint32_t sid = sym_lookup(d, a, s);
+                        const uint32_t e = sid == NONE ? NONE : hc_get(L, sid, kc, ar);
+                        if (e != NONE) {
+                            const uint32_t c = find(L, L.cid[e]);
+                            cid[i] = c;
+                            nref = b0;
+                            refs[nref++] = c;
+                        }
+                    }
+                    rbeg[i] = b0;
+                    rend[i] = nref;
+                }
+                if (nref >= 64) { st = A_PROGRAM; break; }
+                if (inst_err) { shp++; continue; }
+                const uint32_t top = ni - 1;
+                if (cid[top] != NONE && cid[top] == matched) continue;
+                bool ovf = false;
+                if (reaches(L, refs + rbeg[top], rend[top] - rbeg[top], matched, &ovf)) { cyc++; continue; }
+                if (ovf) { st = A_CAPACITY; break; }
+                // _instance_shape (rewrite.py:508-514) then the matched-class shape test
+                Shape sh[MAXI];
+                for (uint32_t i = 0; i < ni && !inst_err; i++) {
+                    const int32_t* ins = tp + 1 + INSTR * i;
+                    if (ins[0] == 0) { sh[i] = class_shape(L, rec[ins[1]]); continue; }
+                    const uint32_t ar = (uint32_t)ins[3];
+                    Shape cs[4];
+                    for (uint32_t j = 0; j < ar; j++) cs[j] = sh[ins[5 + j]];
+                    Sym s;
+                    if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
+                    sh[i] = s.shape;
+                }
+                if (inst_err) { shp++; continue; }
+                const Shape msh = class_shape(L, matched);
+                if (sh[top].nd != NO_SHAPE && msh.nd != NO_SHAPE && !shape_eq(sh[top], msh)) { shp++; continue; }
+                // _instantiate (rewrite.py:517-523) bottom-up, then union with the matched class
+                uint32_t inst[MAXI];
+                uint32_t err = A_OK;
+                for (uint32_t i = 0; i < ni && err == A_OK; i++) {
+                    const int32_t* ins = tp + 1 + INSTR * i;
+                    if (ins[0] == 0) { inst[i] = find(L, rec[ins[1]]); continue; }
+                    const uint32_t ar = (uint32_t)ins[3];
+                    uint32_t kc[4];
+                    Shape cs[4];
+                    for (uint32_t j = 0; j < ar; j++) { kc[j] = inst[ins[5 + j]]; cs[j] = class_shape(L, kc[j]); }
+                    Sym s;
+                    if (!make_symbol(a, ins, rec, cs, ar, s)) { err = A_PROGRAM; break; }   // checked above
+                    for (uint32_t j = 0; j < ar; j++) kc[j] = find(L, kc[j]);
+                    inst[i] = add_node(L, s, ins[2], kc, cs, &err);
+                    if (err == A_NEED_SYMBOL) {   // describe the missing symbol for host interning
+                        uint32_t* ms = a.missing + 16 * (uint64_t)l;
+                        ms[0] = (uint32_t)s.name; ms[1] = s.arity; ms[2] = s.np;
+                        for (int p = 0; p < 3; p++) { ms[3 + p] = s.code[p]; ms[6 + p] = (uint32_t)s.ival[p]; }
+                        ms[9] = s.shape.nd;
+                        for (int p = 0; p < 4; p++) ms[10 + p] = s.shape.d[p];
+                        ms[14] = (uint32_t)rule; ms[15] = (uint32_t)ins[2];
+                    }
+                }
+                if (err != A_OK) { st = err; break; }
+                union_classes(L, inst[top], matched);
+            }
+        }
+    }
+    d.n_cnt[l] = L.n;
+    d.u_cnt[l] = L.U;
+    a.status[l] = st;
+    rep[0] = found; rep[1] = L.changed ? 1u : 0u; rep[2] = cyc; rep[3] = shp;
+}
+
+}  // namespace esat

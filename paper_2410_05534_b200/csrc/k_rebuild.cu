@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d) {
     const uint32_t l = blockIdx.x;
     const uint32_t tid = threadIdx.x;
     const uint64_t b = d.nb[l], k0 = d.kb[l], u0 = d.ub[l], t0 = d.tb[l];
-    const uint32_t n0 = (uint32_t)(d.nb[l + 1] - b);
-    const uint32_t U = (uint32_t)(d.ub[l + 1] - u0);
+    const uint32_t n0 = d.n_cnt ? d.n_cnt[l] : (uint32_t)(d.nb[l + 1] - b);
+    const uint32_t U = d.n_cnt ? d.u_cnt[l] : (uint32_t)(d.ub[l + 1] - u0);
     const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
     uint32_t* parent = d.uf_parent + u0;
     uint8_t* rank = d.uf_rank + u0;

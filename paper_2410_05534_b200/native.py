@@ -62,8 +62,11 @@ def lib():
                      "esat_download_rebuild", "esat_download_view", "esat_download_matches",
                      "esat_download_extract", "esat_result_device_ptrs", "esat_ctx_set_stream",
                      "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork",
-                     "esat_batch_set_pool2"):
+                     "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
+                     "esat_download_apply", "esat_download_state"):
             getattr(L, name).restype = C.c_int
+        L.esat_apply_setup.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_uint32, vp, vp, C.c_uint32, vp,
+                                       C.c_uint32, vp, C.c_uint32, vp, vp]
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
         L.esat_batch_set_pool2.argtypes = [vp, C.c_double, C.c_double]
         _lib = L
@@ -76,7 +79,10 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_download_rebuild", "esat_download_view", "esat_download_matches", "esat_download_extract",
             "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results",
             "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork",
-            "esat_batch_set_pool2")
+            "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
+            "esat_download_apply", "esat_download_state")
+
+A_OK, A_NODE_LIMIT, A_NEED_SYMBOL, A_CAPACITY, A_PROGRAM = range(5)
 
 
 def _p(a):
@@ -135,6 +141,17 @@ class Context:
                 np.ascontiguousarray(arrays["params"], np.int32)]
         self.check(self.L.esat_symtab_upload(self.h, C.c_uint32(n), *[_p(a) for a in keep]))
 
+    def apply_setup(self, lang: int, cost_mode: int, coeff: float, sym: dict, rule_off, rule_words):
+        """Symbol identities + rule target programs for esat_apply (apply.py)."""
+        keep = [np.ascontiguousarray(sym["ndim"], np.uint8), _u32(sym["dims"]), _u32(sym["table"]),
+                np.ascontiguousarray(sym["vint"], np.int32), _u32(rule_off),
+                np.ascontiguousarray(rule_words, np.int32)]
+        self._apply_keep = keep
+        self.check(self.L.esat_apply_setup(self.h, lang, cost_mode, C.c_double(coeff), C.c_uint32(len(keep[0])),
+                                           _p(keep[0]), _p(keep[1]), C.c_uint32(len(keep[2])), _p(keep[2]),
+                                           C.c_uint32(len(keep[3])), _p(keep[3]), C.c_uint32(len(keep[4]) - 1),
+                                           _p(keep[4]), _p(keep[5])))
+
     def upload_patterns(self, programs: list):
         words = np.concatenate([np.asarray(p, np.int32) for p in programs]) if programs else np.zeros(1, np.int32)
         off = np.cumsum([0] + [len(p) for p in programs]).astype(np.uint32)
@@ -184,6 +201,31 @@ class DeviceBatch:
 
     def rebuild(self):
         self.ctx.check(self.L.esat_rebuild(self.h))
+
+    def set_counts(self, n_cnt, u_cnt):
+        self._cnt_keep = (_u32(n_cnt), _u32(u_cnt))
+        self.ctx.check(self.L.esat_batch_set_counts(self.h, *[_p(a) for a in self._cnt_keep]))
+
+    def apply(self, leaf_rule, node_limit: int = 0):
+        lr = _u32(leaf_rule)
+        self.ctx.check(self.L.esat_apply(self.h, _p(lr), C.c_uint32(node_limit)))
+
+    def download_apply(self) -> dict:
+        L = self.n_leaves
+        st, rep, miss = np.zeros(L, np.uint32), np.zeros((L, 4), np.uint32), np.zeros((L, 16), np.uint32)
+        self.ctx.check(self.L.esat_download_apply(self.h, _p(st), _p(rep), _p(miss)))
+        return {"status": st, "report": rep, "missing": miss}
+
+    def download_state(self) -> dict:
+        """The batch's input arena (dirty state after an apply) and live counts."""
+        L, N, K, U = self.n_leaves, self.N, self.K, self.U
+        o = {"n": np.zeros(L, np.uint32), "U": np.zeros(L, np.uint32), "hc_sym": np.zeros(N, np.uint32),
+             "hc_koff": np.zeros(N + L, np.uint32), "hc_kids": np.zeros(max(K, 1), np.uint32),
+             "hc_cid": np.zeros(N, np.uint32), "hc_cost": np.zeros(N, np.float64),
+             "uf_parent": np.zeros(U, np.uint32), "uf_rank": np.zeros(U, np.uint8)}
+        self.ctx.check(self.L.esat_download_state(self.h, *[_p(o[k]) for k in (
+            "n", "U", "hc_sym", "hc_koff", "hc_kids", "hc_cid", "hc_cost", "uf_parent", "uf_rank")]))
+        return o
 
     def set_pool(self, entries_per_node: float, bitsets_per_node: float | None = None):
         if bitsets_per_node is None:

@@ -122,6 +122,19 @@ class LeafPipeline:
 
     LAUNCHES_PER_STEP = 4  # k_rebuild, k_ematch, k_join, k_extract
 
+    def apply_programs(self, name_id, code) -> tuple:
+        """Target programs of every rule for esat_apply, wired to this pipeline's match lists
+        (single-source rules: the e-match list of their pattern; multi-pattern: their join)."""
+        from .apply import compile_rule_targets, pack_rules
+
+        progs = []
+        for r in self.rules:
+            if r.multi:
+                progs.append(compile_rule_targets(r.rule, name_id, code, None, 1, self.joins.index(r)))
+            else:
+                progs.append(compile_rule_targets(r.rule, name_id, code, None, 0, r.pattern_ids[0]))
+        return pack_rules(progs)
+
     def match_counts(self) -> np.ndarray:
         """Unique matches per rule per leaf of the last step: [rules, leaves]."""
         rows = []
