@@ -181,3 +181,85 @@ def pack_rules(programs: list) -> tuple:
         off[i + 1] = off[i] + len(p)
     words = np.concatenate(programs).astype(np.int32) if programs else np.zeros(1, np.int32)
     return off, words
+
+
+class ApplyDriver:
+    """Runs esat_apply over a LeafPipeline's batch with a live symbol table.
+
+    A leaf whose instantiation needs an operator symbol the table has never seen stops with
+    ESAT_A_NEED_SYMBOL and a descriptor of it; the driver interns those symbols here (exactly the
+    Symbol TensorLanguage/TermLanguage.make_symbol would have built), re-uploads the table, the
+    pattern and target programs (attribute codes are order-preserving, so they move), re-matches
+    on the unchanged rebuilt view and re-applies -- the rebuilt state is still intact on the device."""
+
+    def __init__(self, pipe, symtab, language, cost_config=None):
+        from .cost_model import CostModelConfig
+        from .tensor_ir import TensorLanguage
+
+        self.pipe, self.symtab, self.language = pipe, symtab, language
+        cfg = cost_config or CostModelConfig()
+        self.lang = LANG_TENSOR if isinstance(language, TensorLanguage) else LANG_TERM
+        self.cost_mode = {"term": COST_TERM, "unit": COST_UNIT, "analytic": COST_ANALYTIC}[cfg.mode]
+        self.coeff = float(cfg.coefficient)
+        self.interned = 0
+        self.upload()
+
+    def _name_id(self, name):
+        return self.symtab.name_id(name, create=False)
+
+    def upload(self):
+        st = self.symtab
+        st.finalize()
+        self.pipe.ctx.upload_symtab(st.arrays())
+        self.pipe.recompile(self._name_id, st.code)
+        off, words = self.pipe.apply_programs(self._name_id, st.code)
+        self.pipe.ctx.apply_setup(self.lang, self.cost_mode, self.coeff, symtab_symbol_arrays(st), off, words)
+
+    def _target_node(self, rule_idx: int, t: int, i: int):
+        order = []
+
+        def walk(p):
+            if not _is_var(p):
+                for c in p.children:
+                    walk(c)
+            order.append(p)
+
+        walk(self.pipe.rules[rule_idx].rule.targets[t])
+        return order[i]
+
+    def _intern(self, desc):
+        from .egraph import Symbol
+
+        p = self._target_node(int(desc[14]), int(desc[15]) >> 8, int(desc[15]) & 0xFF)
+        arity = int(desc[1])
+        if self.lang == LANG_TERM:
+            payload = int(p.name) if re.fullmatch(r"-?\d+", p.name) else None
+        else:
+            params = []
+            for j, s in enumerate(p.params or ()):
+                params.append(self.symtab.values[int(desc[3 + j])] if _is_pvar(s) else s)
+            nd = int(desc[9])
+            shape = None if nd == NO_SHAPE else tuple(int(x) for x in desc[10:10 + nd])
+            payload = (tuple(params), shape)
+        before = len(self.symtab)
+        self.symtab.intern(Symbol(p.name, arity, payload), self.language)
+        self.interned += len(self.symtab) - before
+
+    def apply(self, leaf_rule, node_limit: int = 0, max_rounds: int = 256) -> dict:
+        from . import native
+
+        b = self.pipe.batch
+        for _ in range(max_rounds):
+            b.apply(leaf_rule, node_limit)
+            res = b.download_apply()
+            need = np.nonzero(res["status"] == native.A_NEED_SYMBOL)[0]
+            if need.size == 0:
+                return res
+            before = len(self.symtab)
+            for l in need:
+                self._intern(res["missing"][l])
+            if len(self.symtab) == before:
+                raise RuntimeError("device asked for symbols that are already interned")
+            self.upload()
+            self.pipe.ematch()   # codes moved: re-derive the match records on the same view
+        raise RuntimeError("symbol interning did not converge")

@@ -114,7 +114,7 @@ struct esat_batch {
     std::vector<uint32_t> m_sig, j_sig;
     // apply loop: live counts (valid once set by esat_batch_set_counts or an apply) + scratch
     bool counts = false;
-    uint32_t *d_ncnt = nullptr, *d_ucnt = nullptr;
+    uint32_t *d_ncnt = nullptr, *d_ucnt = nullptr, *d_ureb = nullptr;
     uint32_t *a_rule = nullptr, *a_status = nullptr, *a_report = nullptr, *a_missing = nullptr;
     uint32_t *a_shead = nullptr, *a_stail = nullptr, *a_snext = nullptr, *a_sseen = nullptr, *a_sstack = nullptr;
 };
@@ -914,7 +914,8 @@ int esat_apply_setup(esat_ctx* c, int lang, int cost_mode, double coeff, uint32_
 static int ensure_apply_buffers(esat_batch* b) {
     if (b->d_ncnt) return ESAT_OK;
     const uint64_t N = b->N, K = b->K, U = b->U, L = b->L;
-    OWN(b->d_ncnt, L); OWN(b->d_ucnt, L);
+    OWN(b->d_ncnt, L); OWN(b->d_ucnt, L); OWN(b->d_ureb, L);
+    b->d.u_reb = b->d_ureb;
     OWN(b->a_rule, L); OWN(b->a_status, L); OWN(b->a_report, 4 * L); OWN(b->a_missing, 16 * L);
     OWN(b->a_shead, U); OWN(b->a_stail, U); OWN(b->a_sseen, U); OWN(b->a_snext, N); OWN(b->a_sstack, N + K);
     return ESAT_OK;
@@ -946,7 +947,7 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
     if (!b->rebuilt) return fail(c, ESAT_E_STATE, "apply requires a rebuilt e-graph");
     cudaSetDevice(c->device);
     int r;
-    if ((r = ensure_apply_buffers(b))) return r;
+    if (!b->d_ureb) return fail(c, ESAT_E_STATE, "esat_apply: call esat_batch_set_counts before the rebuild");
     if ((r = verify_matches(b))) return r;
     for (uint32_t l = 0; l < b->L; l++) {
         const uint32_t ru = leaf_rule[l];
@@ -959,16 +960,7 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
             return fail(c, ESAT_E_STATE, "rule %u: record width %d differs from the match list's", ru, W);
     }
     CK(c, cudaMemcpyAsync(b->a_rule, leaf_rule, 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
-    if (!b->counts) {   // first apply on a plain upload: counts are the arena spans
-        std::vector<uint32_t> nc(b->L), uc(b->L);
-        for (uint32_t l = 0; l < b->L; l++) {
-            nc[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]);
-            uc[l] = (uint32_t)(b->ub[l + 1] - b->ub[l]);
-        }
-        CK(c, cudaMemcpyAsync(b->d_ncnt, nc.data(), 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
-        CK(c, cudaMemcpyAsync(b->d_ucnt, uc.data(), 4ull * b->L, cudaMemcpyHostToDevice, c->stream));
-        CK(c, cudaStreamSynchronize(c->stream));
-    }
+    if (!b->counts) return fail(c, ESAT_E_STATE, "esat_apply: arena without live counts (esat_batch_set_counts)");
     Dev d = b->d;
     d.n_cnt = b->d_ncnt;
     d.u_cnt = b->d_ucnt;
@@ -995,7 +987,8 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
     b->counts = true;
     b->d.n_cnt = b->d_ncnt;
     b->d.u_cnt = b->d_ucnt;
-    b->rebuilt = false;
+    // the rebuilt view and the rebuild outputs still describe the pre-apply state, so an apply can
+    // be retried (after host interning of a missing symbol) until the next esat_rebuild
     b->upload_gen++;
     return ESAT_OK;
 }

@@ -28,6 +28,7 @@ struct Dev {
     uint8_t* uf_rank;
     const uint32_t* root;
     uint32_t *n_cnt, *u_cnt;          // live hashcons entries / ids per leaf (null: the base spans; set after an apply)
+    uint32_t* u_reb;                  // ids of the last rebuilt state (written by k_rebuild when non-null)
     // rebuild output: compacted hashcons
     uint32_t *o_n, *o_merges, *o_sym, *o_koff, *o_kids, *o_cid;
     double* o_cost;

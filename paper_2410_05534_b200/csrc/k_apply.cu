@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
     L.cap_k = (uint32_t)(d.kb[l + 1] - k0);
     L.cap_u = (uint32_t)(d.ub[l + 1] - u0);
     L.n = d.o_n[l];
-    L.U = d.n_cnt ? d.u_cnt[l] : L.cap_u;
+    L.U = d.u_reb[l];   // ids of the rebuilt state (an apply never changes the rebuild's outputs)
     L.sym = a.w_sym + b; L.koff = a.w_koff + b + l; L.kids = a.w_kids + k0; L.cid = a.w_cid + b;
     L.cost = a.w_cost + b;
     L.parent = a.w_parent + u0; L.rank = a.w_rank + u0;
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
                         for (int p = 0; p < 3; p++) { ms[3 + p] = s.code[p]; ms[6 + p] = (uint32_t)s.ival[p]; }
                         ms[9] = s.shape.nd;
                         for (int p = 0; p < 4; p++) ms[10 + p] = s.shape.d[p];
-                        ms[14] = (uint32_t)rule; ms[15] = (uint32_t)ins[2];
+                        ms[14] = (uint32_t)rule; ms[15] = ((uint32_t)t << 8) | i;   // target, instruction
                     }
                 }
                 if (err != A_OK) { st = err; break; }

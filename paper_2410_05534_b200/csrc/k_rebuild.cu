@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d) {
 
     PassIn in{d.hc_sym + b, d.hc_koff + b + l, d.hc_kids + k0, d.hc_cid + b, d.hc_cost + b};
     uint32_t n = n0;
-    if (tid == 0) sh_merges = 0;
+    if (tid == 0) { sh_merges = 0; if (d.u_reb) d.u_reb[l] = U; }
     // the working union-find starts as a copy of the leaf's input (snapshot semantics)
     for (uint32_t x = tid; x < U; x += T) { parent[x] = d.uf_parent_in[u0 + x]; rank[x] = d.uf_rank_in[u0 + x]; }
     __syncthreads();

@@ -66,6 +66,13 @@ class LeafPipeline:
         self.joins = [r for r in self.rules if r.multi]
         self.batch = None
 
+    def recompile(self, name_id, code):
+        """Recompile and re-upload the source patterns (after the symbol table changed)."""
+        rules = [r.rule for r in self.rules]
+        self.programs, self.rules = compile_rules(rules, name_id, code)
+        self.ctx.upload_patterns(self.programs)
+        self.joins = [r for r in self.rules if r.multi]
+
     def load(self, packed: dict):
         if self.batch is not None:
             self.batch.close()

@@ -106,3 +106,78 @@ def test_apply_matches_reference_rollouts(group):
     b.close()
     ctx.close()
     assert not bad, (len(bad), len(pairs), bad[:6])
+
+
+@pytest.mark.parametrize("group", ["toy", "analog_resnext50", "analog_inception_v3", "zoo"])
+def test_apply_interns_missing_symbols(group):
+    """Start from a live symbol table holding only the symbols of the pre-apply states: every new
+    operator symbol the rules instantiate comes back as ESAT_A_NEED_SYMBOL, is interned on the
+    host (ApplyDriver) and the apply is retried on the unchanged rebuilt view. The result must be
+    the reference's post-apply state, compared through symbol identities."""
+    import ast
+
+    from paper_2410_05534_b200 import native
+    from paper_2410_05534_b200.apply import ApplyDriver
+    from paper_2410_05534_b200.arena import Batch, LeafState, unpack_state
+    from paper_2410_05534_b200.cost_model import CostModelConfig
+    from paper_2410_05534_b200.egraph import Symbol
+    from paper_2410_05534_b200.pipeline import LeafPipeline
+    from paper_2410_05534_b200.symtab import SymbolTable
+    from paper_2410_05534_b200.tensor_ir import TensorLanguage, TermLanguage
+
+    lang, cost_mode, coeff = GROUPS[group]
+    g = load_group(group)
+    fs = FrozenSymtab(g["symtab"])
+    cases = g["cases"]
+    # first steps only: the table then lacks the symbols the first application creates
+    pairs = [(a, p) for a, p in consecutive_pairs(cases) if cases[a]["name"].endswith("/step0")]
+    rules = rules_of(g)
+    rule_pos = {r.id: i for i, r in enumerate(rules)}
+    gsyms = [Symbol(n, a, ast.literal_eval(p)) for n, a, p in fs.d["symbols"]]
+    gkey = [(s.name, s.arity, repr(s.payload)) for s in gsyms]
+    language = TensorLanguage() if lang else TermLanguage()
+    cfg = CostModelConfig(mode={0: "term", 1: "unit", 2: "analytic"}[cost_mode])
+    pre = [LeafState.from_json(cases[a]["state"]) for a, _ in pairs]
+    used = sorted({int(s) for lf in pre for s in lf.hc_sym})
+    st = SymbolTable()
+    remap = np.full(len(gsyms), 0xFFFFFFFF, np.uint32)
+    for s in used:
+        remap[s] = st.intern(gsyms[s], language)
+    for lf in pre:
+        lf.hc_sym = remap[lf.hc_sym]
+    packed = Batch(pre).pack_with_headroom(nodes=2048)
+    ctx = native.Context(0)
+    st.finalize()
+    pipe = LeafPipeline(ctx, st.arrays(), rules, lambda n: st.name_id(n, create=False), st.code)
+    b = pipe.load(packed)
+    b.set_counts(packed["n_cnt"], packed["u_cnt"])
+    pipe.rebuild()
+    drv = ApplyDriver(pipe, st, language, cfg)
+    pipe.ematch()
+    res = drv.apply(np.array([rule_pos[cases[post]["rule"]] for _, post in pairs], np.uint32))
+    fresh = {int(s) for _, p in pairs for s in cases[p]["state"]["hc_sym"]} - set(used)
+    assert drv.interned == len(fresh), (drv.interned, len(fresh))
+    state = b.download_state()
+    bad = []
+    for l, (_, post) in enumerate(pairs):
+        exp = cases[post]
+        if res["status"][l] != 0:
+            bad.append((exp["name"], "status", int(res["status"][l])))
+            continue
+        rep = exp["apply"]
+        if [int(x) for x in res["report"][l]] != [rep["matches_found"], int(rep["changed"]), rep["cycles_filtered"],
+                                                  rep["shape_filtered"]]:
+            bad.append((exp["name"], "report"))
+        got = unpack_state(packed, state, l)
+        want = LeafState.from_json(exp["state"])
+        keys_got = [(s.name, s.arity, repr(s.payload)) for s in (st.symbols[i] for i in got.hc_sym)]
+        if keys_got != [gkey[i] for i in want.hc_sym]:
+            bad.append((exp["name"], "symbols"))
+        for k in ("hc_koff", "hc_kids", "hc_cid", "uf_rank"):
+            if not np.array_equal(getattr(got, k), getattr(want, k)):
+                bad.append((exp["name"], k))
+        if not np.array_equal(got.hc_cost.view(np.uint64), want.hc_cost.view(np.uint64)):
+            bad.append((exp["name"], "hc_cost"))
+    b.close()
+    ctx.close()
+    assert not bad, (len(bad), len(pairs), bad[:6])
