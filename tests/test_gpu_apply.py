@@ -181,3 +181,56 @@ def test_apply_interns_missing_symbols(group):
     b.close()
     ctx.close()
     assert not bad, (len(bad), len(pairs), bad[:6])
+
+
+@pytest.mark.parametrize("group", ["toy", "zoo", "analog_nasrnn", "analog_inception_v3"])
+def test_device_resident_rollouts(group):
+    """Whole reference rollouts replayed on the device without leaving it: one leaf per rollout,
+    each step = rebuild -> e-match + join -> apply (the leaf's recorded rule), the arena's headroom
+    absorbing the growth. After every step each leaf must hold the reference's dirty state."""
+    from paper_2410_05534_b200 import native
+    from paper_2410_05534_b200.arena import Batch, LeafState, unpack_state
+    from paper_2410_05534_b200.pipeline import LeafPipeline
+
+    lang, cost_mode, coeff = GROUPS[group]
+    g = load_group(group)
+    fs = FrozenSymtab(g["symtab"])
+    cases = g["cases"]
+    seqs = {}
+    for i, c in enumerate(cases):
+        m = re.fullmatch(r"(.*)/step(\d+)", c["name"])
+        if m:
+            seqs.setdefault(m.group(1), {})[int(m.group(2))] = i
+    seqs = [s for s in seqs.values() if 0 in s and len(s) > 1]
+    rules = rules_of(g)
+    rule_pos = {r.id: i for i, r in enumerate(rules)}
+    packed = Batch([LeafState.from_json(cases[s[0]]["state"]) for s in seqs]).pack_with_headroom(nodes=6144)
+    ctx = native.Context(0)
+    pipe = LeafPipeline(ctx, fs.arrays, rules, fs.name_id, fs.code)
+    b = pipe.load(packed)
+    b.set_counts(packed["n_cnt"], packed["u_cnt"])
+    off, words = pipe.apply_programs(fs.name_id, fs.code)
+    ctx.apply_setup(lang, cost_mode, coeff, frozen_symbol_arrays(fs), off, words)
+    bad, checked = [], 0
+    for k in range(1, max(max(s) for s in seqs) + 1):
+        pipe.rebuild()
+        pipe.ematch()
+        lr = np.array([rule_pos[cases[s[k]]["rule"]] if k in s else 0xFFFFFFFF for s in seqs], np.uint32)
+        b.apply(lr)
+        res = b.download_apply()
+        st = b.download_state()
+        for l, s in enumerate(seqs):
+            if k not in s:
+                continue
+            checked += 1
+            want = LeafState.from_json(cases[s[k]]["state"])
+            got = unpack_state(packed, st, l)
+            same = (res["status"][l] == 0 and all(np.array_equal(getattr(got, f), getattr(want, f))
+                                                  for f in ("hc_sym", "hc_koff", "hc_kids", "hc_cid", "uf_rank"))
+                    and np.array_equal(got.hc_cost.view(np.uint64), want.hc_cost.view(np.uint64))
+                    and np.array_equal(find_all(got.uf_parent), find_all(want.uf_parent)))
+            if not same:
+                bad.append(cases[s[k]]["name"])
+    b.close()
+    ctx.close()
+    assert checked >= 5 and not bad, (checked, bad[:5])
