@@ -50,7 +50,7 @@ def load_golden_leaves(model: str):
     codes = {(type(v), v): i for i, v in enumerate(st["values"])}
     ref = np.array([float.fromhex(c["extract"]["ocf"]["cost"]) for c in g["cases"]])
     return (leaves, symarr, lambda n: names.get(n, -1), lambda v: codes.get((type(v), v), NO_MATCH_CODE), ref,
-            {"model": model, "source": "golden"})
+            {"model": model, "source": "golden", "symbols": st["symbols"], "values": st["values"]})
 
 
 def load_leaves(model: str):
@@ -78,6 +78,62 @@ def load_leaves(model: str):
 
     code = lambda v: codes.get((type(v), v), NO_MATCH_CODE)  # noqa: E731
     return leaves, symarr, name_id, code, z["ref_ocf"], meta
+
+
+def measure_apply(ctx, leaves, B: int, rotate: int, symarr, name_id, code, meta, reps: int = 10):
+    """k_apply (device apply loop) on the same leaves: every leaf applies one of its
+    live rules (1..600 matches, the rollouts' own draw rule, seeded), timed alone with CUDA events
+    (the apply reads the rebuilt state and rewrites the batch input, so repeats are identical)."""
+    import torch
+
+    from paper_2410_05534_b200.apply import LANG_TENSOR, COST_ANALYTIC, symbol_arrays
+    from paper_2410_05534_b200.arena import Batch
+    from paper_2410_05534_b200.pipeline import LeafPipeline
+
+    if not meta.get("symbols"):
+        return None
+    n = len(leaves)
+    packed = Batch([leaves[(rotate + i) % n] for i in range(B)]).pack_with_headroom(nodes=2048)
+    pipe = LeafPipeline(ctx, symarr, rules(), name_id, code)
+    b = pipe.load(packed)
+    b.set_counts(packed["n_cnt"], packed["u_cnt"])
+    pipe.rebuild()
+    pipe.ematch()
+    counts = pipe.match_counts()
+    rng = np.random.default_rng(0)
+    leaf_rule = np.full(B, 0xFFFFFFFF, np.uint32)
+    for l in range(B):
+        live = np.nonzero((counts[:, l] > 0) & (counts[:, l] <= meta.get("max_matches", 600)))[0]
+        if live.size:
+            leaf_rule[l] = int(rng.choice(live))
+    poff, flat = symarr["poff"], symarr["params"]
+    codes = [flat[poff[i]:poff[i + 1]] for i in range(len(symarr["name"]))]
+    sa = symbol_arrays(symarr["name"], symarr["arity"], [s[2] for s in meta["symbols"]], codes, meta["values"])
+    off, words = pipe.apply_programs(name_id, code)
+    ctx.apply_setup(LANG_TENSOR, COST_ANALYTIC, 1e-9, sa, off, words)
+    b.apply(leaf_rule)
+    res = b.download_apply()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        b.apply(leaf_rule)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    st = b.download_state()
+    reb = b.download_rebuild()
+    ok = res["status"] == 0
+    out = {"kernel_ms": ms, "leaf_applies_per_s": B / (ms / 1e3), "leaves": B,
+           "rule_choice": "uniform over each leaf's rules with 1..600 matches (seed 0)",
+           "status_counts": {str(k): int(v) for k, v in zip(*np.unique(res["status"], return_counts=True))},
+           "matches_applied": int(res["report"][ok, 0].sum()),
+           "changed_leaves": int(res["report"][ok, 1].sum()),
+           "cycles_filtered": int(res["report"][ok, 2].sum()), "shape_filtered": int(res["report"][ok, 3].sum()),
+           "nodes_added": int((st["n"].astype(np.int64) - reb["n"].astype(np.int64))[ok].sum()),
+           "parity": "tests/test_gpu_apply.py (reference rollouts, bit-exact)"}
+    b.close()
+    return out
 
 
 def make_batch(leaves, B: int, rotate: int):
@@ -391,6 +447,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = B * world * args.e2e_steps / e2e_s
+    apply_line = measure_apply(ctx, leaves, B, rank * B, symarr, name_id, code, meta)
 
     if rank != 0:
         if world > 1:
@@ -441,6 +498,7 @@ def main():
                                    "traffic": (json.loads(tr.read_text()).get(k) if tr.exists() else None)}
                                for k in abytes},
         "schedule": "k_rebuild -> [k_extract on a side stream || k_ematch -> k_join] -> join streams",
+        "apply": apply_line,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": pipe.LAUNCHES_PER_STEP * K,
         "clocks": clk.summary(),

@@ -65,7 +65,7 @@ def payload_shape(payload):
 
 
 def symbol_key_words(name_id: int, arity: int, codes, shape) -> list:
-    w = [name_id & 0xFFFFFFFF, arity, len(codes), *[c & 0xFFFFFFFF for c in codes]]
+    w = [int(name_id) & 0xFFFFFFFF, int(arity), len(codes), *[int(c) & 0xFFFFFFFF for c in codes]]
     if shape is None:
         w.append(NO_SHAPE)
     else:

@@ -981,7 +981,7 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
     a.s_head = b->a_shead; a.s_tail = b->a_stail; a.s_next = b->a_snext; a.s_seen = b->a_sseen;
     a.s_stack = b->a_sstack;
     tic(c);
-    if (b->L) k_apply<<<(b->L + 127) / 128, 128, 0, c->stream>>>(d, a);
+    if (b->L) k_apply<<<b->L, 32, 0, c->stream>>>(d, a);
     toc(c);
     if ((r = launch_check(c, "k_apply"))) return r;
     b->counts = true;

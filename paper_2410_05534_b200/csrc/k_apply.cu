@@ -49,7 +49,7 @@ struct Leaf {
     uint32_t* parent;
     uint8_t* rank;
     uint32_t *head, *tail, *next, *seen, *stack, *tab;
-    uint32_t tmask, stamp;
+    uint32_t tmask, stamp, lane;
     bool changed;
 };
 
@@ -278,23 +278,47 @@ __device__ __forceinline__ void list_push(Leaf& L, uint32_t c, uint32_t e) {
 }
 
 // would_create_cycle (rewrite.py:492-505): is goal reachable from refs through child edges?
-__device__ bool reaches(Leaf& L, const uint32_t* refs, uint32_t nrefs, uint32_t goal, bool* overflow) {
-    const uint32_t st = ++L.stamp;
-    uint32_t sp = 0;
-    const uint32_t cap = L.cap_k + L.cap_n;
-    for (uint32_t i = 0; i < nrefs; i++) L.stack[sp++] = find(L, refs[i]);
-    while (sp) {
-        const uint32_t c = L.stack[--sp];
-        if (c == goal) return true;
-        if (L.seen[c] == st) continue;
-        L.seen[c] = st;
-        for (uint32_t e = L.head[c]; e != NONE; e = L.next[e])
-            for (uint32_t q = L.koff[e]; q < L.koff[e + 1]; q++) {
-                if (sp >= cap) { *overflow = true; return false; }
-                L.stack[sp++] = find(L, L.kids[q]);
-            }
+// Warp-cooperative BFS (same reachable set as the reference's DFS): a queue of classes, 32 expanded
+// per step, children's roots claimed once per query with an epoch-stamped atomic exchange.
+__device__ bool reaches(Leaf& L, const uint32_t* refs, uint32_t nrefs, uint32_t goal, bool* overflow,
+                        uint32_t* qtail) {
+    const uint32_t st = ++L.stamp, cap = L.cap_k + L.cap_n;
+    bool found = false;
+    if (L.lane == 0) {
+        uint32_t qt = 0;
+        for (uint32_t i = 0; i < nrefs && !found; i++) {
+            const uint32_t c = find(L, refs[i]);
+            if (c == goal) found = true;
+            else if (L.seen[c] != st) { L.seen[c] = st; L.stack[qt++] = c; }
+        }
+        *qtail = qt;
     }
-    return false;
+    __syncwarp();
+    found = __shfl_sync(0xffffffffu, found, 0);
+    uint32_t qh = 0, qt = *qtail;
+    while (!found && qh < qt) {
+        const uint32_t idx = qh + L.lane;
+        if (idx < qt) {
+            const uint32_t c = L.stack[idx];
+            for (uint32_t e = L.head[c]; e != NONE && !found; e = L.next[e])
+                for (uint32_t q = L.koff[e]; q < L.koff[e + 1]; q++) {
+                    const uint32_t r = find(L, L.kids[q]);
+                    if (r == goal) { found = true; break; }
+                    if (atomicExch(&L.seen[r], st) != st) {
+                        const uint32_t pos = atomicAdd(qtail, 1u);
+                        if (pos < cap) L.stack[pos] = r;
+                        else *overflow = true;
+                    }
+                }
+        }
+        found = __any_sync(0xffffffffu, found);
+        __syncwarp();
+        qh = qh + 32 < qt ? qh + 32 : qt;
+        qt = *qtail;
+        if (qt > cap) { qt = cap; }
+    }
+    __syncwarp();
+    return found;
 }
 
 // add (egraph.py:175-187); returns the class or NONE on failure (*err set)
@@ -306,40 +330,50 @@ __device__ uint32_t add_node(Leaf& L, const Sym& s, int op, const uint32_t* k, c
     }
     if (sid == NONE) { *err = A_NEED_SYMBOL; return NONE; }
     if (L.n + 1 > L.cap_n || L.K + s.arity > L.cap_k || L.U + 1 > L.cap_u) { *err = A_CAPACITY; return NONE; }
-    const uint32_t id = L.U++;
-    L.parent[id] = id;
-    L.rank[id] = 0;
-    L.head[id] = NONE;
-    L.seen[id] = 0;
+    const uint32_t id = L.U++;   // every lane keeps the counters; lane 0 writes the state
     const uint32_t e = L.n++;
-    L.sym[e] = sid;
-    for (uint32_t i = 0; i < s.arity; i++) L.kids[L.K + i] = k[i];
+    const uint32_t k0 = L.K;
     L.K += s.arity;
-    L.koff[e + 1] = L.K;
-    L.cid[e] = id;
-    L.cost[e] = node_cost(*L.a, op, s, cs);
-    hc_insert(L, e);
-    list_push(L, id, e);
+    if (L.lane == 0) {
+        L.parent[id] = id;
+        L.rank[id] = 0;
+        L.head[id] = NONE;
+        L.seen[id] = 0;
+        L.sym[e] = sid;
+        for (uint32_t i = 0; i < s.arity; i++) L.kids[k0 + i] = k[i];
+        L.koff[e + 1] = L.K;
+        L.cid[e] = id;
+        L.cost[e] = node_cost(*L.a, op, s, cs);
+        hc_insert(L, e);
+        list_push(L, id, e);
+    }
+    __syncwarp();
     L.changed = true;
     return id;
 }
 
 __device__ void union_classes(Leaf& L, uint32_t a, uint32_t b) {
     const uint32_t ra = find(L, a), rb = find(L, b);
+    __syncwarp();
     if (ra == rb) return;
-    const uint32_t win = uf_union(L.parent, L.rank, ra, rb), lose = win == ra ? rb : ra;
-    if (L.head[lose] != NONE) {
-        if (L.head[win] == NONE) { L.head[win] = L.head[lose]; L.tail[win] = L.tail[lose]; }
-        else { L.next[L.tail[win]] = L.head[lose]; L.tail[win] = L.tail[lose]; }
-        L.head[lose] = NONE;
+    if (L.lane == 0) {
+        const uint32_t win = uf_union(L.parent, L.rank, ra, rb), lose = win == ra ? rb : ra;
+        if (L.head[lose] != NONE) {
+            if (L.head[win] == NONE) { L.head[win] = L.head[lose]; L.tail[win] = L.tail[lose]; }
+            else { L.next[L.tail[win]] = L.head[lose]; L.tail[win] = L.tail[lose]; }
+            L.head[lose] = NONE;
+        }
     }
+    __syncwarp();
     L.changed = true;
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
-    const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
+    // one warp per leaf: the lanes stage the rebuilt state into the working arrays, build the
+    // class lists and the lookup table; lane 0 then replays the matches in order
+    const uint32_t l = blockIdx.x, lane = threadIdx.x;
     if (l >= d.L) return;
     const uint32_t rule = a.leaf_rule[l];
     uint32_t* rep = a.report + 4 * (uint64_t)l;
@@ -360,29 +394,40 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
     L.tmask = (uint32_t)(d.tb[l + 1] - t0) - 1;
     L.stamp = 0;
     L.changed = false;
-    // the rebuilt state becomes the working state: hashcons entries (canonical keys, class =
-    // find(c)), union-find, class membership lists, lookup table
+    // the rebuilt state becomes the working state: hashcons entries (canonical keys, classes
+    // are roots), union-find, class membership lists, lookup table
     const uint32_t* okoff = d.o_koff + b + l;
-    L.koff[0] = 0;
-    for (uint32_t e = 0; e < L.n; e++) {
+    if (lane == 0) L.koff[0] = 0;
+    for (uint32_t e = lane; e < L.n; e += 32) {
         L.sym[e] = d.o_sym[b + e];
         L.cid[e] = d.o_cid[b + e];
         L.cost[e] = d.o_cost[b + e];
         L.koff[e + 1] = okoff[e + 1];
     }
     L.K = okoff[L.n];
-    for (uint32_t q = 0; q < L.K; q++) L.kids[q] = d.o_kids[k0 + q];
-    for (uint32_t x = 0; x < L.U; x++) {
+    for (uint32_t q = lane; q < L.K; q += 32) L.kids[q] = d.o_kids[k0 + q];
+    for (uint32_t x = lane; x < L.U; x += 32) {
         L.parent[x] = d.uf_parent[u0 + x];
         L.rank[x] = d.uf_rank[u0 + x];
         L.head[x] = NONE;
         L.seen[x] = 0;
     }
-    for (uint32_t s = 0; s <= L.tmask; s++) L.tab[s] = NONE;
-    for (uint32_t e = 0; e < L.n; e++) {
-        list_push(L, find(L, L.cid[e]), e);
-        hc_insert(L, e);
+    for (uint32_t s = lane; s <= L.tmask; s += 32) L.tab[s] = NONE;
+    __syncwarp();
+    for (uint32_t e = lane; e < L.n; e += 32) {
+        const uint32_t c = L.cid[e];   // rebuilt classes are union-find roots
+        const uint32_t old = atomicExch(&L.head[c], e);
+        L.next[e] = old;
+        if (old == NONE) L.tail[c] = e;
+        const uint32_t ar = L.koff[e + 1] - L.koff[e];
+        for (uint32_t s = node_hash(L.sym[e], L.kids + L.koff[e], ar) & L.tmask;; s = (s + 1) & L.tmask)
+            if (atomicCAS(&L.tab[s], NONE, e) == NONE) break;
     }
+    __syncwarp();
+    // from here every lane runs the same sequential replay (identical values in registers); state
+    // writes are issued by lane 0 and fenced with __syncwarp, the cycle test uses all lanes
+    __shared__ uint32_t sh_qtail;
+    L.lane = lane;
     uint32_t st = A_OK, found = 0, cyc = 0, shp = 0;
     if (rule != NONE && a.node_limit && L.n >= a.node_limit) st = A_NODE_LIMIT;   // rewrite.py:532-537
     if (rule != NONE && st == A_OK) {
@@ -449,7 +494,8 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
                 const uint32_t top = ni - 1;
                 if (cid[top] != NONE && cid[top] == matched) continue;
                 bool ovf = false;
-                if (reaches(L, refs + rbeg[top], rend[top] - rbeg[top], matched, &ovf)) { cyc++; continue; }
+                if (reaches(L, refs + rbeg[top], rend[top] - rbeg[top], matched, &ovf, &sh_qtail)) { cyc++; continue; }
+                ovf = __any_sync(0xffffffffu, ovf);
                 if (ovf) { st = A_CAPACITY; break; }
                 // _instance_shape (rewrite.py:508-514) then the matched-class shape test
                 Shape sh[MAXI];
@@ -480,7 +526,7 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
                     if (!make_symbol(a, ins, rec, cs, ar, s)) { err = A_PROGRAM; break; }   // checked above
                     for (uint32_t j = 0; j < ar; j++) kc[j] = find(L, kc[j]);
                     inst[i] = add_node(L, s, ins[2], kc, cs, &err);
-                    if (err == A_NEED_SYMBOL) {   // describe the missing symbol for host interning
+                    if (err == A_NEED_SYMBOL && lane == 0) {   // describe the missing symbol for host interning
                         uint32_t* ms = a.missing + 16 * (uint64_t)l;
                         ms[0] = (uint32_t)s.name; ms[1] = s.arity; ms[2] = s.np;
                         for (int p = 0; p < 3; p++) { ms[3 + p] = s.code[p]; ms[6 + p] = (uint32_t)s.ival[p]; }
@@ -494,6 +540,7 @@ __global__ void __launch_bounds__(128) k_apply(Dev d, AArgs a) {
             }
         }
     }
+    if (lane != 0) return;
     d.n_cnt[l] = L.n;
     d.u_cnt[l] = L.U;
     a.status[l] = st;

@@ -134,6 +134,7 @@ def main():
             sym_name=arr["name"], sym_arity=arr["arity"], sym_rank=arr["rank"], sym_poff=arr["poff"],
             sym_params=arr["params"],
             meta=np.array(json.dumps({"model": model, "names": gst.names, "values": gst.values,
+                                      "symbols": [[s.name, s.arity, repr(s.payload)] for s in gst.symbols],
                                       "max_matches": MAX_MATCHES, "node_limit": NODE_LIMIT})),
             ref_ocf=np.array([r[3] for r in res], np.float64),
             ref_default=np.array([r[4] for r in res], np.float64),
