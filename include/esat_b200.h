@@ -181,6 +181,14 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit);
 /* status[L], report[L][4] = {matches_found, changed, cycles_filtered, shape_filtered}
  * (ApplyReport, rewrite.py:440-448), missing[L][16] = descriptor of a symbol to intern */
 int esat_download_apply(esat_batch* b, uint32_t* status, uint32_t* report, uint32_t* missing);
+/* ---- WL fingerprint: EGraph.fingerprint (egraph.py:247-296) per rebuilt leaf ----
+ * krank[s] = rank of symbol s's key (name, arity, repr(payload)) in Python tuple order,
+ * key_bytes[key_off[s]:key_off[s+1]] = repr(key) (UTF-8) (paper_2410_05534_b200/fingerprint.py) */
+int esat_fingerprint_setup(esat_ctx* ctx, uint32_t n_syms, const uint32_t* krank, const uint32_t* key_off,
+                           const uint8_t* key_bytes);
+int esat_fingerprint(esat_batch* b);
+/* fp[L] = the reference's 64-bit fingerprint; status[L] 0 ok */
+int esat_download_fingerprint(esat_batch* b, uint64_t* fp, uint32_t* status);
 /* the batch input (dirty) arena with live counts: hashcons + union-find, spans as created */
 int esat_download_state(esat_batch* b, uint32_t* n_cnt, uint32_t* u_cnt, uint32_t* sym, uint32_t* koff,
                         uint32_t* kids, uint32_t* cid, double* cost, uint32_t* parent, uint8_t* rank);

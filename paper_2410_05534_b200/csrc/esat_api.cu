@@ -14,6 +14,7 @@ template <int T> __global__ void k_extract(Dev, XArgs);
 }  // namespace esat
 #include "k_ematch_args.cuh"
 #include "k_apply_args.cuh"
+#include "k_fingerprint_args.cuh"
 
 using namespace esat;
 
@@ -48,6 +49,10 @@ struct esat_ctx {
     uint32_t *a_dims = nullptr, *a_table = nullptr, *a_rule_off = nullptr;
     int32_t *a_vint = nullptr, *a_prog = nullptr;
     std::vector<int32_t> a_head;   // per rule: from_join, list index, W
+    // fingerprint setup (esat_fingerprint_setup)
+    uint32_t f_nsyms = 0;
+    uint32_t *f_krank = nullptr, *f_koff = nullptr;
+    uint8_t* f_kbytes = nullptr;
 };
 
 namespace {
@@ -117,6 +122,10 @@ struct esat_batch {
     uint32_t *d_ncnt = nullptr, *d_ucnt = nullptr, *d_ureb = nullptr;
     uint32_t *a_rule = nullptr, *a_status = nullptr, *a_report = nullptr, *a_missing = nullptr;
     uint32_t *a_shead = nullptr, *a_stail = nullptr, *a_snext = nullptr, *a_sseen = nullptr, *a_sstack = nullptr;
+    // fingerprint buffers
+    unsigned long long *f_lab0 = nullptr, *f_lab1 = nullptr, *f_tkey = nullptr, *f_fp = nullptr;
+    uint32_t *f_rep0 = nullptr, *f_rep1 = nullptr, *f_nord = nullptr, *f_tval = nullptr, *f_cord = nullptr,
+             *f_status = nullptr;
 };
 
 namespace {
@@ -1034,6 +1043,58 @@ int esat_download_state(esat_batch* b, uint32_t* n_cnt, uint32_t* u_cnt, uint32_
     if (parent) CK(c, cudaMemcpyAsync(parent, b->d.uf_parent_in, 4 * U, cudaMemcpyDeviceToHost, s));
     if (rank) CK(c, cudaMemcpyAsync(rank, b->d.uf_rank_in, U, cudaMemcpyDeviceToHost, s));
     CK(c, cudaStreamSynchronize(s));
+    return ESAT_OK;
+}
+
+
+// ---- WL fingerprint (K12) --------------------------------------------------------
+
+int esat_fingerprint_setup(esat_ctx* c, uint32_t n_syms, const uint32_t* krank, const uint32_t* key_off,
+                           const uint8_t* key_bytes) {
+    if (!c || !krank || !key_off || !key_bytes) return ESAT_E_ARG;
+    if (n_syms != c->n_syms) return fail(c, ESAT_E_STATE, "fingerprint symbols (%u) != symbol table (%u)", n_syms, c->n_syms);
+    cudaSetDevice(c->device);
+    int r;
+    const uint32_t nb = key_off[n_syms];
+    if ((r = dalloc(c, &c->f_krank, n_syms))) return r;
+    if ((r = dalloc(c, &c->f_koff, n_syms + 1))) return r;
+    if ((r = dalloc(c, &c->f_kbytes, nb ? nb : 1))) return r;
+    CK(c, cudaMemcpy(c->f_krank, krank, 4ull * n_syms, cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(c->f_koff, key_off, 4ull * (n_syms + 1), cudaMemcpyHostToDevice));
+    if (nb) CK(c, cudaMemcpy(c->f_kbytes, key_bytes, nb, cudaMemcpyHostToDevice));
+    c->f_nsyms = n_syms;
+    return ESAT_OK;
+}
+
+int esat_fingerprint(esat_batch* b) {
+    if (!b) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!c->f_krank || c->f_nsyms != c->n_syms) return fail(c, ESAT_E_STATE, "esat_fingerprint_setup not called for this symbol table");
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "fingerprint requires a rebuilt e-graph");
+    cudaSetDevice(c->device);
+    if (!b->f_lab0) {
+        const uint64_t N = b->N, T = b->T, L = b->L;
+        OWN(b->f_lab0, N); OWN(b->f_lab1, N); OWN(b->f_rep0, N); OWN(b->f_rep1, N); OWN(b->f_nord, N);
+        OWN(b->f_tkey, T); OWN(b->f_tval, T); OWN(b->f_cord, T); OWN(b->f_fp, L); OWN(b->f_status, L);
+    }
+    FArgs a{};
+    a.krank = c->f_krank; a.key_off = c->f_koff; a.key_bytes = c->f_kbytes;
+    a.lab0 = b->f_lab0; a.lab1 = b->f_lab1; a.rep0 = b->f_rep0; a.rep1 = b->f_rep1; a.nord = b->f_nord;
+    a.tkey = b->f_tkey; a.tval = b->f_tval; a.cord = b->f_cord; a.fp = b->f_fp; a.status = b->f_status;
+    tic(c);
+    if (b->L) k_fingerprint<128><<<b->L, 128, 0, c->stream>>>(b->d, a);
+    toc(c);
+    return launch_check(c, "k_fingerprint");
+}
+
+int esat_download_fingerprint(esat_batch* b, uint64_t* fp, uint32_t* status) {
+    if (!b) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    if (!b->f_fp) return fail(c, ESAT_E_STATE, "no fingerprints computed");
+    cudaSetDevice(c->device);
+    if (fp) CK(c, cudaMemcpyAsync(fp, b->f_fp, 8ull * b->L, cudaMemcpyDeviceToHost, c->stream));
+    if (status) CK(c, cudaMemcpyAsync(status, b->f_status, 4ull * b->L, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
     return ESAT_OK;
 }
 

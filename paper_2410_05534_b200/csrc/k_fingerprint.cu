@@ -1,0 +1,310 @@
+// K12: EGraph.fingerprint (egraph.py:247-296) for every leaf of a rebuilt batch -- the
+// Weisfeiler-Lehman class refinement whose 64-bit result keys the MCTS extraction cache
+// (SURVEY §8(f)2). Bit-exact: labels are BLAKE2b-64 digests (egraph.py:124-129) of the very
+// bytes Python's repr() produces for the sorted tuples the reference hashes, so the device
+// streams those bytes into its own BLAKE2b instead of building Python objects:
+//   label0(c)   = H(repr(sorted(symbol.key() of c's nodes)))
+//   label_r(c)  = H(repr(sorted((symbol.key(), (label_{r-1}(child), ...)) for c's nodes)))
+// until the induced partition (class -> smallest class id with the same label) repeats, at most
+// max(1, C) rounds; then fp = H(repr(sorted(sorted descriptions per class)), repr(root label)).
+// symbol.key() is (name, arity, repr(payload)); its repr bytes and its rank among all keys
+// (Python tuple order) come from the host (fingerprint.py).
+//
+// Schedule: one CTA per leaf. Per round a thread owns a class (sorts its node descriptions,
+// streams their repr into BLAKE2b); the partition is recomputed with an atomicMin hash table
+// keyed by label; the final class order is a CTA bitonic sort with the list comparator, and one
+// thread streams the body.
+#include "esat_internal.cuh"
+#include "k_fingerprint_args.cuh"
+
+namespace esat {
+
+namespace {
+
+__constant__ uint64_t B2B_IV[8] = {0x6a09e667f3bcc908ull, 0xbb67ae8584caa73bull, 0x3c6ef372fe94f82bull,
+                                   0xa54ff53a5f1d36f1ull, 0x510e527fade682d1ull, 0x9b05688c2b3e6c1full,
+                                   0x1f83d9abfb41bd6bull, 0x5be0cd19137e2179ull};
+__constant__ uint8_t B2B_SIGMA[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+__device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(digest_size=8))
+    uint64_t h[8];
+    uint64_t t;
+    uint32_t n;
+    uint8_t buf[128];
+
+    __device__ void init() {
+        for (int i = 0; i < 8; i++) h[i] = B2B_IV[i];
+        h[0] ^= 0x01010008ull;
+        t = 0;
+        n = 0;
+    }
+    __device__ void compress(bool last) {
+        uint64_t m[16], v[16];
+        for (int i = 0; i < 16; i++) {
+            uint64_t w = 0;
+            for (int b = 7; b >= 0; b--) w = (w << 8) | buf[8 * i + b];
+            m[i] = w;
+        }
+        for (int i = 0; i < 8; i++) { v[i] = h[i]; v[i + 8] = B2B_IV[i]; }
+        v[12] ^= t;
+        if (last) v[14] = ~v[14];
+#pragma unroll 1
+        for (int r = 0; r < 12; r++) {
+            const uint8_t* s = B2B_SIGMA[r];
+#define B2G(a, b, c, d, x, y)                         \
+    v[a] = v[a] + v[b] + x; v[d] = rotr(v[d] ^ v[a], 32); \
+    v[c] = v[c] + v[d];     v[b] = rotr(v[b] ^ v[c], 24); \
+    v[a] = v[a] + v[b] + y; v[d] = rotr(v[d] ^ v[a], 16); \
+    v[c] = v[c] + v[d];     v[b] = rotr(v[b] ^ v[c], 63);
+            B2G(0, 4, 8, 12, m[s[0]], m[s[1]]);
+            B2G(1, 5, 9, 13, m[s[2]], m[s[3]]);
+            B2G(2, 6, 10, 14, m[s[4]], m[s[5]]);
+            B2G(3, 7, 11, 15, m[s[6]], m[s[7]]);
+            B2G(0, 5, 10, 15, m[s[8]], m[s[9]]);
+            B2G(1, 6, 11, 12, m[s[10]], m[s[11]]);
+            B2G(2, 7, 8, 13, m[s[12]], m[s[13]]);
+            B2G(3, 4, 9, 14, m[s[14]], m[s[15]]);
+#undef B2G
+        }
+        for (int i = 0; i < 8; i++) h[i] ^= v[i] ^ v[i + 8];
+    }
+    __device__ __forceinline__ void put(uint8_t c) {
+        if (n == 128) { t += 128; compress(false); n = 0; }
+        buf[n++] = c;
+    }
+    __device__ void puts(const char* s) { while (*s) put((uint8_t)*s++); }
+    __device__ void putb(const uint8_t* s, uint32_t len) { for (uint32_t i = 0; i < len; i++) put(s[i]); }
+    __device__ void putu(uint64_t x) {   // decimal repr of a non-negative int
+        char d[24];
+        int k = 0;
+        do { d[k++] = (char)('0' + x % 10); x /= 10; } while (x);
+        while (k) put((uint8_t)d[--k]);
+    }
+    // int.from_bytes(digest, "big"): the digest is h[0] little-endian
+    __device__ uint64_t final() {
+        t += n;
+        for (uint32_t i = n; i < 128; i++) buf[i] = 0;
+        compress(true);
+        return __byte_perm((uint32_t)(h[0] >> 32), 0, 0x0123) | ((uint64_t)__byte_perm((uint32_t)h[0], 0, 0x0123) << 32);
+    }
+};
+
+struct Leaf {
+    const Dev* d;
+    const FArgs* a;
+    uint32_t C;
+    const uint32_t *coff, *nko, *kpos, *nsym;
+};
+
+// description order of two nodes: (symbol key rank, child labels lexicographic)
+__device__ __forceinline__ bool desc_less(const Leaf& L, const unsigned long long* lab, uint32_t x, uint32_t y) {
+    const uint32_t sx = L.nsym[x], sy = L.nsym[y];
+    const uint32_t rx = L.a->krank[sx], ry = L.a->krank[sy];
+    if (rx != ry) return rx < ry;
+    const uint32_t qx = L.nko[x], ax = L.nko[x + 1] - qx, qy = L.nko[y], ay = L.nko[y + 1] - qy;
+    const uint32_t m = ax < ay ? ax : ay;
+    for (uint32_t i = 0; i < m; i++) {
+        const uint64_t lx = lab[L.kpos[qx + i]], ly = lab[L.kpos[qy + i]];
+        if (lx != ly) return lx < ly;
+    }
+    return ax < ay;
+}
+
+// sorts class c's nodes by description into ord[] (the class's own span of nord); returns the count
+__device__ uint32_t sorted_nodes(const Leaf& L, const unsigned long long* lab, uint32_t c, uint32_t* ord, bool with_labels) {
+    const uint32_t n0 = L.coff[c], nn = L.coff[c + 1] - n0;
+    for (uint32_t i = 0; i < nn; i++) {
+        const uint32_t x = n0 + i;
+        uint32_t j = i;
+        while (j > 0) {
+            const uint32_t y = ord[j - 1];
+            const bool lt = with_labels ? desc_less(L, lab, x, y) : L.a->krank[L.nsym[x]] < L.a->krank[L.nsym[y]];
+            if (!lt) break;
+            ord[j] = y;
+            j--;
+        }
+        ord[j] = x;
+    }
+    return nn;
+}
+
+__device__ void put_key(const Leaf& L, B2b& h, uint32_t sym) {
+    const uint32_t o = L.a->key_off[sym], e = L.a->key_off[sym + 1];
+    h.putb(L.a->key_bytes + o, e - o);
+}
+
+// repr((symbol.key(), (label, ...)))
+__device__ void put_desc(const Leaf& L, B2b& h, const unsigned long long* lab, uint32_t x) {
+    h.put('(');
+    put_key(L, h, L.nsym[x]);
+    h.puts(", (");
+    const uint32_t q = L.nko[x], ar = L.nko[x + 1] - q;
+    for (uint32_t i = 0; i < ar; i++) {
+        if (i) h.puts(", ");
+        h.putu(lab[L.kpos[q + i]]);
+    }
+    if (ar == 1) h.put(',');
+    h.puts("))");
+}
+
+__device__ bool class_less(const Leaf& L, const unsigned long long* lab, const uint32_t* nord, uint32_t a, uint32_t b) {
+    const uint32_t na = L.coff[a + 1] - L.coff[a], nb = L.coff[b + 1] - L.coff[b];
+    const uint32_t m = na < nb ? na : nb;
+    for (uint32_t i = 0; i < m; i++) {
+        const uint32_t x = nord[L.coff[a] + i], y = nord[L.coff[b] + i];
+        if (desc_less(L, lab, x, y)) return true;
+        if (desc_less(L, lab, y, x)) return false;
+    }
+    return na < nb;
+}
+
+}  // namespace
+
+template <int T>
+__global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
+    const uint32_t l = blockIdx.x, tid = threadIdx.x;
+    const uint64_t b = d.nb[l], t0 = d.tb[l];
+    Leaf L;
+    L.d = &d; L.a = &a;
+    L.C = d.v_C[l];
+    L.coff = d.cls_off + b + l;
+    L.nko = d.nd_koff + b + l;
+    L.kpos = d.nd_kpos + d.kb[l];
+    L.nsym = d.nd_sym + b;
+    const uint32_t C = L.C;
+    unsigned long long* lab[2] = {a.lab0 + b, a.lab1 + b};
+    uint32_t* rep[2] = {a.rep0 + b, a.rep1 + b};
+    uint32_t* nord = a.nord + b;
+    const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
+    unsigned long long* tkey = a.tkey + t0;
+    uint32_t* tval = a.tval + t0;
+    __shared__ uint32_t sh_bad, sh_changed;
+    if (tid == 0) sh_bad = 0;
+    __syncthreads();
+    // round 0: labels from the sorted symbol keys
+    for (uint32_t c = tid; c < C; c += T) {
+        uint32_t* ord = nord + L.coff[c];
+        const uint32_t nn = sorted_nodes(L, nullptr, c, ord, false);
+        B2b h;
+        h.init();
+        h.put('[');
+        for (uint32_t i = 0; i < nn; i++) {
+            if (i) h.puts(", ");
+            put_key(L, h, L.nsym[ord[i]]);
+        }
+        h.put(']');
+        h.put(0x1f);
+        lab[0][c] = h.final();
+        rep[0][c] = NONE;
+    }
+    __syncthreads();
+    int cur = 0;
+    const uint32_t rounds = C > 1 ? C : 1;
+    for (uint32_t it = 0; it < rounds && !sh_bad; it++) {
+        const unsigned long long* lc = lab[cur];
+        unsigned long long* ln = lab[cur ^ 1];
+        for (uint32_t c = tid; c < C; c += T) {
+            uint32_t* ord = nord + L.coff[c];
+            const uint32_t nn = sorted_nodes(L, lc, c, ord, true);
+            B2b h;
+            h.init();
+            h.put('[');
+            for (uint32_t i = 0; i < nn; i++) {
+                if (i) h.puts(", ");
+                put_desc(L, h, lc, ord[i]);
+            }
+            h.put(']');
+            h.put(0x1f);
+            ln[c] = h.final();
+        }
+        for (uint32_t s = tid; s < tsz; s += T) { tkey[s] = ~0ull; tval[s] = NONE; }
+        if (tid == 0) sh_changed = 0;
+        __syncthreads();
+        // partition: every class -> smallest class position (= smallest id) with its label
+        for (uint32_t c = tid; c < C; c += T) {
+            const unsigned long long key = ln[c];
+            uint32_t s = (uint32_t)(mix64(key) & tmask);
+            while (true) {
+                const unsigned long long prev = atomicCAS(&tkey[s], ~0ull, key);
+                if (prev == ~0ull || prev == key) break;
+                s = (s + 1) & tmask;
+            }
+            atomicMin(&tval[s], c);
+        }
+        __syncthreads();
+        uint32_t* rp = rep[cur ^ 1];
+        const uint32_t* rq = rep[cur];
+        for (uint32_t c = tid; c < C; c += T) {
+            const unsigned long long key = ln[c];
+            uint32_t s = (uint32_t)(mix64(key) & tmask);
+            while (tkey[s] != key) s = (s + 1) & tmask;
+            rp[c] = tval[s];
+            if (it == 0 || rp[c] != rq[c]) sh_changed = 1;   // the first partition never matches None
+        }
+        __syncthreads();
+        cur ^= 1;
+        const bool stop = !sh_changed;
+        __syncthreads();
+        if (stop) break;
+    }
+    if (sh_bad) {
+        if (tid == 0) { a.status[l] = 1; a.fp[l] = 0; }
+        return;
+    }
+    // body: classes sorted by their sorted descriptions (final labels)
+    const unsigned long long* lf = lab[cur];
+    for (uint32_t c = tid; c < C; c += T) sorted_nodes(L, lf, c, nord + L.coff[c], true);
+    uint32_t P = 1;
+    while (P < C) P <<= 1;
+    uint32_t* cord = a.cord + t0;   // tb rows: >= 2n >= P
+    for (uint32_t i = tid; i < P; i += T) cord[i] = i < C ? i : NONE;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = tid; i < P; i += T) {
+                const uint32_t p = i ^ j;
+                if (p <= i) continue;
+                const uint32_t x = cord[i], y = cord[p];
+                const bool up = (i & k) == 0;
+                // NONE (padding) sorts last
+                const bool gt = x == NONE ? y != NONE : (y != NONE && class_less(L, lf, nord, y, x));
+                if (gt == up) { cord[i] = y; cord[p] = x; }
+            }
+            __syncthreads();
+        }
+    if (tid == 0) {
+        B2b h;
+        h.init();
+        h.put('[');
+        for (uint32_t i = 0; i < C; i++) {
+            const uint32_t c = cord[i];
+            if (i) h.puts(", ");
+            h.put('[');
+            for (uint32_t q = L.coff[c]; q < L.coff[c + 1]; q++) {
+                if (q != L.coff[c]) h.puts(", ");
+                put_desc(L, h, lf, nord[q]);
+            }
+            h.put(']');
+        }
+        h.put(']');
+        h.put(0x1f);
+        const uint32_t rp = d.v_root[l];
+        if (rp == NONE) h.puts("None");
+        else h.putu(lf[rp]);
+        h.put(0x1f);
+        a.fp[l] = h.final();
+        a.status[l] = 0;
+    }
+}
+
+template __global__ void k_fingerprint<128>(Dev, FArgs);
+
+}  // namespace esat

@@ -63,7 +63,8 @@ def lib():
                      "esat_download_extract", "esat_result_device_ptrs", "esat_ctx_set_stream",
                      "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork",
                      "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
-                     "esat_download_apply", "esat_download_state"):
+                     "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
+                     "esat_download_fingerprint"):
             getattr(L, name).restype = C.c_int
         L.esat_apply_setup.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_uint32, vp, vp, C.c_uint32, vp,
                                        C.c_uint32, vp, C.c_uint32, vp, vp]
@@ -80,7 +81,8 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_result_device_ptrs", "esat_last_kernel_ms", "esat_ctx_set_stream", "esat_copy_results",
             "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork",
             "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
-            "esat_download_apply", "esat_download_state")
+            "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
+            "esat_download_fingerprint")
 
 A_OK, A_NODE_LIMIT, A_NEED_SYMBOL, A_CAPACITY, A_PROGRAM = range(5)
 
@@ -152,6 +154,11 @@ class Context:
                                            C.c_uint32(len(keep[3])), _p(keep[3]), C.c_uint32(len(keep[4]) - 1),
                                            _p(keep[4]), _p(keep[5])))
 
+    def fingerprint_setup(self, krank, key_off, key_bytes):
+        keep = [_u32(krank), _u32(key_off), np.frombuffer(bytes(key_bytes), np.uint8).copy()]
+        self._fp_keep = keep
+        self.check(self.L.esat_fingerprint_setup(self.h, C.c_uint32(len(keep[0])), *[_p(a) for a in keep]))
+
     def upload_patterns(self, programs: list):
         words = np.concatenate([np.asarray(p, np.int32) for p in programs]) if programs else np.zeros(1, np.int32)
         off = np.cumsum([0] + [len(p) for p in programs]).astype(np.uint32)
@@ -209,6 +216,14 @@ class DeviceBatch:
     def apply(self, leaf_rule, node_limit: int = 0):
         lr = _u32(leaf_rule)
         self.ctx.check(self.L.esat_apply(self.h, _p(lr), C.c_uint32(node_limit)))
+
+    def fingerprint(self):
+        self.ctx.check(self.L.esat_fingerprint(self.h))
+
+    def download_fingerprint(self):
+        fp, st = np.zeros(self.n_leaves, np.uint64), np.zeros(self.n_leaves, np.uint32)
+        self.ctx.check(self.L.esat_download_fingerprint(self.h, _p(fp), _p(st)))
+        return fp, st
 
     def download_apply(self) -> dict:
         L = self.n_leaves

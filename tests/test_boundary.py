@@ -66,3 +66,15 @@ def test_pattern_program_layout():
     assert rec0[0] == 1 and rec0[1] == 3 and rec0[2] == 2 and rec0[3] == 3
     slots = prog[rec0[4]: rec0[4] + 3]
     assert slots.tolist() == [-(1 + 1), -(0 + 1), 9]  # ?s -> pvar 1 (sorted p,s), ?p -> 0, literal none
+
+
+def test_fingerprint_key_tables():
+    """Host tables of the device fingerprint: key ranks in Python tuple order, repr bytes exact."""
+    from paper_2410_05534_b200.fingerprint import key_tables
+
+    keys = [("relu", 1, "((), (4, 8))"), ("matmul", 2, "((), (4, 8))"), ("conv2d", 2, "((1, 0, 'relu'), (1, 2))"),
+            ("matmul", 2, "((), (16, 8))")]
+    krank, off, blob = key_tables(keys)
+    assert [keys[i] for i in np.argsort(krank)] == sorted(keys)
+    for i, k in enumerate(keys):
+        assert blob[off[i]:off[i + 1]] == repr(k).encode()
