@@ -136,6 +136,31 @@ def measure_apply(ctx, leaves, B: int, rotate: int, symarr, name_id, code, meta,
     return out
 
 
+def measure_fingerprint(ctx, batch, meta, reps: int = 10):
+    """k_fingerprint (EGraph.fingerprint: the MCTS extraction-cache key) on the
+    rebuilt leaves of the main batch, timed alone with CUDA events."""
+    import torch
+
+    from paper_2410_05534_b200.fingerprint import key_tables
+
+    if not meta.get("symbols"):
+        return None
+    ctx.fingerprint_setup(*key_tables([tuple(s) for s in meta["symbols"]]))
+    batch.fingerprint()
+    fp, status = batch.download_fingerprint()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        batch.fingerprint()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"kernel_ms": ms, "leaf_fingerprints_per_s": batch.n_leaves / (ms / 1e3),
+            "distinct_fingerprints": int(len(np.unique(fp))), "status_nonzero": int(np.sum(status != 0)),
+            "parity": "tests/test_gpu_fingerprint.py (reference fingerprints of 1,819 states, bit-exact)"}
+
+
 def make_batch(leaves, B: int, rotate: int):
     from paper_2410_05534_b200.arena import Batch
 
@@ -447,6 +472,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = B * world * args.e2e_steps / e2e_s
+    fp_line = measure_fingerprint(ctx, batch, meta)
     apply_line = measure_apply(ctx, leaves, B, rank * B, symarr, name_id, code, meta)
 
     if rank != 0:
@@ -499,6 +525,7 @@ def main():
                                for k in abytes},
         "schedule": "k_rebuild -> [k_extract on a side stream || k_ematch -> k_join] -> join streams",
         "apply": apply_line,
+        "fingerprint": fp_line,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": pipe.LAUNCHES_PER_STEP * K,
         "clocks": clk.summary(),

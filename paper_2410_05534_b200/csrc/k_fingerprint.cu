@@ -36,23 +36,20 @@ __device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | 
 
 struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(digest_size=8))
     uint64_t h[8];
-    uint64_t t;
-    uint32_t n;
-    uint8_t buf[128];
+    uint64_t m[16];   // message block as little-endian words
+    uint64_t t;       // bytes compressed so far
+    uint64_t acc;     // bytes of the word being filled
+    uint32_t n;       // bytes in the current block (including acc)
 
     __device__ void init() {
         for (int i = 0; i < 8; i++) h[i] = B2B_IV[i];
         h[0] ^= 0x01010008ull;
         t = 0;
         n = 0;
+        acc = 0;
     }
     __device__ void compress(bool last) {
-        uint64_t m[16], v[16];
-        for (int i = 0; i < 16; i++) {
-            uint64_t w = 0;
-            for (int b = 7; b >= 0; b--) w = (w << 8) | buf[8 * i + b];
-            m[i] = w;
-        }
+        uint64_t v[16];
         for (int i = 0; i < 8; i++) { v[i] = h[i]; v[i + 8] = B2B_IV[i]; }
         v[12] ^= t;
         if (last) v[14] = ~v[14];
@@ -77,8 +74,14 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
         for (int i = 0; i < 8; i++) h[i] ^= v[i] ^ v[i + 8];
     }
     __device__ __forceinline__ void put(uint8_t c) {
-        if (n == 128) { t += 128; compress(false); n = 0; }
-        buf[n++] = c;
+        if (n == 128) {   // a full block is compressed only once more data follows (BLAKE2b rule)
+            t += 128;
+            compress(false);
+            n = 0;
+        }
+        acc |= (uint64_t)c << (8 * (n & 7));
+        n++;
+        if ((n & 7) == 0) { m[(n >> 3) - 1] = acc; acc = 0; }
     }
     __device__ void puts(const char* s) { while (*s) put((uint8_t)*s++); }
     __device__ void putb(const uint8_t* s, uint32_t len) { for (uint32_t i = 0; i < len; i++) put(s[i]); }
@@ -91,7 +94,8 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
     // int.from_bytes(digest, "big"): the digest is h[0] little-endian
     __device__ uint64_t final() {
         t += n;
-        for (uint32_t i = n; i < 128; i++) buf[i] = 0;
+        if (n & 7) m[n >> 3] = acc;
+        for (uint32_t w = (n + 7) >> 3; w < 16; w++) m[w] = 0;
         compress(true);
         return __byte_perm((uint32_t)(h[0] >> 32), 0, 0x0123) | ((uint64_t)__byte_perm((uint32_t)h[0], 0, 0x0123) << 32);
     }
