@@ -611,7 +611,7 @@ static int ematch_launch(esat_batch* b) {
     CK(c, cudaMemsetAsync(b->d_over, 0, sizeof(uint32_t), c->stream));
     MArgs a{};
     a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = b->m_mode;
-    a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw;
+    a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw; a.nzl = b->d_raw + 32ull * (b->N + 1);
     a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
     Dev d = b->d;
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
@@ -714,7 +714,7 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
         }
         CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
         CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
-        if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 4ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts
+        if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 8ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts + work list
         if (!b->stage_cap) {
             if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
             if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;

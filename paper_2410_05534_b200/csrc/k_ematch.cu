@@ -412,8 +412,14 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     auto prog_ptr = [&](uint32_t pi) -> const int32_t* { return (progs_smem ? sprog : a.prog) + sp_off[pi]; };
     const uint32_t PC = P * C;
     uint32_t* pc = a.raw + d.nb[l] * MAXP;   // [P][C] counts -> offsets (C <= n, P <= 32)
+    uint32_t* nzl = a.nzl + d.nb[l] * MAXP;  // (pattern, class) pairs with matches (any order)
+    __shared__ uint32_t sh_nz;
+    if (tid == 0) sh_nz = 0;
+    __syncthreads();
+    uint32_t pi_i = C ? tid / C : 0, r_i = C ? tid - pi_i * C : 0;
     for (uint32_t i = tid; i < PC; i += T) {
-        const uint32_t pi = i / C, r = i - pi * C;
+        const uint32_t pi = pi_i, r = r_i;
+        for (r_i += T; r_i >= C; r_i -= C) pi_i++;   // next (pattern, class) of this thread
         uint32_t n = 0;
         const uint32_t rb = sp_rbit[pi];
         if (!rb || (cmask[r] & rb)) {
@@ -425,6 +431,7 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
             }
         }
         pc[i] = n;
+        if (n) nzl[atomicAdd(&sh_nz, 1u)] = i;
     }
     __syncthreads();
     // exclusive scan of pc in place: each warp owns a contiguous quarter and walks it 32 elements at
@@ -470,8 +477,9 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     }
     __syncthreads();
     if (sh_base != ~0ull) {
-        const uint32_t grand = sp_rbase[P];
-        for (uint32_t i = tid; i < PC; i += T) {
+        const uint32_t grand = sp_rbase[P], nz = sh_nz;
+        for (uint32_t j = tid; j < nz; j += T) {
+            const uint32_t i = nzl[j];
             const uint32_t beg = pc[i], end = (i + 1 < PC) ? pc[i + 1] : grand;
             if (beg == end) continue;
             const uint32_t pi = i / C, r = i - pi * C, W = sp_W[pi];

@@ -25,6 +25,7 @@ struct MArgs {
     uint32_t* overflow;
     uint32_t smem_bytes;        // dynamic shared memory for staging one leaf's view
     uint32_t* raw;              // [L][32][T] per-thread raw match counts (count -> fill placement)
+    uint32_t* nzl;              // [L][32][C] (pattern, class) pairs with matches (pass-2 work list)
     int no_flat;                // 1: always use the generic backtracking matcher
 };
 
