@@ -677,7 +677,9 @@ __device__ uint8_t plan_slot(JoinPlan& p, uint8_t field) {
     return (uint8_t)p.F++;
 }
 
-__device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ) {
+// v1: source 1's join variable (its equality with source 0's is guaranteed by the index lookup,
+// so it needs no per-product check)
+__device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ, uint32_t v1) {
     p.W = 2 + NV + NQ;
     p.src[0] = 0; p.idx[0] = 0; p.src[1] = 1; p.idx[1] = 0;
     for (uint32_t o = 0; o < NV + NQ; o++) { p.src[2 + o] = 255; p.idx[2 + o] = 0; }
@@ -689,8 +691,11 @@ __device__ void make_plan(JoinPlan& p, const Src* s, uint32_t NV, uint32_t NQ) {
     }
     for (uint32_t v = 0; v < s[1].V; v++) {
         const uint32_t o = 2 + s[1].vmap[v];
-        if (p.src[o] == 0) { p.c0[p.nchk] = p.idx[o]; p.c1[p.nchk] = 1 + v; p.nchk++; }
-        else { p.src[o] = 1; p.idx[o] = 1 + v; }
+        if (p.src[o] == 0) {
+            if (v != v1) { p.c0[p.nchk] = p.idx[o]; p.c1[p.nchk] = 1 + v; p.nchk++; }
+        } else {
+            p.src[o] = 1; p.idx[o] = 1 + v;
+        }
     }
     for (uint32_t q = 0; q < s[1].Q; q++) {
         const uint32_t o = 2 + NV + s[1].qmap[q];
@@ -822,7 +827,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     const uint32_t* w1 = src[S > 1 ? 1 : 0].w;
     const uint32_t W0 = src[0].W, W1 = src[S > 1 ? 1 : 0].W;
     __shared__ JoinPlan sh_plan;
-    if (indexed && tid == 0) make_plan(sh_plan, src, NV, NQ);
+    if (indexed && tid == 0) make_plan(sh_plan, src, NV, NQ, v1);
     __syncthreads();
     extern __shared__ uint32_t jrun[];
     uint32_t* s1 = jrun + a.run_cap;
