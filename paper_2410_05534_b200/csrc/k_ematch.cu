@@ -868,7 +868,6 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             }
             __syncthreads();
         }
-        __shared__ uint32_t sh_m1[NW][MAX_W];
         // source-0 root-group starts as a bitmask (bit i: record i starts a group), built once
         constexpr uint32_t GB_WORDS = 1024;
         __shared__ uint32_t sh_gbits[GB_WORDS];
@@ -894,15 +893,12 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         };
         auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
             uint32_t n = 0;
-            uint32_t* m1s = sh_m1[warp];
             for (uint32_t g = wlo; g < whi;) {
                 const uint32_t ge = gend(g);
                 const uint32_t gstart = n;
                 for (uint32_t i = g; i < ge; i++) {
-                    const uint32_t* m1 = w0 + (uint64_t)i * W0;
-                    __syncwarp();
-                    if (lane < W0) m1s[lane] = m1[lane];
-                    __syncwarp();
+                    // the source-0 record is read with warp-uniform loads (one broadcast each)
+                    const uint32_t* m1s = w0 + (uint64_t)i * W0;
                     const uint32_t x = m1s[1 + v0];
                     uint32_t p0, p1;
                     if (use_run) {
