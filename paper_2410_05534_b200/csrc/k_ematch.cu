@@ -434,30 +434,52 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         if (n) nzl[atomicAdd(&sh_nz, 1u)] = i;
     }
     __syncthreads();
-    // exclusive scan of pc in place: each warp owns a contiguous quarter and walks it 32 elements at
-    // a time (coalesced) with shuffle scans; pass A sums, pass B writes prefixes
+    // exclusive scan of pc in place: each warp owns a contiguous, 128-aligned share and walks it 128
+    // elements at a time (one uint4 per lane, coalesced) with a 4-wide local prefix + shuffle scan;
+    // pass A sums, pass B writes prefixes. pc rows start 128-B aligned (leaf base x 32 words).
     {
         constexpr uint32_t NW = T / 32;
         __shared__ uint32_t sh_wsum[NW];
         const uint32_t lane = tid & 31, warp = tid >> 5;
-        const uint32_t qw = (PC + NW - 1) / NW, lo = min(PC, warp * qw), hi = min(PC, lo + qw);
+        const uint32_t qw = ((PC + NW - 1) / NW + 127) & ~127u;
+        const uint32_t lo = min(PC, warp * qw), hi = min(PC, lo + qw);
+        auto load4 = [&](uint32_t i) -> uint4 {   // elements i..i+3, zero past hi
+            if (i + 3 < hi) return reinterpret_cast<const uint4*>(pc)[i >> 2];
+            uint4 q = make_uint4(0, 0, 0, 0);
+            if (i < hi) q.x = pc[i];
+            if (i + 1 < hi) q.y = pc[i + 1];
+            if (i + 2 < hi) q.z = pc[i + 2];
+            return q;
+        };
         uint32_t sum = 0;
-        for (uint32_t i = lo + lane; i < hi; i += 32) sum += pc[i];
+        for (uint32_t i = lo + 4 * lane; i < hi; i += 128) {
+            const uint4 q = load4(i);
+            sum += q.x + q.y + q.z + q.w;
+        }
         sum = __reduce_add_sync(0xffffffffu, sum);
         if (lane == 0) sh_wsum[warp] = sum;
         __syncthreads();
         uint32_t carry = 0, total = 0;
         for (uint32_t w = 0; w < NW; w++) { if (w < warp) carry += sh_wsum[w]; total += sh_wsum[w]; }
-        for (uint32_t b0 = lo; b0 < hi; b0 += 32) {
-            const uint32_t i = b0 + lane;
-            const uint32_t v = i < hi ? pc[i] : 0u;
-            uint32_t x = v;
+        for (uint32_t b0 = lo; b0 < hi; b0 += 128) {
+            const uint32_t i = b0 + 4 * lane;
+            const uint4 q = load4(i);
+            const uint32_t s0 = q.x, s1 = s0 + q.y, s2 = s1 + q.z, s3 = s2 + q.w;
+            uint32_t x = s3;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= (uint32_t)o) x += y;
             }
-            if (i < hi) pc[i] = carry + x - v;
+            const uint32_t ex = carry + x - s3;
+            const uint4 r = make_uint4(ex, ex + s0, ex + s1, ex + s2);
+            if (i + 3 < hi) {
+                reinterpret_cast<uint4*>(pc)[i >> 2] = r;
+            } else {
+                if (i < hi) pc[i] = r.x;
+                if (i + 1 < hi) pc[i + 1] = r.y;
+                if (i + 2 < hi) pc[i + 2] = r.z;
+            }
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
         __syncthreads();
