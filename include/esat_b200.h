@@ -178,8 +178,9 @@ int esat_batch_set_counts(esat_batch* b, const uint32_t* n_cnt, const uint32_t* 
 /* apply rule leaf_rule[l] (0xFFFFFFFF: none) to every leaf, using the match lists of the last
  * esat_ematch / esat_join calls; the leaf's dirty state replaces the batch input (next: esat_rebuild) */
 int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit);
-/* status[L], report[L][4] = {matches_found, changed, cycles_filtered, shape_filtered}
- * (ApplyReport, rewrite.py:440-448), missing[L][16] = descriptor of a symbol to intern */
+/* status[L], report[L][8] = {matches_found, changed, cycles_filtered, shape_filtered (ApplyReport,
+ * rewrite.py:440-448), unions performed, e-nodes added, 0, 0}, missing[L][16] = descriptor of a
+ * symbol to intern */
 int esat_download_apply(esat_batch* b, uint32_t* status, uint32_t* report, uint32_t* missing);
 /* ---- WL fingerprint: EGraph.fingerprint (egraph.py:247-296) per rebuilt leaf ----
  * krank[s] = rank of symbol s's key (name, arity, repr(payload)) in Python tuple order,

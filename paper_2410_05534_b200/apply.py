@@ -192,13 +192,16 @@ class ApplyDriver:
     pattern and target programs (attribute codes are order-preserving, so they move), re-matches
     on the unchanged rebuilt view and re-applies -- the rebuilt state is still intact on the device."""
 
-    def __init__(self, pipe, symtab, language, cost_config=None):
+    def __init__(self, pipe, symtab, language, cost_config=None, symbol_cls=None):
         from .cost_model import CostModelConfig
-        from .tensor_ir import TensorLanguage
+        from .egraph import Symbol
 
         self.pipe, self.symtab, self.language = pipe, symtab, language
+        self.symbol_cls = symbol_cls or Symbol   # the caller's Symbol class (ours or the reference's)
         cfg = cost_config or CostModelConfig()
-        self.lang = LANG_TENSOR if isinstance(language, TensorLanguage) else LANG_TERM
+        # tensor symbols carry (attributes, shape) payloads (tensor_ir.py:243-265); duck-typed so the
+        # reference's own language objects work too
+        self.lang = LANG_TENSOR if type(language).__name__ == "TensorLanguage" else LANG_TERM
         self.cost_mode = {"term": COST_TERM, "unit": COST_UNIT, "analytic": COST_ANALYTIC}[cfg.mode]
         self.coeff = float(cfg.coefficient)
         self.interned = 0
@@ -228,8 +231,7 @@ class ApplyDriver:
         return order[i]
 
     def _intern(self, desc):
-        from .egraph import Symbol
-
+        Symbol = self.symbol_cls  # noqa: N806
         p = self._target_node(int(desc[14]), int(desc[15]) >> 8, int(desc[15]) & 0xFF)
         arity = int(desc[1])
         if self.lang == LANG_TERM:

@@ -925,7 +925,7 @@ static int ensure_apply_buffers(esat_batch* b) {
     const uint64_t N = b->N, K = b->K, U = b->U, L = b->L;
     OWN(b->d_ncnt, L); OWN(b->d_ucnt, L); OWN(b->d_ureb, L);
     b->d.u_reb = b->d_ureb;
-    OWN(b->a_rule, L); OWN(b->a_status, L); OWN(b->a_report, 4 * L); OWN(b->a_missing, 16 * L);
+    OWN(b->a_rule, L); OWN(b->a_status, L); OWN(b->a_report, 8 * L); OWN(b->a_missing, 16 * L);
     OWN(b->a_shead, U); OWN(b->a_stail, U); OWN(b->a_sseen, U); OWN(b->a_snext, N); OWN(b->a_sstack, N + K);
     return ESAT_OK;
 }
@@ -1010,7 +1010,7 @@ int esat_download_apply(esat_batch* b, uint32_t* status, uint32_t* report, uint3
     cudaStream_t s = c->stream;
     const uint64_t L = b->L;
     if (status) CK(c, cudaMemcpyAsync(status, b->a_status, 4 * L, cudaMemcpyDeviceToHost, s));
-    if (report) CK(c, cudaMemcpyAsync(report, b->a_report, 16 * L, cudaMemcpyDeviceToHost, s));
+    if (report) CK(c, cudaMemcpyAsync(report, b->a_report, 32 * L, cudaMemcpyDeviceToHost, s));
     if (missing) CK(c, cudaMemcpyAsync(missing, b->a_missing, 64 * L, cudaMemcpyDeviceToHost, s));
     CK(c, cudaStreamSynchronize(s));
     return ESAT_OK;

@@ -352,10 +352,10 @@ __device__ uint32_t add_node(Leaf& L, const Sym& s, int op, const uint32_t* k, c
     return id;
 }
 
-__device__ void union_classes(Leaf& L, uint32_t a, uint32_t b) {
+__device__ bool union_classes(Leaf& L, uint32_t a, uint32_t b) {
     const uint32_t ra = find(L, a), rb = find(L, b);
     __syncwarp();
-    if (ra == rb) return;
+    if (ra == rb) return false;
     if (L.lane == 0) {
         const uint32_t win = uf_union(L.parent, L.rank, ra, rb), lose = win == ra ? rb : ra;
         if (L.head[lose] != NONE) {
@@ -366,6 +366,7 @@ __device__ void union_classes(Leaf& L, uint32_t a, uint32_t b) {
     }
     __syncwarp();
     L.changed = true;
+    return true;
 }
 
 }  // namespace
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     const uint32_t l = blockIdx.x, lane = threadIdx.x;
     if (l >= d.L) return;
     const uint32_t rule = a.leaf_rule[l];
-    uint32_t* rep = a.report + 4 * (uint64_t)l;
+    uint32_t* rep = a.report + 8 * (uint64_t)l;
     const uint64_t b = d.nb[l], k0 = d.kb[l], u0 = d.ub[l], t0 = d.tb[l];
     Leaf L;
     L.d = &d; L.a = &a; L.l = l;
@@ -429,6 +430,8 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     __shared__ uint32_t sh_qtail;
     L.lane = lane;
     uint32_t st = A_OK, found = 0, cyc = 0, shp = 0;
+    const uint32_t n_before = L.n;
+    uint32_t unions = 0;
     if (rule != NONE && a.node_limit && L.n >= a.node_limit) st = A_NODE_LIMIT;   // rewrite.py:532-537
     if (rule != NONE && st == A_OK) {
         const int32_t* rp = a.prog + a.rule_off[rule];
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                     }
                 }
                 if (err != A_OK) { st = err; break; }
-                union_classes(L, inst[top], matched);
+                if (union_classes(L, inst[top], matched)) unions++;
             }
         }
     }
@@ -545,6 +548,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     d.u_cnt[l] = L.U;
     a.status[l] = st;
     rep[0] = found; rep[1] = L.changed ? 1u : 0u; rep[2] = cyc; rep[3] = shp;
+    rep[4] = unions; rep[5] = L.n - n_before; rep[6] = 0; rep[7] = 0;
 }
 
 }  // namespace esat

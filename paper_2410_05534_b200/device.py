@@ -86,6 +86,12 @@ def _upload(eg, costs=None):
 def rebuild(eg) -> int:
     """EGraph.rebuild on the device; the host structure is replaced by the device result."""
     b, packed = _upload(eg)
+    return _write_back(eg, b, packed)
+
+
+def _write_back(eg, b, packed, version_bump: int = 0) -> int:
+    """Replace the host structure by batch b's rebuilt leaf 0 (hashcons in the reference's
+    order, union-find, classes in ascending id); returns the rebuild's merge count."""
     out = b.download_rebuild()
     view = b.download_view()
     merges = int(out["merges"][0])
@@ -98,8 +104,9 @@ def rebuild(eg) -> int:
     cid = out["hc_cid"][:n]
     nodes = [ENodeT(st.symbols[int(sym[i])], tuple(int(k) for k in kids[koff[i]:koff[i + 1]])) for i in range(n)]
     eg.hashcons = {nodes[i]: int(cid[i]) for i in range(n)}
-    eg._uf.parent = [int(x) for x in out["uf_parent"]]
-    eg._uf.rank = [int(x) for x in out["uf_rank"]]
+    U = int(b.download_state()["U"][0]) if "u_cnt" in packed else len(out["uf_parent"])
+    eg._uf.parent = [int(x) for x in out["uf_parent"][:U]]
+    eg._uf.rank = [int(x) for x in out["uf_rank"][:U]]
     groups = defaultdict(set)
     parents = defaultdict(set)
     for node, c in eg.hashcons.items():
@@ -112,7 +119,7 @@ def rebuild(eg) -> int:
     order = [int(c) for c in view["cls_id"][: int(view["C"][0])]]
     eg.classes = {c: EClassT(c, groups[c], parents.get(c, set())) for c in order}
     eg.dirty.clear()
-    eg._version += merges
+    eg._version += merges + version_bump
     eg._esat_resident = _Resident(eg._version, b, view, packed)
     return merges
 
@@ -183,3 +190,55 @@ def extract(eg, costs: dict, method: str):
         kids = tuple(int(cls_id[p]) for p in v["nd_kpos"][nko[j]:nko[j + 1]])
         chosen[int(cls_id[k])] = ENodeT(symt.symbols[int(v["nd_sym"][j])], kids)
     return st, NONE, float(out["root_cost"][0]), chosen
+
+
+def apply_rule(eg, rule, node_limit: int = 0, language=None):
+    """apply_rule (rewrite.py:526-570) on the device: k_ematch/k_join for the rule's sources,
+    k_apply for the instantiations and unions, k_rebuild; the rebuilt result is written back into
+    the host e-graph. New operator symbols are interned on the host (apply.ApplyDriver)."""
+    from .apply import ApplyDriver
+    from .cost_model import CostModelConfig
+    from .egraph import StructuralError
+    from .pipeline import LeafPipeline
+    from .rewrite import ApplyReport
+    from .tensor_ir import TermLanguage
+
+    lang = language or eg.language or TermLanguage()
+    if node_limit:
+        n = eg.size()[0]
+        if n >= node_limit:
+            raise StructuralError(f"node limit {node_limit} not above current node count {n}")
+    if eg.dirty:
+        raise StructuralError("ematch requires a rebuilt e-graph")
+    s = session()
+    leaf = export_state(eg, s.symtab)
+    s.sync_symtab()
+    head = max(256, 2 * leaf.n)
+    while True:
+        packed = Batch([leaf]).pack_with_headroom(nodes=head, kids=2 * head, ids=head)
+        pipe = LeafPipeline(s.ctx, s.symtab.arrays(), [rule], lambda nm: s.symtab.name_id(nm, create=False),
+                            s.symtab.code)
+        b = pipe.load(packed)
+        b.set_counts(packed["n_cnt"], packed["u_cnt"])
+        pipe.rebuild()
+        drv = ApplyDriver(pipe, s.symtab, lang, CostModelConfig(mode="term"), symbol_cls=_node_class(eg)[1])
+        pipe.ematch()
+        res = drv.apply(np.zeros(1, np.uint32))
+        st = int(res["status"][0])
+        if st != native.A_CAPACITY:
+            break
+        head *= 4
+    s._uploaded = -1   # the driver re-uploaded the (possibly grown) table
+    s.sync_symtab()
+    if st != native.A_OK:
+        raise RuntimeError(f"device apply failed with status {st}")
+    found, changed, cyc, shp, unions, adds = (int(x) for x in res["report"][0][:6])
+    rep = ApplyReport(rule_id=rule.id)
+    rep.matches_found, rep.cycles_filtered, rep.shape_filtered = found, cyc, shp
+    before = eg._version
+    pipe.rebuild()
+    _write_back(eg, b, packed, version_bump=adds + unions)
+    rep.changed = eg._version != before
+    rep.nodes_after, rep.classes_after = eg.size()
+    rep.hit_node_limit = bool(node_limit) and rep.nodes_after >= node_limit
+    return rep

@@ -227,7 +227,7 @@ class DeviceBatch:
 
     def download_apply(self) -> dict:
         L = self.n_leaves
-        st, rep, miss = np.zeros(L, np.uint32), np.zeros((L, 4), np.uint32), np.zeros((L, 16), np.uint32)
+        st, rep, miss = np.zeros(L, np.uint32), np.zeros((L, 8), np.uint32), np.zeros((L, 16), np.uint32)
         self.ctx.check(self.L.esat_download_apply(self.h, _p(st), _p(rep), _p(miss)))
         return {"status": st, "report": rep, "missing": miss}
 

@@ -136,44 +136,14 @@ def _instantiate(eg, lang, pat, sub) -> int:
 
 
 def apply_rule(egraph: EGraph, rule: Rule, node_limit: int = 0, language=None) -> ApplyReport:
-    """Apply every match of `rule`, union targets with matched classes, rebuild (rewrite.py:526-573)."""
-    lang = _lang(egraph, language)
-    if node_limit:
-        n = egraph.size()[0]
-        if n >= node_limit:
-            raise StructuralError(f"node limit {node_limit} not above current node count {n}")
-    rep = ApplyReport(rule_id=rule.id)
-    subs = joint_match(egraph, rule.sources, lang)
-    rep.matches_found = len(subs)
-    before = egraph.version
-    for sub in subs:
-        for k, tgt in enumerate(rule.targets):
-            root = egraph.find(sub.roots[k])
-            try:
-                refs, existing = _refs(egraph, lang, tgt, sub)
-            except InstantiationError:
-                rep.shape_filtered += 1
-                continue
-            if existing is not None and existing == root:
-                continue
-            if would_create_cycle(egraph, refs, root):
-                rep.cycles_filtered += 1
-                continue
-            try:
-                shape = _shape(egraph, lang, tgt, sub)
-            except InstantiationError:
-                rep.shape_filtered += 1
-                continue
-            have = lang.class_shape(egraph, root)
-            if shape is not None and have is not None and shape != have:
-                rep.shape_filtered += 1
-                continue
-            egraph.union(_instantiate(egraph, lang, tgt, sub), root)
-    egraph.rebuild()
-    rep.changed = egraph.version != before
-    rep.nodes_after, rep.classes_after = egraph.size()
-    rep.hit_node_limit = bool(node_limit) and rep.nodes_after >= node_limit
-    return rep
+    """Apply every match of `rule`, union targets with matched classes, rebuild (rewrite.py:526-573).
+
+    Runs on the device (device.apply_rule: k_ematch/k_join -> k_apply -> k_rebuild); the
+    helpers above (_refs, would_create_cycle, _shape, _instantiate) are the host restatement of
+    the same steps, kept as the reference's public helpers."""
+    from . import device
+
+    return device.apply_rule(egraph, rule, node_limit, _lang(egraph, language))
 
 
 def is_saturated(egraph: EGraph, rules: list, node_limit: int = 0, language=None) -> bool:
