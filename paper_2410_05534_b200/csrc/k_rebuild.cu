@@ -234,14 +234,36 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d) {
     const uint32_t C = base_c;
     if (tid == 0) cls_off[C] = n;
     __syncthreads();
-    for (uint32_t j = tid; j < n; j += T) perm[atomicAdd(&coff_of[ocid[j]], 1u)] = j;
+    // node_sort_key as a packed key per entry: hi = rank << 32 | (child0 + 1), lo = child1 + 1
+    // (0 = absent, so shorter prefixes sort first); more than two children -> the full comparator
+    constexpr uint32_t WIDE = 0xFFFFFFFFu;
+    uint32_t *key_r = d.s_ksym + b, *key_c0 = d.s_cval + b, *key_c1 = d.s_val + b;
+    for (uint32_t j = tid; j < n; j += T) {
+        perm[atomicAdd(&coff_of[ocid[j]], 1u)] = j;
+        const uint32_t q = okoff[j], a = okoff[j + 1] - q;
+        key_r[j] = d.sym_rank[osym[j]];
+        key_c0[j] = a > 0 ? okids[q] + 1 : 0u;
+        key_c1[j] = a > 2 ? WIDE : (a > 1 ? okids[q + 1] + 1 : 0u);
+    }
     __syncthreads();
     for (uint32_t k = tid; k < C; k += T) {  // per-class insertion sort (classes are small)
         const uint32_t lo = cls_off[k], hi = cls_off[k + 1];
         for (uint32_t i = lo + 1; i < hi; i++) {
             const uint32_t v = perm[i];
+            const unsigned long long hv = ((unsigned long long)key_r[v] << 32) | key_c0[v];
+            const uint32_t lv = key_c1[v];
             uint32_t j = i;
-            while (j > lo && node_less(d.sym_rank, osym, okoff, okids, v, perm[j - 1])) { perm[j] = perm[j - 1]; j--; }
+            while (j > lo) {
+                const uint32_t u = perm[j - 1];
+                const unsigned long long hu = ((unsigned long long)key_r[u] << 32) | key_c0[u];
+                bool lt;
+                if (hv != hu) lt = hv < hu;
+                else if (lv == WIDE || key_c1[u] == WIDE) lt = node_less(d.sym_rank, osym, okoff, okids, v, u);
+                else lt = lv < key_c1[u];
+                if (!lt) break;
+                perm[j] = u;
+                j--;
+            }
             perm[j] = v;
         }
     }
