@@ -301,7 +301,6 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
     OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N);
-    OWN(x.need, N); OWN(x.lnode, N); OWN(x.lcls, N); OWN(x.lvn, NL); OWN(x.nval, N); OWN(x.naux, 2 * N);
     x.slot_stride = N;
     *out = b;
     return ESAT_OK;
@@ -417,7 +416,6 @@ static int launch_extract(esat_batch* b, int method, cudaStream_t s) {
         x.pool_kbase = b->d_pbk;
         x.pool_key = b->pool_key;
         x.pool_val = b->pool_val;
-        x.pool_stride = 0;   // one cumulative region per leaf
     }
     static const int xt = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 32;
     if (b->L) {

@@ -62,13 +62,8 @@ struct XArgs {
     const uint64_t* pool_kbase;
     uint32_t *pool_key;
     double* pool_val;
-    uint64_t pool_stride;        // unused (0)
     uint32_t *hoff, *hrng;               // [2][node rows] history block offset / occupied range per class position (pass parity)
     uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip)
-    uint8_t* need;               // [node rows] class needs re-evaluation in the current pass
-    uint32_t *lnode, *lcls, *lvn; // e-nodes in level order, their classes, level ends (node-parallel phase)
-    double* nval;                // [node rows] node cost of the current pass
-    uint32_t* naux;              // [2][node rows] generic-arity node history (offset, length)
     uint64_t slot_stride;
 };
 
