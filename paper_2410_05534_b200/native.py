@@ -114,9 +114,13 @@ class Context:
     def close(self):
         if self.h:
             self.L.esat_ctx_destroy(self.h)
-            self.h = C.c_void_p()
+            self.h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter teardown: module globals may already be gone
+            pass
 
     def sync(self):
         self.check(self.L.esat_ctx_sync(self.h))
@@ -184,9 +188,13 @@ class DeviceBatch:
     def close(self):
         if self.h:
             self.L.esat_batch_destroy(self.h)
-            self.h = C.c_void_p()
+            self.h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter teardown: module globals may already be gone
+            pass
 
     @property
     def N(self):
