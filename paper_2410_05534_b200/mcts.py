@@ -252,10 +252,10 @@ def optimize_mcts(egraph, rules, cfg: MctsConfig, cost_config, symtab=None, engi
     from .arena import export_state
     from .symtab import SymbolTable
 
-    symtab = symtab or SymbolTable()
+    symtab = SymbolTable() if symtab is None else symtab
     language = egraph.language
     state = export_state(egraph, symtab, cost_config)
-    engine = engine or DeviceEngine(rules, symtab, language, cost_config, method=cfg.main_extractor,
+    engine = engine if engine is not None else DeviceEngine(rules, symtab, language, cost_config, method=cfg.main_extractor,
                                     headroom=cfg.headroom)
     rng = random.Random(cfg.seed)
     (state,), cost, n, app = engine.evaluate([state])

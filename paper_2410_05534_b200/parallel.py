@@ -41,3 +41,36 @@ def rewards(prev_cost, new_cost):
     import torch
 
     return torch.clamp(prev_cost - new_cost, min=0.0)
+
+
+def root_parallel_sweep(run_seed, seeds, group=None):
+    """Root-parallel MCTS sweep (BASELINE config 5: 64 seeds sharded over 8 GPUs).
+
+    Rank r runs ``run_seed(seed) -> (final_cost, trace)`` for its contiguous share of ``seeds``;
+    the per-seed results ``(seed, final cost, trace hash)`` are all-gathered (NCCL over NVLink, gloo
+    in the CPU tests) so every rank holds the whole sweep in seed order and the same best seed."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    s, e = leaf_shard(len(seeds), world, rank)
+    per = -(-len(seeds) // world)   # padded share so every rank contributes equal-size tensors
+    rows = torch.full((per, 3), -1.0, dtype=torch.float64)
+    for i, seed in enumerate(seeds[s:e]):
+        cost, trace = run_seed(seed)
+        h = int.from_bytes(hashlib.blake2b(repr(list(trace)).encode(), digest_size=6).digest(), "big")
+        rows[i] = torch.tensor([float(seed), float(cost), float(h)], dtype=torch.float64)
+    if world > 1:
+        backend = dist.get_backend(group)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+        src = rows.to(dev)
+        out = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(out, src, group=group)
+        rows = torch.cat([o.cpu() for o in out])
+    res = [(int(r[0]), float(r[1]), int(r[2])) for r in rows.tolist() if r[0] >= 0]
+    res.sort()
+    best = min(res, key=lambda t: (t[1], t[0])) if res else None
+    return res, best

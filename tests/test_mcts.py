@@ -62,3 +62,28 @@ def test_analog_mcts_deterministic_and_improves():
     assert runs[0] == runs[1]
     initial, final, trace = runs[0]
     assert trace and final <= initial, runs[0]
+
+
+@pytest.mark.gpu
+def test_seed_sweep_single_rank():
+    """Config 5 structure on one GPU: the sweep's rows equal direct optimize_mcts runs per seed."""
+    from paper_2410_05534_b200 import analogs
+    from paper_2410_05534_b200 import tensor_ir as T
+    from paper_2410_05534_b200.cost_model import CostModelConfig
+    from paper_2410_05534_b200.mcts import MctsConfig, optimize_mcts
+    from paper_2410_05534_b200.parallel import root_parallel_sweep
+    from paper_2410_05534_b200.patterns import load_rules
+
+    rules = load_rules("taso_analog")
+
+    def run(seed):
+        eg = T.graph_to_egraph(analogs.build_analog("nasnet_a", T.GraphBuilder))
+        cfg = MctsConfig(budget=16, node_limit=2000, seed=seed, batch=8, max_sim_steps=3)
+        _, final, trace = optimize_mcts(eg, rules, cfg, CostModelConfig())
+        return final, trace
+
+    res, best = root_parallel_sweep(run, [0, 1])
+    direct = [run(0), run(1)]
+    assert all(d[1] for d in direct)   # the searches applied rules
+    assert [r[1] for r in res] == [d[0] for d in direct]
+    assert best[1] == min(d[0] for d in direct)

@@ -51,3 +51,35 @@ def test_allgather_matches_single_rank(world):
         assert p.exitcode == 0
     assert np.array_equal(c, costs) and np.array_equal(st, status)
     assert np.allclose(r, 1.0)
+
+
+def _sweep_worker(rank, world, port, seeds, q):
+    from paper_2410_05534_b200.parallel import root_parallel_sweep
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # stand-in for optimize_mcts: deterministic per seed
+    res, best = root_parallel_sweep(lambda s: (float((s * 37) % 11), [s % 5, s % 3]), seeds)
+    q.put((rank, res, best))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_root_parallel_sweep_matches_single_rank():
+    """Config 5's 64-seed sweep sharded over 2 ranks equals the single-rank sweep on every rank."""
+    from paper_2410_05534_b200.parallel import root_parallel_sweep
+
+    seeds = list(range(64))
+    single, best1 = root_parallel_sweep(lambda s: (float((s * 37) % 11), [s % 5, s % 3]), seeds)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29611
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, seeds, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, res, best in outs:
+        assert res == single and best == best1, rank
+    assert len(single) == 64 and best1[1] == 0.0
