@@ -107,6 +107,8 @@ struct esat_batch {
     uint64_t *d_m_off = nullptr, *d_j_off = nullptr;
     uint32_t *stage = nullptr, *m_out = nullptr, *j_out = nullptr, *d_over = nullptr;
     uint64_t stage_cap = 0, m_cap = 0, j_cap = 0;
+    unsigned long long* j_gkeys = nullptr;   // join index scratch for long source-1 lists
+    uint64_t j_gkey_cap = 0;
     unsigned long long* d_tops = nullptr;   // [0] stage, [1] ematch out, [2] join stage, [3] join out
     uint32_t* d_jspec = nullptr;
     uint64_t jspec_cap = 0;
@@ -313,7 +315,7 @@ int esat_batch_destroy(esat_batch* b) {
     cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
-    cudaFree(b->d_over); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
+    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
     delete b;
     return ESAT_OK;
 }
@@ -757,6 +759,7 @@ static int join_launch(esat_batch* b) {
     a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
     a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
     a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
+    a.gkeys = b->j_gkeys; a.gkey_cap = b->j_gkey_cap;
     // run table in dynamic SMEM: one u32 per class id of the largest leaf (capped)
     uint64_t umax = 0;
     for (uint64_t l = 0; l < L; l++) umax = b->ub[l + 1] - b->ub[l] > umax ? b->ub[l + 1] - b->ub[l] : umax;
@@ -788,6 +791,7 @@ static int join_settle(esat_batch* b) {
         CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 16, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
         if (!over) { b->j_verified = true; b->j_pending = false; return ESAT_OK; }
+        if ((over & 4) && (r = regrow(c, &b->j_gkeys, &b->j_gkey_cap, tops[0]))) return r;
         if ((r = regrow(c, &b->j_out, &b->j_cap, tops[1]))) return r;
         if ((r = join_launch(b))) return r;
     }

@@ -835,15 +835,33 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         for (uint32_t b = 0; b < src[1].V && v0 == NONE; b++)
             for (uint32_t a0 = 0; a0 < src[0].V; a0++)
                 if (src[0].vmap[a0] == src[1].vmap[b]) { v0 = a0; v1 = b; break; }
-    const bool indexed = v0 != NONE && src[1].n <= JOIN_SMEM_KEYS;
+    // source 1 sorted by (join value, record): in SMEM, or for long lists (e-graph explosion) in a
+    // global scratch region bump-allocated per CTA (overflow -> the host regrows and relaunches)
+    __shared__ unsigned long long sh_koff;
+    const bool big = v0 != NONE && src[1].n > JOIN_SMEM_KEYS;
     uint32_t n1p = 0;
-    if (indexed) {
+    if (v0 != NONE) {
         n1p = 1;
         while (n1p < src[1].n) n1p <<= 1;
+    }
+    if (big && tid == 0) {
+        unsigned long long o = atomicAdd(&a.tops[0], (unsigned long long)n1p);
+        if (o + n1p > a.gkey_cap) { atomicOr(a.overflow, 4u); o = ~0ull; }
+        sh_koff = o;
+    }
+    __syncthreads();
+    if (big && sh_koff == ~0ull) {   // no index scratch yet: the relaunch after regrowth does the work
+        if (tid == 0) { a.count[(uint64_t)r * L + l] = 0; a.off[(uint64_t)r * L + l] = 0; }
+        return;
+    }
+    unsigned long long* keys = big ? a.gkeys + sh_koff : sh_keys;
+    const bool indexed = v0 != NONE;
+    if (indexed) {
         for (uint32_t i = tid; i < n1p; i += T)
-            sh_keys[i] = i < src[1].n ? ((unsigned long long)src[1].w[(uint64_t)i * src[1].W + 1 + v1] << 32) | i
-                                      : ~0ull;
-        block_bitonic(sh_keys, n1p);
+            keys[i] = i < src[1].n ? ((unsigned long long)src[1].w[(uint64_t)i * src[1].W + 1 + v1] << 32) | i
+                                   : ~0ull;
+        __syncthreads();
+        block_bitonic(keys, n1p);
     }
     const uint32_t* w0 = src[0].w;
     const uint32_t* w1 = src[S > 1 ? 1 : 0].w;
@@ -858,7 +876,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         const uint32_t F = sh_plan.F, W1s = src[1].W;
         for (uint32_t e = tid; e < src[1].n * F; e += T) {
             const uint32_t p = e / F, f = e - p * F;
-            s1[e] = src[1].w[(uint64_t)(uint32_t)sh_keys[p] * W1s + sh_plan.f1[f]];
+            s1[e] = src[1].w[(uint64_t)(uint32_t)keys[p] * W1s + sh_plan.f1[f]];
         }
         __syncthreads();
     }
@@ -881,10 +899,10 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             for (uint32_t x = tid; x < U; x += T) jrun[x] = 0;
             __syncthreads();
             for (uint32_t q = tid; q < n1; q += T) {
-                const uint32_t x = (uint32_t)(sh_keys[q] >> 32);
-                if (q == 0 || (uint32_t)(sh_keys[q - 1] >> 32) != x) {
+                const uint32_t x = (uint32_t)(keys[q] >> 32);
+                if (q == 0 || (uint32_t)(keys[q - 1] >> 32) != x) {
                     uint32_t e = q + 1;
-                    while (e < n1 && (uint32_t)(sh_keys[e] >> 32) == x) e++;
+                    while (e < n1 && (uint32_t)(keys[e] >> 32) == x) e++;
                     jrun[x] = q | ((e - q) << 16);
                 }
             }
@@ -928,8 +946,8 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                         p0 = rr & 0xFFFFu;
                         p1 = p0 + (rr >> 16);
                     } else {
-                        p0 = lower_bound_key(sh_keys, n1, (unsigned long long)x << 32);
-                        p1 = lower_bound_key(sh_keys, n1, ((unsigned long long)x + 1ull) << 32);
+                        p0 = lower_bound_key(keys, n1, (unsigned long long)x << 32);
+                        p1 = lower_bound_key(keys, n1, ((unsigned long long)x + 1ull) << 32);
                     }
                     if (!out && jp.nchk == 0) { n += p1 - p0; continue; }   // every product is consistent
                     if (staged) {
@@ -943,7 +961,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                     for (uint32_t base = p0; base < p1; base += 32) {
                         const uint32_t p = base + lane;
                         bool ok = p < p1;
-                        const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)sh_keys[p] * W1 : w1;
+                        const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)keys[p] * W1 : w1;
                         for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.c1[c]];
                         const uint32_t mask = __ballot_sync(0xffffffffu, ok);
                         if (out && ok) {

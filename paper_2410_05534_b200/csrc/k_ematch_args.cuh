@@ -48,6 +48,8 @@ struct JArgs {
     const uint64_t* id_base;    // per-leaf id bases (run-table size)
     uint32_t run_cap;           // dynamic SMEM run-table entries
     uint32_t s1_cap;            // dynamic SMEM words for the staged source-1 fields (after the run table)
+    unsigned long long* gkeys;  // global index scratch for source-1 lists beyond the SMEM index
+    uint64_t gkey_cap;          //   (bump-allocated through tops[0]; overflow bit 4 -> regrow)
 };
 
 constexpr uint32_t JOIN_SMEM_S1 = 4096;   // SMEM words for staged source-1 join fields
