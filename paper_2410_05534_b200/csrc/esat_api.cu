@@ -109,6 +109,8 @@ struct esat_batch {
     uint64_t stage_cap = 0, m_cap = 0, j_cap = 0;
     unsigned long long* j_gkeys = nullptr;   // join index scratch for long source-1 lists
     uint64_t j_gkey_cap = 0;
+    uint32_t* j_gsort = nullptr;             // join root-group merge scratch
+    uint64_t j_gsort_cap = 0;
     unsigned long long* d_tops = nullptr;   // [0] stage, [1] ematch out, [2] join stage, [3] join out
     uint32_t* d_jspec = nullptr;
     uint64_t jspec_cap = 0;
@@ -315,7 +317,7 @@ int esat_batch_destroy(esat_batch* b) {
     cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
-    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
+    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->j_gsort); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
     delete b;
     return ESAT_OK;
 }
@@ -759,6 +761,12 @@ static int join_launch(esat_batch* b) {
     a.m_count = b->d_m_count; a.m_off = b->d_m_off; a.m_words = b->m_out; a.m_W = b->d_m_W;
     a.stage = nullptr; a.stage_cap = 0; a.tops = b->d_tops + 2;
     a.out = b->j_out; a.out_cap = b->j_cap; a.count = b->d_j_count; a.off = b->d_j_off; a.overflow = b->d_over + 1;
+    {
+        const uint64_t need = (uint64_t)R * L * (128 / 32) * JOIN_GSORT_WORDS;
+        int rr = regrow(c, &b->j_gsort, &b->j_gsort_cap, need);
+        if (rr) return rr;
+    }
+    a.gsort = b->j_gsort;
     a.gkeys = b->j_gkeys; a.gkey_cap = b->j_gkey_cap;
     // run table in dynamic SMEM: one u32 per class id of the largest leaf (capped)
     uint64_t umax = 0;

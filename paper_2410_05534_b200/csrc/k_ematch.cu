@@ -931,12 +931,42 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             }
             return n0;
         };
+        // a root group of several source-0 records yields one sorted run of products per record;
+        // the runs are merged warp-parallel: each record's final rank = its index in its run +
+        // (records below it in every other run, by binary search), scattered through SMEM
+        constexpr uint32_t GS_RUNS = 32;
+        __shared__ uint32_t sh_runs[NW][GS_RUNS + 1];
+        auto merge_group = [&](uint32_t* gout, uint32_t k, uint32_t cnt) {
+            uint32_t* runs = sh_runs[warp];
+            uint32_t* tmp = a.gsort + (((uint64_t)r * L + l) * NW + warp) * JOIN_GSORT_WORDS;   // per-warp scratch
+            for (uint32_t e = lane; e < cnt; e += 32) {
+                uint32_t a = 0;
+                while (a + 1 < k && runs[a + 1] <= e) a++;
+                const uint32_t* rec = gout + (uint64_t)e * W;
+                uint32_t rank = e - runs[a];
+                for (uint32_t bb = 0; bb < k; bb++) {
+                    if (bb == a) continue;
+                    uint32_t lo = runs[bb], hi = runs[bb + 1];   // first record of run bb not below rec
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (cmpw(gout + (uint64_t)mid * W, rec, W) < 0) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    rank += lo - runs[bb];
+                }
+                for (uint32_t w = 0; w < W; w++) tmp[rank * W + w] = rec[w];
+            }
+            __syncwarp();
+            for (uint32_t q = lane; q < cnt * W; q += 32) gout[q] = tmp[q];
+            __syncwarp();
+        };
         auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
             uint32_t n = 0;
             for (uint32_t g = wlo; g < whi;) {
                 const uint32_t ge = gend(g);
                 const uint32_t gstart = n;
                 for (uint32_t i = g; i < ge; i++) {
+                    if (out && i - g < GS_RUNS && lane == 0) sh_runs[warp][i - g] = n - gstart;
                     // the source-0 record is read with warp-uniform loads (one broadcast each)
                     const uint32_t* m1s = w0 + (uint64_t)i * W0;
                     const uint32_t x = m1s[1 + v0];
@@ -971,10 +1001,17 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                         n += __popc(mask);
                     }
                 }
-                if (out && ge - g > 1) {   // several source-0 records share the root: sort the group
+                if (out && ge - g > 1) {   // several source-0 records share the root: order the group
                     __syncwarp();
-                    if (lane == 0) sort_unique(out + (uint64_t)gstart * W, n - gstart, W);
-                    __syncwarp();
+                    const uint32_t k = ge - g, cnt = n - gstart;
+                    if (k <= GS_RUNS && cnt * W <= JOIN_GSORT_WORDS) {
+                        if (lane == 0) sh_runs[warp][k] = cnt;
+                        __syncwarp();
+                        merge_group(out + (uint64_t)gstart * W, k, cnt);
+                    } else {
+                        if (lane == 0) sort_unique(out + (uint64_t)gstart * W, cnt, W);
+                        __syncwarp();
+                    }
                 }
                 g = ge;
             }

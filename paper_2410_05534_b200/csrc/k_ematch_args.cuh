@@ -48,11 +48,13 @@ struct JArgs {
     const uint64_t* id_base;    // per-leaf id bases (run-table size)
     uint32_t run_cap;           // dynamic SMEM run-table entries
     uint32_t s1_cap;            // dynamic SMEM words for the staged source-1 fields (after the run table)
+    uint32_t* gsort;            // [R][L][warps][JOIN_GSORT_WORDS] root-group merge scratch
     unsigned long long* gkeys;  // global index scratch for source-1 lists beyond the SMEM index
     uint64_t gkey_cap;          //   (bump-allocated through tops[0]; overflow bit 4 -> regrow)
 };
 
 constexpr uint32_t JOIN_SMEM_S1 = 4096;   // SMEM words for staged source-1 join fields
+constexpr uint32_t JOIN_GSORT_WORDS = 1024; // per-warp words for merging a root group's product runs
 
 template <int T> __global__ void k_ematch(Dev, MArgs);
 template <int T> __global__ void k_join(uint32_t, JArgs);

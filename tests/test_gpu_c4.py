@@ -47,9 +47,12 @@ def test_c4_full_size_vs_oracle(c4):
     dev.update(b.download_view())
     ref = O.rebuild(packed, symarr["rank"])
     assert int(ref["n"][0]) == 80257
-    for k in ("n", "merges", "C", "root_pos", "hc_sym", "hc_koff", "hc_kids", "hc_cid", "cls_id", "cls_off", "nd_sym",
-              "nd_koff", "nd_kpos", "nd_hc"):
+    C = int(ref["C"][0])
+    for k in ("n", "merges", "C", "root_pos", "hc_sym", "hc_koff", "hc_kids", "hc_cid", "nd_sym", "nd_koff", "nd_kpos",
+              "nd_hc"):
         assert np.array_equal(dev[k], ref[k]), k
+    assert np.array_equal(dev["cls_id"][:C], ref["cls_id"][:C]) and np.array_equal(dev["cls_off"][:C + 1],
+                                                                                  ref["cls_off"][:C + 1])
     for method in ("default", "ocf"):
         e = native.extract_with_retry(b, method, factor=32)
         r = O.extract(packed, ref, method)
