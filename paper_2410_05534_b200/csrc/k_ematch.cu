@@ -236,10 +236,34 @@ __device__ __forceinline__ int cmpw(const uint32_t* a, const uint32_t* b, uint32
     return 0;
 }
 
-// insertion sort + unique of n records of W words in place; returns unique count
+__device__ __forceinline__ void swapw(uint32_t* a, uint32_t* b, uint32_t W) {
+    for (uint32_t w = 0; w < W; w++) { const uint32_t t = a[w]; a[w] = b[w]; b[w] = t; }
+}
+
+// in-place heapsort of n records of W words (the long slices: O(n log n) instead of insertion's n^2)
+__device__ void heap_sort_records(uint32_t* base, uint32_t n, uint32_t W) {
+    auto sift = [&](uint32_t root, uint32_t end) {
+        while (true) {
+            uint32_t c = 2 * root + 1;
+            if (c >= end) return;
+            if (c + 1 < end && cmpw(base + (uint64_t)c * W, base + (uint64_t)(c + 1) * W, W) < 0) c++;
+            if (cmpw(base + (uint64_t)root * W, base + (uint64_t)c * W, W) >= 0) return;
+            swapw(base + (uint64_t)root * W, base + (uint64_t)c * W, W);
+            root = c;
+        }
+    };
+    for (uint32_t i = n / 2; i-- > 0;) sift(i, n);
+    for (uint32_t end = n; end-- > 1;) {
+        swapw(base, base + (uint64_t)end * W, W);
+        sift(0, end);
+    }
+}
+
+// sort + unique of n records of W words in place; returns unique count
 __device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
     uint32_t tmp[MAX_W];
-    for (uint32_t i = 1; i < n; i++) {
+    if (n > 32) heap_sort_records(base, n, W);
+    else for (uint32_t i = 1; i < n; i++) {
         for (uint32_t w = 0; w < W; w++) tmp[w] = base[i * W + w];
         uint32_t j = i;
         while (j > 0 && cmpw(base + (j - 1) * W, tmp, W) > 0) {
@@ -538,24 +562,39 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         }
     }
     __syncthreads();
+    // squeeze out the gaps deduplicated slices left (records whose root word is NONE), block-wide
+    // and in order: chunks of T records are read, ranked by a block scan and written back; a
+    // record only ever moves left, never into the unread part of the list
+    __shared__ uint32_t sp_final[MAXP];
+    if (tid < P) sp_final[tid] = sp_rbase[tid + 1] - sp_rbase[tid];
+    __syncthreads();
+    if (sh_base != ~0ull)
+        for (uint32_t pi = 0; pi < P; pi++) {
+            if (!sp_dup[pi]) continue;
+            const uint32_t W = sp_W[pi], tot = sp_final[pi];
+            uint32_t* base = a.out + sp_wbase[pi];
+            uint32_t o = 0;
+            for (uint32_t c0 = 0; c0 < tot; c0 += T) {
+                const uint32_t rr = c0 + tid;
+                uint32_t rec[MAX_W];
+                const bool keep = rr < tot && base[(uint64_t)rr * W] != NONE;
+                if (keep)
+                    for (uint32_t w = 0; w < W; w++) rec[w] = base[(uint64_t)rr * W + w];
+                uint32_t kt;
+                const uint32_t pos = block_exscan(keep ? 1u : 0u, sh_scan, &kt);
+                __syncthreads();
+                if (keep)
+                    for (uint32_t w = 0; w < W; w++) base[(uint64_t)(o + pos) * W + w] = rec[w];
+                o += kt;
+                __syncthreads();
+            }
+            if (tid == 0) sp_final[pi] = o;
+            __syncthreads();
+        }
     if (tid < P) {
         const uint32_t pi = tid;
         const uint64_t oi = (uint64_t)pi * L + l;
-        uint32_t tot = sp_rbase[pi + 1] - sp_rbase[pi];
-        if (sh_base != ~0ull && sp_dup[pi]) {
-            // rare: squeeze out the gaps left by deduplicated slices (left-to-right, in order)
-            const uint32_t W = sp_W[pi];
-            uint32_t* base = a.out + sp_wbase[pi];
-            uint32_t o = 0;
-            for (uint32_t rr = 0; rr < tot; rr++)
-                if (base[(uint64_t)rr * W] != NONE) {
-                    if (o != rr)
-                        for (uint32_t w = 0; w < W; w++) base[(uint64_t)o * W + w] = base[(uint64_t)rr * W + w];
-                    o++;
-                }
-            tot = o;
-        }
-        a.count[oi] = sh_base == ~0ull ? 0 : tot;
+        a.count[oi] = sh_base == ~0ull ? 0 : sp_final[pi];
         a.off[oi] = sh_base == ~0ull ? 0 : sp_wbase[pi];
     }
 }
