@@ -241,7 +241,7 @@ __device__ __forceinline__ void swapw(uint32_t* a, uint32_t* b, uint32_t W) {
 }
 
 // in-place heapsort of n records of W words (the long slices: O(n log n) instead of insertion's n^2)
-__device__ void heap_sort_records(uint32_t* base, uint32_t n, uint32_t W) {
+__device__ __noinline__ void heap_sort_records(uint32_t* base, uint32_t n, uint32_t W) {
     auto sift = [&](uint32_t root, uint32_t end) {
         while (true) {
             uint32_t c = 2 * root + 1;
@@ -797,6 +797,33 @@ __device__ uint32_t indexed_products(const uint32_t* w0, uint32_t W0, const uint
 
 }  // namespace
 
+// A root group of several source-0 records yields one sorted run of products per record; the runs
+// are merged warp-parallel: each record's final rank = its index in its run + (records below it in
+// every other run, by binary search), scattered through a per-warp scratch and copied back.
+__device__ __noinline__ void merge_group(uint32_t* gout, uint32_t k, uint32_t cnt, uint32_t W, const uint32_t* runs,
+                                         uint32_t* tmp, uint32_t lane) {
+    for (uint32_t e = lane; e < cnt; e += 32) {
+        uint32_t a = 0;
+        while (a + 1 < k && runs[a + 1] <= e) a++;
+        const uint32_t* rec = gout + (uint64_t)e * W;
+        uint32_t rank = e - runs[a];
+        for (uint32_t bb = 0; bb < k; bb++) {
+            if (bb == a) continue;
+            uint32_t lo = runs[bb], hi = runs[bb + 1];   // first record of run bb not below rec
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (cmpw(gout + (uint64_t)mid * W, rec, W) < 0) lo = mid + 1;
+                else hi = mid;
+            }
+            rank += lo - runs[bb];
+        }
+        for (uint32_t w = 0; w < W; w++) tmp[rank * W + w] = rec[w];
+    }
+    __syncwarp();
+    for (uint32_t q = lane; q < cnt * W; q += 32) gout[q] = tmp[q];
+    __syncwarp();
+}
+
 // Products of one source-0 record (fields in m1s) with its staged source-1 run [p0, p1): 32 per
 // step, consistent ones compacted by ballot and written as consecutive records from row n.
 // WC > 0 fixes the record width at compile time (plan columns and the source-0 values live in
@@ -893,7 +920,10 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         if (tid == 0) { a.count[(uint64_t)r * L + l] = 0; a.off[(uint64_t)r * L + l] = 0; }
         return;
     }
-    unsigned long long* keys = big ? a.gkeys + sh_koff : sh_keys;
+    unsigned long long* gkeys = big ? a.gkeys + sh_koff : nullptr;
+    unsigned long long* keys = big ? gkeys : sh_keys;   // fill + sort (once)
+    // reads in the walks: SMEM loads on the common path (the generic pointer would cost each one)
+    auto key_at = [&](uint32_t p) -> unsigned long long { return big ? gkeys[p] : sh_keys[p]; };
     const bool indexed = v0 != NONE;
     if (indexed) {
         for (uint32_t i = tid; i < n1p; i += T)
@@ -915,7 +945,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         const uint32_t F = sh_plan.F, W1s = src[1].W;
         for (uint32_t e = tid; e < src[1].n * F; e += T) {
             const uint32_t p = e / F, f = e - p * F;
-            s1[e] = src[1].w[(uint64_t)(uint32_t)keys[p] * W1s + sh_plan.f1[f]];
+            s1[e] = src[1].w[(uint64_t)(uint32_t)key_at(p) * W1s + sh_plan.f1[f]];
         }
         __syncthreads();
     }
@@ -938,10 +968,10 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
             for (uint32_t x = tid; x < U; x += T) jrun[x] = 0;
             __syncthreads();
             for (uint32_t q = tid; q < n1; q += T) {
-                const uint32_t x = (uint32_t)(keys[q] >> 32);
-                if (q == 0 || (uint32_t)(keys[q - 1] >> 32) != x) {
+                const uint32_t x = (uint32_t)(key_at(q) >> 32);
+                if (q == 0 || (uint32_t)(key_at(q - 1) >> 32) != x) {
                     uint32_t e = q + 1;
-                    while (e < n1 && (uint32_t)(keys[e] >> 32) == x) e++;
+                    while (e < n1 && (uint32_t)(key_at(e) >> 32) == x) e++;
                     jrun[x] = q | ((e - q) << 16);
                 }
             }
@@ -975,30 +1005,6 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         // (records below it in every other run, by binary search), scattered through SMEM
         constexpr uint32_t GS_RUNS = 32;
         __shared__ uint32_t sh_runs[NW][GS_RUNS + 1];
-        auto merge_group = [&](uint32_t* gout, uint32_t k, uint32_t cnt) {
-            uint32_t* runs = sh_runs[warp];
-            uint32_t* tmp = a.gsort + (((uint64_t)r * L + l) * NW + warp) * JOIN_GSORT_WORDS;   // per-warp scratch
-            for (uint32_t e = lane; e < cnt; e += 32) {
-                uint32_t a = 0;
-                while (a + 1 < k && runs[a + 1] <= e) a++;
-                const uint32_t* rec = gout + (uint64_t)e * W;
-                uint32_t rank = e - runs[a];
-                for (uint32_t bb = 0; bb < k; bb++) {
-                    if (bb == a) continue;
-                    uint32_t lo = runs[bb], hi = runs[bb + 1];   // first record of run bb not below rec
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (cmpw(gout + (uint64_t)mid * W, rec, W) < 0) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    rank += lo - runs[bb];
-                }
-                for (uint32_t w = 0; w < W; w++) tmp[rank * W + w] = rec[w];
-            }
-            __syncwarp();
-            for (uint32_t q = lane; q < cnt * W; q += 32) gout[q] = tmp[q];
-            __syncwarp();
-        };
         auto walk = [&](uint32_t* out) -> uint32_t {   // out == nullptr: count only
             uint32_t n = 0;
             for (uint32_t g = wlo; g < whi;) {
@@ -1030,7 +1036,7 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                     for (uint32_t base = p0; base < p1; base += 32) {
                         const uint32_t p = base + lane;
                         bool ok = p < p1;
-                        const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)keys[p] * W1 : w1;
+                        const uint32_t* m2 = ok ? w1 + (uint64_t)(uint32_t)key_at(p) * W1 : w1;
                         for (uint32_t c = 0; c < jp.nchk && ok; c++) ok = m1s[jp.c0[c]] == m2[jp.c1[c]];
                         const uint32_t mask = __ballot_sync(0xffffffffu, ok);
                         if (out && ok) {
@@ -1046,7 +1052,8 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
                     if (k <= GS_RUNS && cnt * W <= JOIN_GSORT_WORDS) {
                         if (lane == 0) sh_runs[warp][k] = cnt;
                         __syncwarp();
-                        merge_group(out + (uint64_t)gstart * W, k, cnt);
+                        merge_group(out + (uint64_t)gstart * W, k, cnt, W, sh_runs[warp],
+                                    a.gsort + (((uint64_t)r * L + l) * NW + warp) * JOIN_GSORT_WORDS, lane);
                     } else {
                         if (lane == 0) sort_unique(out + (uint64_t)gstart * W, cnt, W);
                         __syncwarp();
