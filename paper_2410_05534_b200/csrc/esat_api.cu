@@ -111,6 +111,10 @@ struct esat_batch {
     uint64_t j_gkey_cap = 0;
     uint32_t* j_gsort = nullptr;             // join root-group merge scratch
     uint64_t j_gsort_cap = 0;
+    unsigned long long* j_big = nullptr;     // [R][L][2] long-list pair table (k_join -> k_join_big)
+    uint64_t j_big_cap = 0;
+    bool j_big_seen = false, j_big_launched = false;
+    JArgs j_args{};                          // arguments of the last k_join launch (reused by k_join_big)
     unsigned long long* d_tops = nullptr;   // [0] stage, [1] ematch out, [2] join stage, [3] join out
     uint32_t* d_jspec = nullptr;
     uint64_t jspec_cap = 0;
@@ -317,7 +321,7 @@ int esat_batch_destroy(esat_batch* b) {
     cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
-    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->j_gsort); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
+    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->j_gsort); cudaFree(b->j_big); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
     delete b;
     return ESAT_OK;
 }
@@ -747,11 +751,22 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
     return ESAT_OK;
 }
 
+// products of the long-list pairs k_join prepared (their table rows are ~0 otherwise)
+static int join_big_launch(esat_batch* b) {
+    esat_ctx* c = b->ctx;
+    const uint64_t L = b->L;
+    const uint32_t R = b->j_R;
+    constexpr unsigned Z = 512;
+    if (L && R) k_join_big<128><<<dim3((unsigned)L, R, Z), 128, 0, c->stream>>>((uint32_t)L, b->j_args);
+    b->j_big_launched = true;
+    return launch_check(c, "k_join_big");
+}
+
 static int join_launch(esat_batch* b) {
     esat_ctx* c = b->ctx;
     const uint64_t L = b->L;
     const uint32_t R = b->j_R, nsrc = b->j_nsrc, nmap_v = b->j_nmap_v, nmap_q = b->j_nmap_q;
-    CK(c, cudaMemsetAsync(b->d_tops + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(c, cudaMemsetAsync(b->d_tops + 2, 0, 3 * sizeof(unsigned long long), c->stream));
     CK(c, cudaMemsetAsync(b->d_over + 1, 0, sizeof(uint32_t), c->stream));
     const uint32_t* p = b->d_jspec;
     JArgs a{};
@@ -768,6 +783,12 @@ static int join_launch(esat_batch* b) {
     }
     a.gsort = b->j_gsort;
     a.gkeys = b->j_gkeys; a.gkey_cap = b->j_gkey_cap;
+    {
+        int rr = regrow(c, &b->j_big, &b->j_big_cap, 2ull * R * L);
+        if (rr) return rr;
+        CK(c, cudaMemsetAsync(b->j_big, 0xFF, 16ull * R * L, c->stream));
+    }
+    a.big = b->j_big;
     // run table in dynamic SMEM: one u32 per class id of the largest leaf (capped)
     uint64_t umax = 0;
     for (uint64_t l = 0; l < L; l++) umax = b->ub[l + 1] - b->ub[l] > umax ? b->ub[l + 1] - b->ub[l] : umax;
@@ -784,9 +805,13 @@ static int join_launch(esat_batch* b) {
     tic(c);
     if (L && R)
         k_join<128><<<dim3((unsigned)L, R), 128, 4 * (run_cap + JOIN_SMEM_S1), c->stream>>>((uint32_t)L, a);
+    b->j_args = a;
+    b->j_big_launched = false;
+    int r = launch_check(c, "k_join");
+    if (!r && b->j_big_seen) r = join_big_launch(b);   // batches known to hold long source lists
     toc(c);
     b->j_relaunch_needed = true;
-    return launch_check(c, "k_join");
+    return r;
 }
 
 static int join_settle(esat_batch* b) {
@@ -794,11 +819,19 @@ static int join_settle(esat_batch* b) {
     int r;
     for (int attempt = 0; attempt < 4; attempt++) {
         uint32_t over = 0;
-        unsigned long long tops[2];
+        unsigned long long tops[3];
         CK(c, cudaMemcpyAsync(&over, b->d_over + 1, 4, cudaMemcpyDeviceToHost, c->stream));
-        CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(tops, b->d_tops + 2, 24, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
-        if (!over) { b->j_verified = true; b->j_pending = false; return ESAT_OK; }
+        if (!over) {
+            if (tops[2] && !b->j_big_launched) {   // long-list pairs were prepared: write them now
+                b->j_big_seen = true;
+                if ((r = join_big_launch(b))) return r;
+            }
+            b->j_verified = true;
+            b->j_pending = false;
+            return ESAT_OK;
+        }
         if ((over & 4) && (r = regrow(c, &b->j_gkeys, &b->j_gkey_cap, tops[0]))) return r;
         if ((r = regrow(c, &b->j_out, &b->j_cap, tops[1]))) return r;
         if ((r = join_launch(b))) return r;

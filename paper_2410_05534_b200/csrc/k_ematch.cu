@@ -865,6 +865,184 @@ __device__ __forceinline__ uint32_t staged_products(const JoinPlan& jp, const ui
     return n;
 }
 
+// ---- long-list joins (BASELINE config 4's explosion) ---------------------------------------
+// Source 1 is sorted by every field it shares with source 0 (the join variable first, then the
+// checked variables / attributes, then the record), so a source-0 record's consistent partners are
+// exactly one run of the index and its product count is the run length. The preparing CTA writes,
+// per source-0 record, the run and the output offset (record order = output order); k_join_big
+// then fills the products with a grid of CTAs over source-0 root groups.
+__device__ __forceinline__ int tuple_cmp(const uint32_t* ra, const uint32_t* fa, const uint32_t* rb,
+                                         const uint32_t* fb, uint32_t nf) {
+    for (uint32_t f = 0; f < nf; f++) {
+        const uint32_t x = ra[fa[f]], y = rb[fb[f]];
+        if (x != y) return x < y ? -1 : 1;
+    }
+    return 0;
+}
+
+template <int T>
+__device__ void big_prepare(const JArgs& a, const Src* src, uint32_t NV, uint32_t NQ, uint32_t W, uint32_t v0,
+                            uint32_t v1, uint32_t n1p, uint32_t l, uint32_t r, uint32_t L, uint32_t* sh_scan) {
+    const uint32_t tid = threadIdx.x, n0 = src[0].n, n1 = src[1].n;
+    __shared__ JoinPlan plan;
+    __shared__ uint32_t f0[1 + 2 * MAX_V], f1[1 + 2 * MAX_V];
+    __shared__ uint32_t sh_nf;
+    __shared__ unsigned long long sh_off, sh_base;
+    if (tid == 0) {
+        make_plan(plan, src, NV, NQ, v1);
+        f0[0] = 1 + v0;
+        f1[0] = 1 + v1;
+        for (uint32_t c = 0; c < plan.nchk; c++) { f0[1 + c] = plan.c0[c]; f1[1 + c] = plan.c1[c]; }
+        sh_nf = 1 + plan.nchk;
+        const unsigned long long need = (unsigned long long)n1p + 2ull * n0;
+        unsigned long long o = atomicAdd(&a.tops[0], need);
+        if (o + need > a.gkey_cap) { atomicOr(a.overflow, 4u); o = ~0ull; }
+        sh_off = o;
+    }
+    __syncthreads();
+    const uint64_t pi = (uint64_t)r * L + l;
+    if (sh_off == ~0ull) {   // no scratch yet: the relaunch after regrowth does the work
+        if (tid == 0) { a.count[pi] = 0; a.off[pi] = 0; }
+        return;
+    }
+    unsigned long long* keys = a.gkeys + sh_off;
+    unsigned long long* recs = keys + n1p;   // [n0][2]: output record offset, run p0 | p1 << 32
+    const uint32_t nf = sh_nf, W1 = src[1].W, W0 = src[0].W;
+    const uint32_t *w0 = src[0].w, *w1 = src[1].w;
+    for (uint32_t i = tid; i < n1p; i += T) keys[i] = i < n1 ? i : ~0ull;
+    __syncthreads();
+    // bitonic sort of record indices by (shared fields, index); padding sorts last
+    for (uint32_t size = 2; size <= n1p; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < n1p / 2; i += T) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long x = keys[lo], y = keys[hi];
+                bool gt;
+                if (x == ~0ull || y == ~0ull) gt = x == ~0ull && y != ~0ull;
+                else {
+                    const int c = tuple_cmp(w1 + x * W1, f1, w1 + y * W1, f1, nf);
+                    gt = c > 0 || (c == 0 && x > y);
+                }
+                if (gt == up) { keys[lo] = y; keys[hi] = x; }
+            }
+            __syncthreads();
+        }
+    // per source-0 record: its run of consistent partners, then output offsets by a block scan
+    unsigned long long carry = 0;
+    for (uint32_t c0 = 0; c0 < n0; c0 += T) {
+        const uint32_t i = c0 + tid;
+        uint32_t p0 = 0, p1 = 0;
+        if (i < n0) {
+            const uint32_t* m0 = w0 + (uint64_t)i * W0;
+            uint32_t lo = 0, hi = n1;
+            while (lo < hi) {   // first partner not below the record's tuple
+                const uint32_t mid = (lo + hi) >> 1;
+                if (tuple_cmp(w1 + keys[mid] * W1, f1, m0, f0, nf) < 0) lo = mid + 1; else hi = mid;
+            }
+            p0 = lo;
+            hi = n1;
+            while (lo < hi) {   // first partner above it
+                const uint32_t mid = (lo + hi) >> 1;
+                if (tuple_cmp(w1 + keys[mid] * W1, f1, m0, f0, nf) <= 0) lo = mid + 1; else hi = mid;
+            }
+            p1 = lo;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_exscan(p1 - p0, sh_scan, &tot);
+        if (i < n0) {
+            recs[2 * (uint64_t)i] = carry + pre;
+            recs[2 * (uint64_t)i + 1] = (unsigned long long)p0 | ((unsigned long long)p1 << 32);
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        unsigned long long base = atomicAdd(&a.tops[1], carry * W);
+        if (base + carry * W > a.out_cap) { atomicOr(a.overflow, 2u); base = ~0ull; }
+        sh_base = base;
+        a.count[pi] = base == ~0ull ? 0 : (uint32_t)carry;
+        a.off[pi] = base == ~0ull ? 0 : base;
+        if (base != ~0ull) {
+            a.big[2 * pi] = sh_off;
+            a.big[2 * pi + 1] = base;
+            atomicAdd(&a.tops[2], 1ull);
+        }
+    }
+}
+
+// Products of the long-list pairs prepared by k_join: grid (L, R, Z), CTA z takes the z-th share of
+// source 0's root groups; a warp writes each record's run 32 products at a time at the record's
+// offset, then orders groups of several records (their runs are sorted, the group is sorted + deduped).
+template <int T>
+__global__ void __launch_bounds__(T) k_join_big(uint32_t L, JArgs a) {
+    const uint32_t l = blockIdx.x, r = blockIdx.y, z = blockIdx.z, Z = gridDim.z, tid = threadIdx.x;
+    const uint64_t pi = (uint64_t)r * L + l;
+    if (a.big[2 * pi] == ~0ull) return;
+    const uint32_t s0 = a.src_off[r], S = a.src_off[r + 1] - s0;
+    if (S != 2) return;
+    const uint32_t NV = a.nv[r], NQ = a.nq[r], W = S + NV + NQ;
+    Src src[2];
+    for (uint32_t s = 0; s < 2; s++) {
+        const uint32_t p = a.src[s0 + s];
+        const uint64_t mi = (uint64_t)p * L + l;
+        src[s].n = a.m_count[mi];
+        src[s].w = a.m_words + a.m_off[mi];
+        src[s].W = a.m_W[p];
+        const uint32_t vo = a.map_off[2 * (s0 + s)], qo = a.map_off[2 * (s0 + s) + 1];
+        src[s].V = a.map_off[2 * (s0 + s + 1)] - vo;
+        src[s].Q = a.map_off[2 * (s0 + s + 1) + 1] - qo;
+        src[s].vmap = a.vmap + vo;
+        src[s].qmap = a.qmap + qo;
+    }
+    uint32_t v0 = NONE, v1 = NONE;
+    for (uint32_t b = 0; b < src[1].V && v0 == NONE; b++)
+        for (uint32_t a0 = 0; a0 < src[0].V; a0++)
+            if (src[0].vmap[a0] == src[1].vmap[b]) { v0 = a0; v1 = b; break; }
+    __shared__ JoinPlan plan;
+    if (tid == 0) make_plan(plan, src, NV, NQ, v1);
+    __syncthreads();
+    const uint32_t n0 = src[0].n, n1 = src[1].n;
+    uint32_t n1p = 1;
+    while (n1p < n1) n1p <<= 1;
+    const unsigned long long* keys = a.gkeys + a.big[2 * pi];
+    const unsigned long long* recs = keys + n1p;
+    uint32_t* out = a.out + a.big[2 * pi + 1];
+    const uint32_t *w0 = src[0].w, *w1 = src[1].w;
+    const uint32_t W0 = src[0].W, W1 = src[1].W;
+    constexpr uint32_t NW = T / 32;
+    const uint32_t warp = tid >> 5, lane = tid & 31;
+    const uint32_t chz = (n0 + Z - 1) / Z;
+    const uint32_t zlo = group_start_at_or_after(src[0], min(n0, z * chz));
+    const uint32_t zhi = group_start_at_or_after(src[0], min(n0, (z + 1) * chz));
+    const uint32_t chw = (zhi - zlo + NW - 1) / NW;
+    const uint32_t wlo = group_start_at_or_after(src[0], min(zhi, zlo + warp * chw));
+    const uint32_t whi = group_start_at_or_after(src[0], min(zhi, zlo + (warp + 1) * chw));
+    for (uint32_t g = wlo; g < whi;) {
+        const uint32_t ge = group_end_warp(src[0], g, lane);
+        for (uint32_t i = g; i < ge; i++) {
+            const uint32_t* m1 = w0 + (uint64_t)i * W0;
+            const unsigned long long o = recs[2 * (uint64_t)i], rr = recs[2 * (uint64_t)i + 1];
+            const uint32_t p0 = (uint32_t)rr, p1 = (uint32_t)(rr >> 32);
+            for (uint32_t p = p0 + lane; p < p1; p += 32) {
+                const uint32_t* m2 = w1 + keys[p] * W1;
+                uint32_t* ob = out + (o + (p - p0)) * W;
+                for (uint32_t w = 0; w < W; w++) ob[w] = plan.src[w] ? m2[plan.idx[w]] : m1[plan.idx[w]];
+            }
+        }
+        if (ge - g > 1) {   // several source-0 records share the root: order the group's products
+            __syncwarp();
+            const unsigned long long gb = recs[2 * (uint64_t)g];
+            const unsigned long long rr = recs[2 * (uint64_t)(ge - 1) + 1];
+            const unsigned long long gend = recs[2 * (uint64_t)(ge - 1)] + ((uint32_t)(rr >> 32) - (uint32_t)rr);
+            if (lane == 0) sort_unique(out + gb * W, (uint32_t)(gend - gb), W);
+            __syncwarp();
+        }
+        g = ge;
+    }
+    (void)v0;
+}
+
 template <int T>
 __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
     const uint32_t l = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
@@ -901,29 +1079,20 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
         for (uint32_t b = 0; b < src[1].V && v0 == NONE; b++)
             for (uint32_t a0 = 0; a0 < src[0].V; a0++)
                 if (src[0].vmap[a0] == src[1].vmap[b]) { v0 = a0; v1 = b; break; }
-    // source 1 sorted by (join value, record): in SMEM, or for long lists (e-graph explosion) in a
-    // global scratch region bump-allocated per CTA (overflow -> the host regrows and relaunches)
-    __shared__ unsigned long long sh_koff;
+    // long source-1 lists (e-graph explosion): the CTA only prepares an index over every shared
+    // field and per-record product runs; k_join_big writes the products with many CTAs
     const bool big = v0 != NONE && src[1].n > JOIN_SMEM_KEYS;
     uint32_t n1p = 0;
     if (v0 != NONE) {
         n1p = 1;
         while (n1p < src[1].n) n1p <<= 1;
     }
-    if (big && tid == 0) {
-        unsigned long long o = atomicAdd(&a.tops[0], (unsigned long long)n1p);
-        if (o + n1p > a.gkey_cap) { atomicOr(a.overflow, 4u); o = ~0ull; }
-        sh_koff = o;
-    }
-    __syncthreads();
-    if (big && sh_koff == ~0ull) {   // no index scratch yet: the relaunch after regrowth does the work
-        if (tid == 0) { a.count[(uint64_t)r * L + l] = 0; a.off[(uint64_t)r * L + l] = 0; }
+    if (big) {
+        big_prepare<T>(a, src, NV, NQ, W, v0, v1, n1p, l, r, L, sh_scan);
         return;
     }
-    unsigned long long* gkeys = big ? a.gkeys + sh_koff : nullptr;
-    unsigned long long* keys = big ? gkeys : sh_keys;   // fill + sort (once)
-    // reads in the walks: SMEM loads on the common path (the generic pointer would cost each one)
-    auto key_at = [&](uint32_t p) -> unsigned long long { return big ? gkeys[p] : sh_keys[p]; };
+    unsigned long long* keys = sh_keys;
+    auto key_at = [&](uint32_t p) -> unsigned long long { return sh_keys[p]; };
     const bool indexed = v0 != NONE;
     if (indexed) {
         for (uint32_t i = tid; i < n1p; i += T)
@@ -1118,5 +1287,6 @@ __global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
 
 template __global__ void k_ematch<128>(Dev, MArgs);
 template __global__ void k_join<128>(uint32_t, JArgs);
+template __global__ void k_join_big<128>(uint32_t, JArgs);
 
 }  // namespace esat

@@ -51,6 +51,7 @@ struct JArgs {
     uint32_t* gsort;            // [R][L][warps][JOIN_GSORT_WORDS] root-group merge scratch
     unsigned long long* gkeys;  // global index scratch for source-1 lists beyond the SMEM index
     uint64_t gkey_cap;          //   (bump-allocated through tops[0]; overflow bit 4 -> regrow)
+    unsigned long long* big;    // [R][L][2] long-list pairs: scratch offsets of (index, record table); ~0 = none
 };
 
 constexpr uint32_t JOIN_SMEM_S1 = 4096;   // SMEM words for staged source-1 join fields
@@ -58,5 +59,6 @@ constexpr uint32_t JOIN_GSORT_WORDS = 1024; // per-warp words for merging a root
 
 template <int T> __global__ void k_ematch(Dev, MArgs);
 template <int T> __global__ void k_join(uint32_t, JArgs);
+template <int T> __global__ void k_join_big(uint32_t, JArgs);
 
 }  // namespace esat
