@@ -425,7 +425,10 @@ static int launch_extract(esat_batch* b, int method, cudaStream_t s) {
         x.pool_key = b->pool_key;
         x.pool_val = b->pool_val;
     }
-    static const int xt = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 32;
+    // one warp per leaf keeps a full batch resident (the MCTS case); a batch with fewer leaves than
+    // SMs (one huge e-graph, config 4) gives each leaf four warps for its wide levels instead
+    static const int xt_env = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 0;
+    const int xt = xt_env ? xt_env : (b->L < 148 ? 128 : 32);
     if (b->L) {
         if (xt == 128) k_extract<128><<<b->L, 128, 0, s>>>(b->d, x);
         else if (xt == 64) k_extract<64><<<b->L, 64, 0, s>>>(b->d, x);
