@@ -308,7 +308,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
-    OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N);
+    OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N); OWN(x.lhn, N); OWN(x.lcc, 2 * N);
     x.slot_stride = N;
     *out = b;
     return ESAT_OK;

@@ -63,7 +63,9 @@ struct XArgs {
     uint32_t *pool_key;
     double* pool_val;
     uint32_t *hoff, *hrng;               // [2][node rows] history block offset / occupied range per class position (pass parity)
-    uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip)
+    uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip): bit 0 cost, bit 1 history
+    uint32_t* lhn;               // [node rows] flushed node of each class at its last merge (flush reuse)
+    double* lcc;                 // [2 x node rows] its child contributions (cc1, cc2)
     uint64_t slot_stride;
 };
 

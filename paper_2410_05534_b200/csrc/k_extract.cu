@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     uint32_t* level = x.level + b;
     uint32_t* order = x.order + b;
     uint32_t* lvcnt = x.lvcnt + b + l;   // C+1 entries
+    uint32_t* lhn = x.lhn + b;           // flushed node (| skip2 << 31) of each class at its last merge
+    double* lcc = x.lcc + 2 * b;         // its two child contributions then
     const bool ocf = x.method == 1;
     uint64_t capk = 0, capv = 0;
     uint32_t* hoffw[2] = {nullptr, nullptr};
@@ -294,6 +296,10 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
 
     __shared__ uint32_t sh_scan[33];
     __shared__ uint32_t sh_flag, sh_maxlv, sh_topk, sh_topv, sh_over;
+#ifdef ESAT_DEBUG
+    __shared__ unsigned dbg[2][8];   // per pass: evaluated classes, their nodes, merges, flush reuses, unchanged
+    if (tid < 16) dbg[tid / 8][tid % 8] = 0;
+#endif
 
     for (uint32_t k = tid; k < C; k += T) {
         cost[k] = __longlong_as_double(0x7ff0000000000000ll);
@@ -400,7 +406,10 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 }
                 double bv = __longlong_as_double(0x7ff0000000000000ll);
                 uint32_t bn = NONE;
-                bool changed = pass == 0;
+                bool changed = pass == 0, hchg = pass == 0;
+#ifdef ESAT_DEBUG
+                if (pass < 2) { atomicAdd(&dbg[pass][0], 1u); atomicAdd(&dbg[pass][1], coff[k + 1] - coff[k]); }
+#endif
                 if (!ocf) {
                     for (uint32_t nd = coff[k]; nd < coff[k + 1]; nd++) {
                         double v = c.ncost[nd];
@@ -427,7 +436,32 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                         }
                         if (bn == NONE || v < bv) { bv = v; bn = nd; }
                     }
-                    if (C > 1) {
+                    // Flush reuse (exact): the same flushed node with the same child contributions and
+                    // children whose histories did not change (flag bit 1, read under the Gauss-Seidel
+                    // rule) merges to the same history -- keep the previous block, no merge, no compare.
+                    const uint32_t hkey = hn == NONE ? NONE : (hn | (h_skip2 ? 0x80000000u : 0u));
+                    bool same = false;
+                    if (C > 1 && pass > 0 && hkey == lhn[k] && !h_gen) {
+                        same = true;
+                        if (hn != NONE) {
+                            for (uint32_t q = c.nko[hn]; q < c.nko[hn + 1] && same; q++) {
+                                const uint32_t j = c.kpos[q];
+                                same = !((j < k ? chg_cur[j] : chg_prv[j]) & 2u);
+                            }
+                            same = same && __double_as_longlong(h_cc1) == __double_as_longlong(lcc[2 * k]) &&
+                                   __double_as_longlong(h_cc2) == __double_as_longlong(lcc[2 * k + 1]);
+                        }
+                    }
+#ifdef ESAT_DEBUG
+                    if (pass < 2) atomicAdd(&dbg[pass][same ? 3 : 2], 1u);
+#endif
+                    if (same) {
+                        hoffw[par][k] = hoffw[ppar][k];
+                        hrngw[par][k] = hrngw[ppar][k];
+                    } else if (C > 1) {
+                        lhn[k] = h_gen ? NONE - 1 : hkey;
+                        lcc[2 * k] = h_cc1;
+                        lcc[2 * k + 1] = h_cc2;
                         uint32_t offk = 0, rng = 0;
                         bool ok = true;
                         if (hn != NONE && h_gen) {
@@ -452,22 +486,23 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                         if (!ok) { offk = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
                         hoffw[par][k] = offk;
                         hrngw[par][k] = rng;
-                        if (!changed) {  // did the flushed history change w.r.t. last pass?
+                        hchg = pass == 0;
+                        if (!hchg) {  // did the flushed history change w.r.t. last pass?
                             const uint32_t ok2 = hoffw[ppar][k], r2 = hrngw[ppar][k];
                             const uint32_t la = rng & 0xFFFFu, ha = rng >> 16, lb = r2 & 0xFFFFu, hb2 = r2 >> 16;
                             const uint32_t lo = min(la, lb), hi = max(ha, hb2);
                             const uint32_t* a1 = pkw + offk;
                             const uint32_t* b1 = pkw + ok2;
-                            for (uint32_t w = 4 * lo; w < 4 * hi && !changed; w++) {
+                            for (uint32_t w = 4 * lo; w < 4 * hi && !hchg; w++) {
                                 const uint32_t p = (w >= 4 * la && w < 4 * ha) ? a1[w] : 0u;
                                 const uint32_t q = (w >= 4 * lb && w < 4 * hb2) ? b1[w] : 0u;
-                                if (p != q) { changed = true; break; }
+                                if (p != q) { hchg = true; break; }
                                 if (!p) continue;
                                 const uint32_t pa = a1[NW + w], pb = b1[NW + w];
                                 if (pa == pb) continue;   // shared storage
                                 for (uint32_t i = 0; i < (uint32_t)__popc(p); i++)
                                     if (__double_as_longlong(pvw[pa + i]) != __double_as_longlong(pvw[pb + i])) {
-                                        changed = true;
+                                        hchg = true;
                                         break;
                                     }
                             }
@@ -475,7 +510,10 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                     }
                 }
                 if (bn != NONE && bv < cost[k]) { cost[k] = bv; ch[k] = bn; sh_flag = 1; changed = true; }
-                chg_cur[k] = changed ? 1 : 0;
+                chg_cur[k] = (changed ? 1 : 0) | (hchg ? 2 : 0);   // bit 0 cost, bit 1 history
+#ifdef ESAT_DEBUG
+                if (pass < 2 && !hchg && !changed) atomicAdd(&dbg[pass][4], 1u);
+#endif
             }
             __syncthreads();
         }
@@ -566,6 +604,9 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
             printf("leaf %u C %u nlv %u passes %u: levels %lld sort %lld pass0 %lld pass1 %lld pass2 %lld k10 %lld cyc\n", l, C,
                    nlv, passes, t_lv - t_start, t_sort - t_lv, t_pass[0] - t_sort, passes > 1 ? t_pass[1] - t_pass[0] : 0ll,
                    passes > 2 ? t_pass[2] - t_pass[1] : 0ll, clock64() - t_pass[passes > 8 ? 7 : passes - 1]);
+        if (l == 0 || l == 5)
+            printf("leaf %u dbg p0 %u %u %u %u %u | p1 %u %u %u %u %u\n", l, dbg[0][0], dbg[0][1], dbg[0][2], dbg[0][3],
+                   dbg[0][4], dbg[1][0], dbg[1][1], dbg[1][2], dbg[1][3], dbg[1][4]);
 #endif
         if (st == X_CAPACITY) err = sh_over;   // 1: bitset pool, 2: value pool
         x.status[l] = st;
