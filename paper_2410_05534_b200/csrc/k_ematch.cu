@@ -437,13 +437,13 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     const uint32_t PC = P * C;
     uint32_t* pc = a.raw + d.nb[l] * MAXP;   // [P][C] counts -> offsets (C <= n, P <= 32)
     uint32_t* nzl = a.nzl + d.nb[l] * MAXP;  // (pattern, class) pairs with matches (any order)
-    __shared__ uint32_t sh_nz;
-    if (tid == 0) sh_nz = 0;
+    __shared__ uint32_t sh_nz, sh_next, sh_next2;
+    if (tid == 0) { sh_nz = 0; sh_next = T; sh_next2 = T; }
     __syncthreads();
-    uint32_t pi_i = C ? tid / C : 0, r_i = C ? tid - pi_i * C : 0;
-    for (uint32_t i = tid; i < PC; i += T) {
-        const uint32_t pi = pi_i, r = r_i;
-        for (r_i += T; r_i >= C; r_i -= C) pi_i++;   // next (pattern, class) of this thread
+    // (pattern, class) pairs are handed out dynamically: a thread that drew a heavy pair does not
+    // also own a fixed share of the rest
+    for (uint32_t i = tid; i < PC; i = atomicAdd(&sh_next, 1u)) {
+        const uint32_t pi = i / C, r = i - pi * C;
         uint32_t n = 0;
         const uint32_t rb = sp_rbit[pi];
         if (!rb || (cmask[r] & rb)) {
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     __syncthreads();
     if (sh_base != ~0ull) {
         const uint32_t grand = sp_rbase[P], nz = sh_nz;
-        for (uint32_t j = tid; j < nz; j += T) {
+        for (uint32_t j = tid; j < nz; j = atomicAdd(&sh_next2, 1u)) {
             const uint32_t i = nzl[j];
             const uint32_t beg = pc[i], end = (i + 1 < PC) ? pc[i + 1] : grand;
             if (beg == end) continue;
