@@ -339,18 +339,34 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     } else {
         m.s_name = d.sym_name; m.s_arity = d.sym_arity; m.s_poff = d.sym_poff; m.s_par = d.sym_par;
     }
-    // the call's pattern programs
-    uint32_t pwords = 0;
-    for (uint32_t pi = 0; pi < a.P; pi++) pwords += a.prog_off[a.pat_ids[pi] + 1] - a.prog_off[a.pat_ids[pi]];
-    const bool progs_smem = pwords <= PROG_WORDS;
-    if (progs_smem) {
-        uint32_t o = 0;
-        for (uint32_t pi = 0; pi < a.P; pi++) {
-            const uint32_t po = a.prog_off[a.pat_ids[pi]], pn = a.prog_off[a.pat_ids[pi] + 1] - po;
-            for (uint32_t w = tid; w < pn; w += T) sprog[o + w] = a.prog[po + w];
-            o += pn;
+    // the call's pattern programs: warp 0 reads every pattern's program range at once (a scan gives
+    // the shared-memory offsets), then the block copies them word-parallel
+    __shared__ uint32_t sp_po[MAXP], sp_pn[MAXP], sp_so[MAXP + 1];
+    if (tid < 32) {
+        uint32_t po = 0, pn = 0;
+        if (tid < a.P) {
+            const uint32_t pid = a.pat_ids[tid];
+            po = a.prog_off[pid];
+            pn = a.prog_off[pid + 1] - po;
         }
+        uint32_t inc = pn;
+#pragma unroll
+        for (uint32_t d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (tid >= d) inc += y;
+        }
+        if (tid < a.P) { sp_po[tid] = po; sp_pn[tid] = pn; sp_so[tid] = inc - pn; }
+        if (tid == 31) sp_so[MAXP] = inc;
     }
+    __syncthreads();
+    const uint32_t pwords = sp_so[MAXP];
+    const bool progs_smem = pwords <= PROG_WORDS;
+    if (progs_smem)
+        for (uint32_t w = tid; w < pwords; w += T) {
+            uint32_t pi = 0;
+            while (pi + 1 < a.P && sp_so[pi + 1] <= w) pi++;
+            sprog[w] = a.prog[sp_po[pi] + (w - sp_so[pi])];
+        }
     __syncthreads();
     if (need <= a.smem_bytes) mbar_wait(&bar, 0);
 
@@ -375,11 +391,8 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     auto nothing = [](uint32_t, const uint32_t*, const int32_t*) {};
     // per-pattern program pointers
     auto prog_of = [&](uint32_t pi, uint32_t& poff_smem) -> const int32_t* {
-        const uint32_t pid = a.pat_ids[pi];
-        const uint32_t po = a.prog_off[pid], pn = a.prog_off[pid + 1] - po;
-        const int32_t* pg = progs_smem ? sprog + poff_smem : a.prog + po;
-        poff_smem += pn;
-        return pg;
+        (void)poff_smem;
+        return progs_smem ? sprog + sp_so[pi] : a.prog + sp_po[pi];
     };
     auto set_prog = [&](const int32_t* pg) {
         m.prog = pg;
@@ -414,22 +427,17 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
     __shared__ uint32_t sp_rbase[MAXP + 1];
     __shared__ unsigned long long sp_wbase[MAXP];
     const uint32_t P = a.P;
-    if (tid == 0) {
-        uint32_t po = 0;
-        for (uint32_t pi = 0; pi < P; pi++) {
-            const uint32_t pid = a.pat_ids[pi];
-            const int32_t* pg = progs_smem ? sprog + po : a.prog + a.prog_off[pid];
-            sp_off[pi] = progs_smem ? po : a.prog_off[pid];
-            po += a.prog_off[pid + 1] - a.prog_off[pid];
-            sp_W[pi] = 1 + pg[1] + pg[2];
-            const uint32_t rname = (uint32_t)pg[3 + 1];
-            sp_rbit[pi] = (cmask && pg[3] == 1 && rname < 32) ? (1u << rname) : 0u;
-            sp_dup[pi] = 0;
-        }
+    if (tid < P) {
+        const uint32_t pi = tid;
+        sp_off[pi] = progs_smem ? sp_so[pi] : sp_po[pi];
+        const int32_t* pg = (progs_smem ? sprog : a.prog) + sp_off[pi];
+        sp_W[pi] = 1 + pg[1] + pg[2];
+        const uint32_t rname = (uint32_t)pg[3 + 1];
+        sp_rbit[pi] = (cmask && pg[3] == 1 && rname < 32) ? (1u << rname) : 0u;
+        sp_dup[pi] = 0;
     }
     for (uint32_t pi = tid; pi < P; pi += T) {
-        const uint32_t pid = a.pat_ids[pi];
-        decode_flat2(a.prog + a.prog_off[pid], sp_flat[pi]);
+        decode_flat2((progs_smem ? sprog + sp_so[pi] : a.prog + sp_po[pi]), sp_flat[pi]);
         if (a.no_flat) sp_flat[pi].ok = 0;
     }
     __syncthreads();
