@@ -134,16 +134,28 @@ __device__ double overlap_max(const LeafCtx& c, const Hist& hA, uint32_t sA, con
 // key wins; Alg. 2's enode_hist[child] = cc overrides an inherited value). Writes the block at
 // ob and fresh values into the value pool; returns the packed range lo4 | hi4 << 16, or NONE
 // when the value pool is exhausted (*over gets bit 2).
+//
+// With hO present (the class's previous flush), the merge also answers "did the history change?"
+// (*chg) and keeps hO's value storage for every word whose keys and values are unchanged, so an
+// unchanged history keeps its value pointers from pass to pass and later comparisons against it
+// are pointer tests. Without hO, *chg is left alone.
 __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, double vA, const Hist& hB,
                                 uint32_t sB, double vB, uint32_t* ob, uint32_t* topv, uint64_t capv, double* pv,
-                                uint32_t* over) {
+                                uint32_t* over, const Hist& hO, bool* chg) {
     const uint32_t NW = c.NW;
     uint32_t lo = 0xFFFFu, hi = 0;
     if (sA != NONE) { lo = min(lo, sA >> 7); hi = max(hi, (sA >> 7) + 1); }
     if (sB != NONE) { lo = min(lo, sB >> 7); hi = max(hi, (sB >> 7) + 1); }
     if (hA.present && hA.hi4 > hA.lo4) { lo = min(lo, hA.lo4); hi = max(hi, hA.hi4); }
     if (hB.present && hB.hi4 > hB.lo4) { lo = min(lo, hB.lo4); hi = max(hi, hB.hi4); }
-    if (hi <= lo) return 0u;
+    bool dif = false;
+    if (hO.present)   // keys of the previous flush outside the new range
+        for (uint32_t w = 4 * hO.lo4; w < 4 * hO.hi4 && !dif; w++)
+            if ((w < 4 * lo || w >= 4 * hi) && hO.bits[w]) dif = true;
+    if (hi <= lo) {
+        if (hO.present) *chg = dif;
+        return 0u;
+    }
     // pass 1: fresh value count (words that mix sources or hold a new key)
     uint32_t fresh = 0;
     for (uint32_t w = 4 * lo; w < 4 * hi; w++) {
@@ -158,19 +170,51 @@ __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, d
     const double *mA = hA.present ? wmax_of(c, hA) : nullptr, *mB = hB.present ? wmax_of(c, hB) : nullptr;
     uint32_t* optr = ob + NW;
     double* omax = reinterpret_cast<double*>(ob + 2 * NW);
+    const uint32_t* pO = hO.present ? wptr_of(c, hO) : nullptr;
+    const double* mO = hO.present ? wmax_of(c, hO) : nullptr;
     uint32_t o = base;
     for (uint32_t w = 4 * lo; w < 4 * hi; w++) {
         const uint32_t wA = hword(hA, w), wB = hword(hB, w), sp = bit_of(sA, w) | bit_of(sB, w);
         uint32_t ow = wA | wB | sp;
         ob[w] = ow;
-        if (!sp && wA && !(wB & ~wA)) { optr[w] = pA[w]; omax[w] = mA[w]; continue; }   // hA's word
-        if (!sp && !wA) {                                                                // hB's word (or empty)
-            optr[w] = wB ? pB[w] : 0u;
-            omax[w] = wB ? mB[w] : 0.0;
+        // same keys as the previous flush so far? (then its values are the comparison)
+        const bool cmp = hO.present && !dif && ow && hword(hO, w) == ow;
+        if (hO.present && !dif && hword(hO, w) != ow) dif = true;
+        if (!sp && (wA ? !(wB & ~wA) : true)) {   // one source's word (hA's, else hB's, or empty)
+            uint32_t sp_ = wA ? pA[w] : (wB ? pB[w] : 0u);
+            const double sm = wA ? mA[w] : (wB ? mB[w] : 0.0);
+            if (cmp && pO[w] != sp_) {
+                const double *x1 = c.pv + sp_, *x2 = c.pv + pO[w];
+                bool eq = true;
+                for (int i = 0, n = __popc(ow); i < n && eq; i++)
+                    eq = __double_as_longlong(x1[i]) == __double_as_longlong(x2[i]);
+                if (eq) sp_ = pO[w];   // identical values: keep the previous storage
+                else dif = true;
+            }
+            optr[w] = sp_;
+            omax[w] = sm;
             continue;
         }
         const double* va = wA ? c.pv + pA[w] : nullptr;
         const double* vb = wB ? c.pv + pB[w] : nullptr;
+        if (cmp) {   // a mixed word with the previous flush's keys: unchanged values keep its storage
+            const double* vo = c.pv + pO[w];
+            bool eq = true;
+            uint32_t m = ow;
+            for (int i = 0; m && eq; i++) {
+                const int bpos = __ffs(m) - 1;
+                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
+                double val;
+                if (key == sA) val = vA;
+                else if (key == sB) val = vB;
+                else if ((wA >> bpos) & 1u) val = va[__popc(wA & below)];
+                else val = vb[__popc(wB & below)];
+                eq = __double_as_longlong(val) == __double_as_longlong(vo[i]);
+                m &= m - 1;
+            }
+            if (eq) { optr[w] = pO[w]; omax[w] = mO[w]; continue; }
+            dif = true;
+        }
         optr[w] = o;
         double mx = 0.0;
         while (ow) {
@@ -187,6 +231,7 @@ __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, d
         }
         omax[w] = mx;
     }
+    if (hO.present) *chg = dif;
     return lo | (hi << 16);
 }
 
@@ -237,13 +282,12 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
                                     : child_cost(c, ck);
         const uint32_t nb = atomicAdd(topk, 4 * NW);
         if ((uint64_t)nb + 4 * NW > capk) { atomicOr(over, 1u); *boff = NONE; *rng = 0; return v + cc; }
-        const uint32_t r = merge_write(c, H, ck, cc, h, NONE, 0.0, pk + nb, topv, capv, pv, over);
+        const uint32_t r = merge_write(c, H, ck, cc, h, NONE, 0.0, pk + nb, topv, capv, pv, over, none, nullptr);
         if (r == NONE) { *boff = NONE; *rng = 0; return v + cc; }
         hb = nb; hr = r;
         H.bits = pk + nb; H.lo4 = r & 0xFFFFu; H.hi4 = r >> 16; H.present = true;
         v = v + cc;
     }
-    (void)none;
     *boff = hb;
     *rng = hr;
     return v;
@@ -463,7 +507,7 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                         lcc[2 * k] = h_cc1;
                         lcc[2 * k + 1] = h_cc2;
                         uint32_t offk = 0, rng = 0;
-                        bool ok = true;
+                        bool ok = true, merged = false, mchg = true;
                         if (hn != NONE && h_gen) {
                             ok = gb != NONE;
                             offk = gb; rng = grng;
@@ -478,16 +522,23 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                                 atomicOr(&sh_over, 1u);
                                 ok = false;
                             } else {
+                                Hist hO{nullptr, 0u, 0u, false};
+                                if (pass > 0) {
+                                    const uint32_t r2 = hrngw[ppar][k];
+                                    hO = Hist{pkw + hoffw[ppar][k], r2 & 0xFFFFu, r2 >> 16, true};
+                                }
                                 rng = merge_write(c, h1, c1, h_cc1, h2, c2, h_cc2, pkw + offk, &sh_topv, capv, pvw,
-                                                  &sh_over);
+                                                  &sh_over, hO, &mchg);
                                 ok = rng != NONE;
+                                merged = pass > 0 && ok;
                             }
                         }   // else: empty history (no node, or a leaf node): the empty range, no block
                         if (!ok) { offk = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
                         hoffw[par][k] = offk;
                         hrngw[par][k] = rng;
                         hchg = pass == 0;
-                        if (!hchg) {  // did the flushed history change w.r.t. last pass?
+                        if (merged) hchg = mchg;   // answered by the merge
+                        else if (!hchg) {  // did the flushed history change w.r.t. last pass?
                             const uint32_t ok2 = hoffw[ppar][k], r2 = hrngw[ppar][k];
                             const uint32_t la = rng & 0xFFFFu, ha = rng >> 16, lb = r2 & 0xFFFFu, hb2 = r2 >> 16;
                             const uint32_t lo = min(la, lb), hi = max(ha, hb2);
