@@ -24,14 +24,6 @@ namespace {
 __constant__ uint64_t B2B_IV[8] = {0x6a09e667f3bcc908ull, 0xbb67ae8584caa73bull, 0x3c6ef372fe94f82bull,
                                    0xa54ff53a5f1d36f1ull, 0x510e527fade682d1ull, 0x9b05688c2b3e6c1full,
                                    0x1f83d9abfb41bd6bull, 0x5be0cd19137e2179ull};
-__constant__ uint8_t B2B_SIGMA[12][16] = {
-    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
-    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
-    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
-    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
-    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
-    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
-
 __device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
 
 struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(digest_size=8))
@@ -48,29 +40,43 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
         n = 0;
         acc = 0;
     }
-    __device__ void compress(bool last) {
+    __device__ __noinline__ void compress(bool last) {
+        // the 12 rounds written out with the BLAKE2b sigma schedule as literals: the message words
+        // are read once into registers and every schedule index is a register name (m itself stays
+        // addressable for put); one out-of-line copy keeps the kernel's code small
+        uint64_t mm[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) mm[i] = m[i];
         uint64_t v[16];
+#pragma unroll
         for (int i = 0; i < 8; i++) { v[i] = h[i]; v[i + 8] = B2B_IV[i]; }
         v[12] ^= t;
         if (last) v[14] = ~v[14];
-#pragma unroll 1
-        for (int r = 0; r < 12; r++) {
-            const uint8_t* s = B2B_SIGMA[r];
 #define B2G(a, b, c, d, x, y)                         \
     v[a] = v[a] + v[b] + x; v[d] = rotr(v[d] ^ v[a], 32); \
     v[c] = v[c] + v[d];     v[b] = rotr(v[b] ^ v[c], 24); \
     v[a] = v[a] + v[b] + y; v[d] = rotr(v[d] ^ v[a], 16); \
     v[c] = v[c] + v[d];     v[b] = rotr(v[b] ^ v[c], 63);
-            B2G(0, 4, 8, 12, m[s[0]], m[s[1]]);
-            B2G(1, 5, 9, 13, m[s[2]], m[s[3]]);
-            B2G(2, 6, 10, 14, m[s[4]], m[s[5]]);
-            B2G(3, 7, 11, 15, m[s[6]], m[s[7]]);
-            B2G(0, 5, 10, 15, m[s[8]], m[s[9]]);
-            B2G(1, 6, 11, 12, m[s[10]], m[s[11]]);
-            B2G(2, 7, 8, 13, m[s[12]], m[s[13]]);
-            B2G(3, 4, 9, 14, m[s[14]], m[s[15]]);
+#define B2R(s0, s1, s2, s3, s4, s5, s6, s7, s8, s9, s10, s11, s12, s13, s14, s15) \
+    B2G(0, 4, 8, 12, mm[s0], mm[s1]) B2G(1, 5, 9, 13, mm[s2], mm[s3])             \
+    B2G(2, 6, 10, 14, mm[s4], mm[s5]) B2G(3, 7, 11, 15, mm[s6], mm[s7])           \
+    B2G(0, 5, 10, 15, mm[s8], mm[s9]) B2G(1, 6, 11, 12, mm[s10], mm[s11])         \
+    B2G(2, 7, 8, 13, mm[s12], mm[s13]) B2G(3, 4, 9, 14, mm[s14], mm[s15])
+        B2R(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15)
+        B2R(14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3)
+        B2R(11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4)
+        B2R(7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8)
+        B2R(9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13)
+        B2R(2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9)
+        B2R(12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11)
+        B2R(13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10)
+        B2R(6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5)
+        B2R(10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0)
+        B2R(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15)
+        B2R(14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3)
+#undef B2R
 #undef B2G
-        }
+#pragma unroll
         for (int i = 0; i < 8; i++) h[i] ^= v[i] ^ v[i + 8];
     }
     __device__ __forceinline__ void put(uint8_t c) {
@@ -88,7 +94,14 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
     __device__ void putu(uint64_t x) {   // decimal repr of a non-negative int
         char d[24];
         int k = 0;
-        do { d[k++] = (char)('0' + x % 10); x /= 10; } while (x);
+        while (x >= 1000000000ull) {   // 9-digit chunks: one 64-bit division per chunk, 32-bit digits
+            uint32_t r = (uint32_t)(x % 1000000000ull);
+            x /= 1000000000ull;
+#pragma unroll
+            for (int i = 0; i < 9; i++) { d[k++] = (char)('0' + r % 10u); r /= 10u; }
+        }
+        uint32_t y = (uint32_t)x;
+        do { d[k++] = (char)('0' + y % 10u); y /= 10u; } while (y);
         while (k) put((uint8_t)d[--k]);
     }
     // int.from_bytes(digest, "big"): the digest is h[0] little-endian
