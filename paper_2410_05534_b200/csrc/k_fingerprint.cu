@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
     unsigned long long* lab[2] = {a.lab0 + b, a.lab1 + b};
     uint32_t* rep[2] = {a.rep0 + b, a.rep1 + b};
     uint32_t* nord = a.nord + b;
+    uint8_t* lchg = a.lchg + b;
     const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
     unsigned long long* tkey = a.tkey + t0;
     uint32_t* tval = a.tval + t0;
@@ -229,6 +230,15 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         const unsigned long long* lc = lab[cur];
         unsigned long long* ln = lab[cur ^ 1];
         for (uint32_t c = tid; c < C; c += T) {
+            // From the second refinement on, a class none of whose children changed label in the last
+            // round hashes exactly the bytes it hashed then, so its label carries over.
+            if (it > 0) {
+                bool dirty = false;
+                for (uint32_t nd = L.coff[c]; nd < L.coff[c + 1] && !dirty; nd++)
+                    for (uint32_t q = L.nko[nd]; q < L.nko[nd + 1]; q++)
+                        if (lchg[L.kpos[q]]) { dirty = true; break; }
+                if (!dirty) { ln[c] = lc[c]; continue; }
+            }
             uint32_t* ord = nord + L.coff[c];
             const uint32_t nn = sorted_nodes(L, lc, c, ord, true);
             B2b h;
@@ -248,6 +258,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         // partition: every class -> smallest class position (= smallest id) with its label
         for (uint32_t c = tid; c < C; c += T) {
             const unsigned long long key = ln[c];
+            lchg[c] = key != lc[c];
             uint32_t s = (uint32_t)(mix64(key) & tmask);
             while (true) {
                 const unsigned long long prev = atomicCAS(&tkey[s], ~0ull, key);
