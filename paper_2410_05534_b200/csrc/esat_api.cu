@@ -1105,7 +1105,7 @@ int esat_fingerprint_setup(esat_ctx* c, uint32_t n_syms, const uint32_t* krank, 
     const uint32_t nb = key_off[n_syms];
     if ((r = dalloc(c, &c->f_krank, n_syms))) return r;
     if ((r = dalloc(c, &c->f_koff, n_syms + 1))) return r;
-    if ((r = dalloc(c, &c->f_kbytes, nb ? nb : 1))) return r;
+    if ((r = dalloc(c, &c->f_kbytes, nb + 16))) return r;   // + 16: k_fingerprint reads whole words
     CK(c, cudaMemcpy(c->f_krank, krank, 4ull * n_syms, cudaMemcpyHostToDevice));
     CK(c, cudaMemcpy(c->f_koff, key_off, 4ull * (n_syms + 1), cudaMemcpyHostToDevice));
     if (nb) CK(c, cudaMemcpy(c->f_kbytes, key_bytes, nb, cudaMemcpyHostToDevice));

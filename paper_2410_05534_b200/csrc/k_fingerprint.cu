@@ -79,30 +79,65 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
 #pragma unroll
         for (int i = 0; i < 8; i++) h[i] ^= v[i] ^ v[i + 8];
     }
-    __device__ __forceinline__ void put(uint8_t c) {
-        if (n == 128) {   // a full block is compressed only once more data follows (BLAKE2b rule)
-            t += 128;
-            compress(false);
-            n = 0;
+    // k (1..8) bytes packed little-endian in v (first byte in the low bits): the stream is filled a
+    // word at a time (one shift-or per word, the spill carried into the next word) instead of bytewise
+    __device__ __forceinline__ void putw(uint64_t v, uint32_t k) {
+        while (k) {
+            if (n == 128) {   // a full block is compressed only once more data follows (BLAKE2b rule)
+                t += 128;
+                compress(false);
+                n = 0;
+            }
+            const uint32_t room = 128 - n, take = k < room ? k : room, sh = n & 7;
+            const uint64_t part = take == 8 ? v : (v & ((1ull << (8 * take)) - 1));
+            acc |= part << (8 * sh);
+            if (sh + take >= 8) {
+                m[n >> 3] = acc;
+                acc = sh ? part >> (8 * (8 - sh)) : 0;
+            }
+            n += take;
+            v = take == 8 ? 0 : v >> (8 * take);
+            k -= take;
         }
-        acc |= (uint64_t)c << (8 * (n & 7));
-        n++;
-        if ((n & 7) == 0) { m[(n >> 3) - 1] = acc; acc = 0; }
     }
-    __device__ void puts(const char* s) { while (*s) put((uint8_t)*s++); }
-    __device__ void putb(const uint8_t* s, uint32_t len) { for (uint32_t i = 0; i < len; i++) put(s[i]); }
-    __device__ void putu(uint64_t x) {   // decimal repr of a non-negative int
-        char d[24];
-        int k = 0;
-        while (x >= 1000000000ull) {   // 9-digit chunks: one 64-bit division per chunk, 32-bit digits
-            uint32_t r = (uint32_t)(x % 1000000000ull);
-            x /= 1000000000ull;
-#pragma unroll
-            for (int i = 0; i < 9; i++) { d[k++] = (char)('0' + r % 10u); r /= 10u; }
+    __device__ __forceinline__ void put(uint8_t c) { putw(c, 1); }
+    // len bytes from s; the buffer is readable (not necessarily meaningful) up to the next 8-byte
+    // boundary past s + len + 8, so whole aligned words are read and funnel-shifted
+    __device__ void putb(const uint8_t* s, uint32_t len) {
+        if (!len) return;
+        const uint32_t mis = (uint32_t)((uintptr_t)s & 7);
+        const uint64_t* w = (const uint64_t*)(s - mis);
+        uint64_t lo = __ldg(w);
+        for (uint32_t i = 0; i < len; i += 8) {
+            const uint64_t hi = __ldg(++w);
+            const uint64_t v = mis ? (lo >> (8 * mis)) | (hi << (8 * (8 - mis))) : lo;
+            putw(v, len - i < 8 ? len - i : 8);
+            lo = hi;
         }
-        uint32_t y = (uint32_t)x;
-        do { d[k++] = (char)('0' + y % 10u); y /= 10u; } while (y);
-        while (k) put((uint8_t)d[--k]);
+    }
+    // the 8 low decimal digits of r (< 1e8), zero-padded, most significant digit in the low byte
+    static __device__ __forceinline__ uint64_t dig8(uint32_t r) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) { w = (w << 8) | (uint64_t)('0' + r % 10u); r /= 10u; }
+        return w;
+    }
+    __device__ __forceinline__ void putu_head(uint32_t r) {   // r < 1e8 without leading zeros
+        uint32_t k = 1;
+        for (uint32_t p = 10; k < 8 && r >= p; p *= 10) k++;
+        putw(dig8(r) >> (8 * (8 - k)), k);
+    }
+    __device__ void putu(uint64_t x) {   // decimal repr of a non-negative int, 8 digits per word
+        if (x < 100000000ull) { putu_head((uint32_t)x); return; }
+        const uint32_t lo = (uint32_t)(x % 100000000ull);
+        x /= 100000000ull;
+        if (x < 100000000ull) {
+            putu_head((uint32_t)x);
+        } else {
+            putu_head((uint32_t)(x / 100000000ull));
+            putw(dig8((uint32_t)(x % 100000000ull)), 8);
+        }
+        putw(dig8(lo), 8);
     }
     // int.from_bytes(digest, "big"): the digest is h[0] little-endian
     __device__ uint64_t final() {
@@ -162,14 +197,14 @@ __device__ void put_key(const Leaf& L, B2b& h, uint32_t sym) {
 __device__ void put_desc(const Leaf& L, B2b& h, const unsigned long long* lab, uint32_t x) {
     h.put('(');
     put_key(L, h, L.nsym[x]);
-    h.puts(", (");
+    h.putw(0x28202cull, 3);   // ", ("
     const uint32_t q = L.nko[x], ar = L.nko[x + 1] - q;
     for (uint32_t i = 0; i < ar; i++) {
-        if (i) h.puts(", ");
+        if (i) h.putw(0x202cull, 2);   // ", "
         h.putu(lab[L.kpos[q + i]]);
     }
     if (ar == 1) h.put(',');
-    h.puts("))");
+    h.putw(0x2929ull, 2);   // "))"
 }
 
 __device__ bool class_less(const Leaf& L, const unsigned long long* lab, const uint32_t* nord, uint32_t a, uint32_t b) {
@@ -215,7 +250,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         h.init();
         h.put('[');
         for (uint32_t i = 0; i < nn; i++) {
-            if (i) h.puts(", ");
+            if (i) h.putw(0x202cull, 2);   // ", "
             put_key(L, h, L.nsym[ord[i]]);
         }
         h.put(']');
@@ -245,7 +280,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
             h.init();
             h.put('[');
             for (uint32_t i = 0; i < nn; i++) {
-                if (i) h.puts(", ");
+                if (i) h.putw(0x202cull, 2);   // ", "
                 put_desc(L, h, lc, ord[i]);
             }
             h.put(']');
@@ -314,10 +349,10 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         h.put('[');
         for (uint32_t i = 0; i < C; i++) {
             const uint32_t c = cord[i];
-            if (i) h.puts(", ");
+            if (i) h.putw(0x202cull, 2);   // ", "
             h.put('[');
             for (uint32_t q = L.coff[c]; q < L.coff[c + 1]; q++) {
-                if (q != L.coff[c]) h.puts(", ");
+                if (q != L.coff[c]) h.putw(0x202cull, 2);   // ", "
                 put_desc(L, h, lf, nord[q]);
             }
             h.put(']');
@@ -325,7 +360,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         h.put(']');
         h.put(0x1f);
         const uint32_t rp = d.v_root[l];
-        if (rp == NONE) h.puts("None");
+        if (rp == NONE) h.putw(0x656e6f4eull, 4);   // "None"
         else h.putu(lf[rp]);
         h.put(0x1f);
         a.fp[l] = h.final();
