@@ -28,10 +28,17 @@ __device__ __forceinline__ uint64_t rotr(uint64_t x, int n) { return (x >> n) | 
 
 struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(digest_size=8))
     uint64_t h[8];
-    uint64_t m[16];   // message block as little-endian words
-    uint64_t t;       // bytes compressed so far
+    // two message blocks as little-endian words: the block being filled (at word `cur`) and at most
+    // one full block whose compression is deferred to the caller's next flush() -- lanes of a warp
+    // hashing different classes then compress together at the same program point instead of each
+    // at its own byte position (SIMT efficiency of the dominant compression)
+    uint64_t m[32];
+    uint64_t t;       // bytes in the stream up to the end of the last full block
+    uint64_t tp;      // counter of the pending block
     uint64_t acc;     // bytes of the word being filled
     uint32_t n;       // bytes in the current block (including acc)
+    uint32_t cur;     // 0 or 16: first word of the block being filled
+    bool pend;        // the other block is full and not yet compressed
 
     __device__ void init() {
         for (int i = 0; i < 8; i++) h[i] = B2B_IV[i];
@@ -39,18 +46,20 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
         t = 0;
         n = 0;
         acc = 0;
+        cur = 0;
+        pend = false;
     }
-    __device__ __noinline__ void compress(bool last) {
+    __device__ __noinline__ void compress(uint32_t base, uint64_t tt, bool last) {
         // the 12 rounds written out with the BLAKE2b sigma schedule as literals: the message words
         // are read once into registers and every schedule index is a register name (m itself stays
         // addressable for put); one out-of-line copy keeps the kernel's code small
         uint64_t mm[16];
 #pragma unroll
-        for (int i = 0; i < 16; i++) mm[i] = m[i];
+        for (int i = 0; i < 16; i++) mm[i] = m[base + i];
         uint64_t v[16];
 #pragma unroll
         for (int i = 0; i < 8; i++) { v[i] = h[i]; v[i + 8] = B2B_IV[i]; }
-        v[12] ^= t;
+        v[12] ^= tt;
         if (last) v[14] = ~v[14];
 #define B2G(a, b, c, d, x, y)                         \
     v[a] = v[a] + v[b] + x; v[d] = rotr(v[d] ^ v[a], 32); \
@@ -85,14 +94,17 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
         while (k) {
             if (n == 128) {   // a full block is compressed only once more data follows (BLAKE2b rule)
                 t += 128;
-                compress(false);
+                if (pend) compress(cur ^ 16, tp, false);   // blocks compress in stream order
+                pend = true;
+                tp = t;
+                cur ^= 16;
                 n = 0;
             }
             const uint32_t room = 128 - n, take = k < room ? k : room, sh = n & 7;
             const uint64_t part = take == 8 ? v : (v & ((1ull << (8 * take)) - 1));
             acc |= part << (8 * sh);
             if (sh + take >= 8) {
-                m[n >> 3] = acc;
+                m[cur + (n >> 3)] = acc;
                 acc = sh ? part >> (8 * (8 - sh)) : 0;
             }
             n += take;
@@ -140,11 +152,19 @@ struct B2b {   // streaming BLAKE2b with an 8-byte digest (hashlib.blake2b(diges
         putw(dig8(lo), 8);
     }
     // int.from_bytes(digest, "big"): the digest is h[0] little-endian
+    // compresses the deferred full block, if any; call where the lanes of a warp are converged
+    __device__ __forceinline__ void flush() {
+        if (pend) {
+            compress(cur ^ 16, tp, false);
+            pend = false;
+        }
+    }
     __device__ uint64_t final() {
+        flush();
         t += n;
-        if (n & 7) m[n >> 3] = acc;
-        for (uint32_t w = (n + 7) >> 3; w < 16; w++) m[w] = 0;
-        compress(true);
+        if (n & 7) m[cur + (n >> 3)] = acc;
+        for (uint32_t w = (n + 7) >> 3; w < 16; w++) m[cur + w] = 0;
+        compress(cur, t, true);
         return __byte_perm((uint32_t)(h[0] >> 32), 0, 0x0123) | ((uint64_t)__byte_perm((uint32_t)h[0], 0, 0x0123) << 32);
     }
 };
@@ -252,6 +272,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
         for (uint32_t i = 0; i < nn; i++) {
             if (i) h.putw(0x202cull, 2);   // ", "
             put_key(L, h, L.nsym[ord[i]]);
+            h.flush();
         }
         h.put(']');
         h.put(0x1f);
@@ -282,6 +303,7 @@ __global__ void __launch_bounds__(T) k_fingerprint(Dev d, FArgs a) {
             for (uint32_t i = 0; i < nn; i++) {
                 if (i) h.putw(0x202cull, 2);   // ", "
                 put_desc(L, h, lc, ord[i]);
+                h.flush();
             }
             h.put(']');
             h.put(0x1f);
