@@ -135,6 +135,7 @@ struct esat_batch {
     uint32_t *f_rep0 = nullptr, *f_rep1 = nullptr, *f_nord = nullptr, *f_tval = nullptr, *f_cord = nullptr,
              *f_status = nullptr;
     uint8_t* f_lchg = nullptr;
+    unsigned long long *f_dec0 = nullptr, *f_dec1 = nullptr;
 };
 
 namespace {
@@ -1121,12 +1122,12 @@ int esat_fingerprint(esat_batch* b) {
     cudaSetDevice(c->device);
     if (!b->f_lab0) {
         const uint64_t N = b->N, T = b->T, L = b->L;
-        OWN(b->f_lab0, N); OWN(b->f_lab1, N); OWN(b->f_rep0, N); OWN(b->f_rep1, N); OWN(b->f_nord, N); OWN(b->f_lchg, N);
+        OWN(b->f_lab0, N); OWN(b->f_lab1, N); OWN(b->f_rep0, N); OWN(b->f_rep1, N); OWN(b->f_nord, N); OWN(b->f_lchg, N); OWN(b->f_dec0, 4 * N); OWN(b->f_dec1, 4 * N);
         OWN(b->f_tkey, T); OWN(b->f_tval, T); OWN(b->f_cord, T); OWN(b->f_fp, L); OWN(b->f_status, L);
     }
     FArgs a{};
     a.krank = c->f_krank; a.key_off = c->f_koff; a.key_bytes = c->f_kbytes;
-    a.lab0 = b->f_lab0; a.lab1 = b->f_lab1; a.rep0 = b->f_rep0; a.rep1 = b->f_rep1; a.nord = b->f_nord; a.lchg = b->f_lchg;
+    a.lab0 = b->f_lab0; a.lab1 = b->f_lab1; a.rep0 = b->f_rep0; a.rep1 = b->f_rep1; a.nord = b->f_nord; a.lchg = b->f_lchg; a.dec0 = b->f_dec0; a.dec1 = b->f_dec1;
     a.tkey = b->f_tkey; a.tval = b->f_tval; a.cord = b->f_cord; a.fp = b->f_fp; a.status = b->f_status;
     tic(c);
     if (b->L) k_fingerprint<128><<<b->L, 128, 0, c->stream>>>(b->d, a);

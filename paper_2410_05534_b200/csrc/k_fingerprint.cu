@@ -214,14 +214,53 @@ __device__ void put_key(const Leaf& L, B2b& h, uint32_t sym) {
 }
 
 // repr((symbol.key(), (label, ...)))
-__device__ void put_desc(const Leaf& L, B2b& h, const unsigned long long* lab, uint32_t x) {
+// decimal repr of x as bytes in o[0..2] (first character in the low byte) and its length in o[3]; a
+// label is printed once per parent reference but converted once per round
+__device__ void store_dec(uint64_t x, unsigned long long* o) {
+    uint64_t w[3] = {0, 0, 0};
+    uint32_t n = 0;
+    auto add = [&](uint64_t v, uint32_t k) {   // k <= 8 bytes, n + k <= 20
+        const uint32_t sh = n & 7;
+        const uint64_t lo = v << (8 * sh), hi = sh ? v >> (8 * (8 - sh)) : 0;
+        if (n < 8) { w[0] |= lo; w[1] |= hi; } else if (n < 16) { w[1] |= lo; w[2] |= hi; } else { w[2] |= lo; }
+        n += k;
+    };
+    auto head = [&](uint32_t r) {
+        uint32_t k = 1;
+        for (uint32_t p = 10; k < 8 && r >= p; p *= 10) k++;
+        add(B2b::dig8(r) >> (8 * (8 - k)), k);
+    };
+    if (x < 100000000ull) {
+        head((uint32_t)x);
+    } else {
+        const uint32_t lo = (uint32_t)(x % 100000000ull);
+        x /= 100000000ull;
+        if (x < 100000000ull) {
+            head((uint32_t)x);
+        } else {
+            head((uint32_t)(x / 100000000ull));
+            add(B2b::dig8((uint32_t)(x % 100000000ull)), 8);
+        }
+        add(B2b::dig8(lo), 8);
+    }
+    o[0] = w[0]; o[1] = w[1]; o[2] = w[2]; o[3] = n;
+}
+
+__device__ __forceinline__ void put_dec(B2b& h, const unsigned long long* o) {
+    const uint32_t len = (uint32_t)o[3];
+    h.putw(o[0], len < 8 ? len : 8);
+    if (len > 8) h.putw(o[1], len < 16 ? len - 8 : 8);
+    if (len > 16) h.putw(o[2], len - 16);
+}
+
+__device__ void put_desc(const Leaf& L, B2b& h, const unsigned long long* dec, uint32_t x) {
     h.put('(');
     put_key(L, h, L.nsym[x]);
     h.putw(0x28202cull, 3);   // ", ("
     const uint32_t q = L.nko[x], ar = L.nko[x + 1] - q;
     for (uint32_t i = 0; i < ar; i++) {
         if (i) h.putw(0x202cull, 2);   // ", "
-        h.putu(lab[L.kpos[q + i]]);
+        put_dec(h, dec + 4ull * L.kpos[q + i]);
     }
     if (ar == 1) h.put(',');
     h.putw(0x2929ull, 2);   // "))"
@@ -256,6 +295,7 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
     uint32_t* rep[2] = {a.rep0 + b, a.rep1 + b};
     uint32_t* nord = a.nord + b;
     uint8_t* lchg = a.lchg + b;
+    unsigned long long* dec[2] = {a.dec0 + 4 * b, a.dec1 + 4 * b};
     const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
     unsigned long long* tkey = a.tkey + t0;
     uint32_t* tval = a.tval + t0;
@@ -277,6 +317,7 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
         h.put(']');
         h.put(0x1f);
         lab[0][c] = h.final();
+        store_dec(lab[0][c], dec[0] + 4ull * c);
         rep[0][c] = NONE;
     }
     __syncthreads();
@@ -293,7 +334,11 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
                 for (uint32_t nd = L.coff[c]; nd < L.coff[c + 1] && !dirty; nd++)
                     for (uint32_t q = L.nko[nd]; q < L.nko[nd + 1]; q++)
                         if (lchg[L.kpos[q]]) { dirty = true; break; }
-                if (!dirty) { ln[c] = lc[c]; continue; }
+                if (!dirty) {
+                    ln[c] = lc[c];
+                    for (int w = 0; w < 4; w++) dec[cur ^ 1][4ull * c + w] = dec[cur][4ull * c + w];
+                    continue;
+                }
             }
             uint32_t* ord = nord + L.coff[c];
             const uint32_t nn = sorted_nodes(L, lc, c, ord, true);
@@ -302,12 +347,13 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
             h.put('[');
             for (uint32_t i = 0; i < nn; i++) {
                 if (i) h.putw(0x202cull, 2);   // ", "
-                put_desc(L, h, lc, ord[i]);
+                put_desc(L, h, dec[cur], ord[i]);
                 h.flush();
             }
             h.put(']');
             h.put(0x1f);
             ln[c] = h.final();
+            store_dec(ln[c], dec[cur ^ 1] + 4ull * c);
         }
         for (uint32_t s = tid; s < tsz; s += T) { tkey[s] = ~0ull; tval[s] = NONE; }
         if (tid == 0) sh_changed = 0;
@@ -375,7 +421,7 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
             h.put('[');
             for (uint32_t q = L.coff[c]; q < L.coff[c + 1]; q++) {
                 if (q != L.coff[c]) h.putw(0x202cull, 2);   // ", "
-                put_desc(L, h, lf, nord[q]);
+                put_desc(L, h, dec[cur], nord[q]);
             }
             h.put(']');
         }

@@ -14,6 +14,7 @@ struct FArgs {
     uint32_t *rep0, *rep1;       // [node rows] partition representative (double buffer)
     uint32_t* nord;              // [node rows] nodes of each class in description order
     uint8_t* lchg;               // [node rows] class label changed in the last round
+    unsigned long long *dec0, *dec1;   // [4 x node rows] decimal repr of each label (3 words + length; double buffer)
     unsigned long long* tkey;    // [table rows] label -> smallest class position
     uint32_t *tval, *cord;       // [table rows]
     unsigned long long* fp;      // [L]
