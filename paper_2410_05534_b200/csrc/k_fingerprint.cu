@@ -299,8 +299,8 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
     const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
     unsigned long long* tkey = a.tkey + t0;
     uint32_t* tval = a.tval + t0;
-    __shared__ uint32_t sh_bad, sh_changed;
-    if (tid == 0) sh_bad = 0;
+    __shared__ uint32_t sh_bad, sh_changed, sh_next;
+    if (tid == 0) { sh_bad = 0; sh_next = T; }
     __syncthreads();
     // round 0: labels from the sorted symbol keys
     for (uint32_t c = tid; c < C; c += T) {
@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
     for (uint32_t it = 0; it < rounds && !sh_bad; it++) {
         const unsigned long long* lc = lab[cur];
         unsigned long long* ln = lab[cur ^ 1];
-        for (uint32_t c = tid; c < C; c += T) {
+        // classes handed out dynamically, so a few big ones no longer stall the end-of-round barrier
+        for (uint32_t c = tid; c < C; c = atomicAdd(&sh_next, 1u)) {
             // From the second refinement on, a class none of whose children changed label in the last
             // round hashes exactly the bytes it hashed then, so its label carries over.
             if (it > 0) {
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
         __syncthreads();
         cur ^= 1;
         const bool stop = !sh_changed;
+        if (tid == 0) sh_next = T;
         __syncthreads();
         if (stop) break;
     }
