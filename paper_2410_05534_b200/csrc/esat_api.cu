@@ -1130,7 +1130,7 @@ int esat_fingerprint(esat_batch* b) {
     a.lab0 = b->f_lab0; a.lab1 = b->f_lab1; a.rep0 = b->f_rep0; a.rep1 = b->f_rep1; a.nord = b->f_nord; a.lchg = b->f_lchg; a.dec0 = b->f_dec0; a.dec1 = b->f_dec1;
     a.tkey = b->f_tkey; a.tval = b->f_tval; a.cord = b->f_cord; a.fp = b->f_fp; a.status = b->f_status;
     tic(c);
-    if (b->L) k_fingerprint<128><<<b->L, 128, 0, c->stream>>>(b->d, a);
+    if (b->L) k_fingerprint<256><<<b->L, 256, 0, c->stream>>>(b->d, a);
     toc(c);
     return launch_check(c, "k_fingerprint");
 }

@@ -280,7 +280,7 @@ __device__ bool class_less(const Leaf& L, const unsigned long long* lab, const u
 }  // namespace
 
 template <int T>
-__global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
+__global__ void __launch_bounds__(T, 1024 / T) k_fingerprint(Dev d, FArgs a) {
     const uint32_t l = blockIdx.x, tid = threadIdx.x;
     const uint64_t b = d.nb[l], t0 = d.tb[l];
     Leaf L;
@@ -438,6 +438,6 @@ __global__ void __launch_bounds__(T, 8) k_fingerprint(Dev d, FArgs a) {
     }
 }
 
-template __global__ void k_fingerprint<128>(Dev, FArgs);
+template __global__ void k_fingerprint<256>(Dev, FArgs);
 
 }  // namespace esat
