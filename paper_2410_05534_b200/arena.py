@@ -210,3 +210,29 @@ def unpack_state(packed: dict, state: dict, l: int) -> LeafState:
                      state["hc_cid"][n0:n0 + n].copy(), state["hc_cost"][n0:n0 + n].copy(),
                      state["uf_parent"][u0:u0 + U].copy(), state["uf_rank"][u0:u0 + U].copy(),
                      int(packed["root"][l]))
+
+
+def to_egraph(state: LeafState, symtab, language=None):
+    """Host ``EGraph`` (ours) of a rebuilt leaf: the hashcons in the leaf's order, union-find
+    arrays and classes regrouped from the hashcons (egraph.py:228-238) -- the inverse of
+    export_state for clean states."""
+    from collections import defaultdict
+
+    from .egraph import EClass, EGraph, ENode
+
+    eg = EGraph(language)
+    ko = state.hc_koff
+    nodes = [ENode(symtab.symbols[int(state.hc_sym[i])], tuple(int(k) for k in state.hc_kids[ko[i]:ko[i + 1]]))
+             for i in range(state.n)]
+    eg.hashcons = {nodes[i]: int(state.hc_cid[i]) for i in range(state.n)}
+    eg._uf.parent = [int(x) for x in state.uf_parent]
+    eg._uf.rank = [int(x) for x in state.uf_rank]
+    groups, parents = defaultdict(set), defaultdict(set)
+    for node, c in eg.hashcons.items():
+        c = eg.find(c)
+        groups[c].add(node)
+        for ch in set(node.children):
+            parents[eg.find(ch)].add((node, c))
+    eg.classes = {c: EClass(c, groups[c], parents.get(c, set())) for c in sorted(groups)}
+    eg.root = None if state.root == NONE else int(state.root)
+    return eg

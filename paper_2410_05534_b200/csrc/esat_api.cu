@@ -28,6 +28,9 @@ struct esat_ctx {
     cudaEvent_t ev_fork = nullptr, ev_done = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
     bool side_timed = false, side_pending = false, fork_armed = false;
     bool timed = false;
+    // max-dynamic-SMEM attributes are per device: tracked per context (one context per device)
+    uint32_t ematch_attr = 0;
+    bool join_attr = false;
     char err[512] = {0};
     // symbol table
     uint32_t n_syms = 0;
@@ -374,8 +377,7 @@ int esat_rebuild(esat_batch* b) {
 int esat_batch_set_pool(esat_batch* b, double entries_per_node) {
     if (!b || !(entries_per_node > 0)) return ESAT_E_ARG;
     b->pool_factor = entries_per_node;
-    b->pool_kfactor = 0.0;
-    b->pool_total = 0;  // force re-allocation on the next OCF extraction
+    b->pool_kfactor = 0.0;   // the layout is recomputed at the next OCF extraction
     return ESAT_OK;
 }
 
@@ -384,34 +386,57 @@ int esat_batch_set_pool2(esat_batch* b, double values_per_node, double bitsets_p
     if (b->pool_factor != values_per_node || b->pool_kfactor != bitsets_per_node) {
         b->pool_factor = values_per_node;
         b->pool_kfactor = bitsets_per_node;
-        b->pool_total = 0;
     }
     return ESAT_OK;
 }
 
+// OCF history pools, laid out per leaf from the live e-node count of the last rebuild (a headroom
+// arena's span is far larger than its leaf) and grown, never shrunk, when a layout needs more.
+// pool_total / pool_ktotal are the allocated capacities: set only after every allocation and copy
+// succeeded, so a failed growth (out of memory) leaves the batch re-allocating on the next call.
 static int ensure_pool(esat_batch* b) {
     esat_ctx* c = b->ctx;
-    if (b->pool_total) return ESAT_OK;
-    b->pb.assign(b->L + 1, 0);
-    b->pbk.assign(b->L + 1, 0);
+    const uint32_t L = b->L;
+    std::vector<uint32_t> live(L);
+    if (b->counts && L) {
+        CK(c, cudaMemcpyAsync(live.data(), b->d.o_n, 4ull * L, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    } else {
+        for (uint32_t l = 0; l < L; l++) live[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]);
+    }
+    std::vector<uint64_t> pb(L + 1, 0), pbk(L + 1, 0);
     const double kf = b->pool_kfactor > 0 ? b->pool_kfactor
                                           : (b->pool_factor / 8.0 > 3.0 ? b->pool_factor / 8.0 : 3.0);
-    for (uint32_t l = 0; l < b->L; l++) {
-        const uint64_t n = b->nb[l + 1] - b->nb[l];
+    for (uint32_t l = 0; l < L; l++) {
+        const uint64_t n = live[l];
         const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)
-        b->pb[l + 1] = b->pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
-        b->pbk[l + 1] = b->pbk[l] + (uint64_t)(kf * (double)n) * 4 * nw + 16 * nw + 64;   // bits|wptr|wmax
+        pb[l + 1] = pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
+        pbk[l + 1] = pbk[l] + (uint64_t)(kf * (double)n) * 4 * nw + 16 * nw + 64;   // bits|wptr|wmax
     }
-    b->pool_total = b->pb[b->L];
-    b->pool_ktotal = b->pbk[b->L];
-    cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
-    b->d_pb = nullptr; b->d_pbk = nullptr; b->pool_key = nullptr; b->pool_val = nullptr;
-    CK(c, cudaMalloc((void**)&b->d_pb, 8ull * (b->L + 1)));
-    CK(c, cudaMalloc((void**)&b->d_pbk, 8ull * (b->L + 1)));
-    CK(c, cudaMemcpy(b->d_pb, b->pb.data(), 8ull * (b->L + 1), cudaMemcpyHostToDevice));
-    CK(c, cudaMemcpy(b->d_pbk, b->pbk.data(), 8ull * (b->L + 1), cudaMemcpyHostToDevice));
-    CK(c, cudaMalloc((void**)&b->pool_key, 4ull * b->pool_ktotal + 64));
-    CK(c, cudaMalloc((void**)&b->pool_val, 8ull * b->pool_total + 64));
+    if (b->d_pb && pb == b->pb && pbk == b->pbk && b->pool_total >= pb[L] && b->pool_ktotal >= pbk[L])
+        return ESAT_OK;
+    if (!b->d_pb) {
+        CK(c, cudaMalloc((void**)&b->d_pb, 8ull * (L + 1)));
+        CK(c, cudaMalloc((void**)&b->d_pbk, 8ull * (L + 1)));
+    }
+    if (b->pool_total < pb[L] || b->pool_ktotal < pbk[L]) {
+        const uint64_t want = pb[L] > b->pool_total ? pb[L] : b->pool_total;
+        const uint64_t kwant = pbk[L] > b->pool_ktotal ? pbk[L] : b->pool_ktotal;
+        CK(c, cudaStreamSynchronize(c->stream));
+        if (c->side) CK(c, cudaStreamSynchronize(c->side));
+        cudaFree(b->pool_key); cudaFree(b->pool_val);
+        b->pool_key = nullptr; b->pool_val = nullptr;
+        b->pool_total = 0; b->pool_ktotal = 0;
+        CK(c, cudaMalloc((void**)&b->pool_key, 4ull * kwant + 64));
+        CK(c, cudaMalloc((void**)&b->pool_val, 8ull * want + 64));
+        b->pool_total = want;
+        b->pool_ktotal = kwant;
+    }
+    b->pb = pb;
+    b->pbk = pbk;
+    CK(c, cudaMemcpyAsync(b->d_pb, b->pb.data(), 8ull * (L + 1), cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(b->d_pbk, b->pbk.data(), 8ull * (L + 1), cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));   // pb / pbk are host vectors that a later call rewrites
     return ESAT_OK;
 }
 
@@ -629,11 +654,10 @@ static int ematch_launch(esat_batch* b) {
     d.sym_par = c->sym_par; d.n_syms = c->n_syms;
     a.smem_bytes = b->m_smem;
     a.no_flat = getenv("ESAT_EMATCH_GENERIC") ? 1 : 0;
-    static uint32_t attr_set = 0;
     const uint32_t cap_bytes = 100 * 1024;
-    if (a.smem_bytes > attr_set) {
+    if (a.smem_bytes > c->ematch_attr) {
         CK(c, cudaFuncSetAttribute(k_ematch<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_bytes));
-        attr_set = cap_bytes;
+        c->ematch_attr = cap_bytes;
     }
     tic(c);
     if (L && P) k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, a);
@@ -801,11 +825,10 @@ static int join_launch(esat_batch* b) {
     a.id_base = b->d.ub;
     a.run_cap = run_cap;
     a.s1_cap = JOIN_SMEM_S1;
-    static bool join_attr = false;
-    if (!join_attr) {
+    if (!c->join_attr) {
         CK(c, cudaFuncSetAttribute(k_join<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    4 * (16384 + JOIN_SMEM_S1)));
-        join_attr = true;
+        c->join_attr = true;
     }
     tic(c);
     if (L && R)

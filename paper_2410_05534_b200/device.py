@@ -54,10 +54,10 @@ def session() -> Session:
 
 
 class _Resident:
-    __slots__ = ("version", "batch", "view", "packed", "costs_key")
+    __slots__ = ("version", "batch", "view", "packed")
 
-    def __init__(self, version, batch, view, packed, costs_key=None):
-        self.version, self.batch, self.view, self.packed, self.costs_key = version, batch, view, packed, costs_key
+    def __init__(self, version, batch, view, packed):
+        self.version, self.batch, self.view, self.packed = version, batch, view, packed
 
 
 def _node_class(eg):
@@ -128,12 +128,14 @@ def _resident(eg, costs=None):
     if eg.dirty:
         return None
     r = getattr(eg, "_esat_resident", None)
-    key = None if costs is None else id(costs)
-    if r is not None and r.version == eg._version and (costs is None or r.costs_key == key):
+    # the resident view is reused only for cost-free calls (matching); every extraction re-exports
+    # the node costs from the dict it is given -- a dict's identity says nothing about its content
+    # (ids are recycled, dicts are edited in place), and the costs are one f64 per e-node
+    if r is not None and r.version == eg._version and costs is None:
         session().sync_symtab()
         return r
     b, packed = _upload(eg, costs)
-    r = _Resident(eg._version, b, b.download_view(), packed, key)
+    r = _Resident(eg._version, b, b.download_view(), packed)
     eg._esat_resident = r
     return r
 

@@ -1,23 +1,41 @@
 """Batched MCTS over rewrite-rule applications (§4.1).
 
-The search tree lives on the host; every e-graph operation of an iteration batch runs on the
-device: expansion applies the sampled rule to a snapshot of the selected node (k_apply, then
-k_rebuild), blacklists come from per-source e-matching of the child (is_rule_applicable,
-rewrite.py:579-589: a rule is inapplicable as soon as one source has no match), and the
-simulations are device-resident random rollouts -- apply, rebuild, extract after every step,
-reward Eq. 3 ``r = sum max(cost_{i-1} - cost_i, 0)`` anchored at the child's own extracted cost.
+The search tree lives on the host; every e-graph operation of an iteration batch is delegated to
+an *engine* with four calls (``initial`` / ``evaluate`` / ``expand`` / ``simulate``, plus ``final``
+for the run's last extraction). ``DeviceEngine`` runs them on the B200: expansion applies the
+sampled rule to a snapshot of the selected node (k_apply, then k_rebuild), blacklists come from
+per-source e-matching of the child (is_rule_applicable, rewrite.py:579-589: a rule is
+inapplicable as soon as one source has no match), and the simulations are device-resident random
+rollouts -- apply, rebuild, extract after every step, reward Eq. 3 ``r = sum max(cost_{i-1} -
+cost_i, 0)`` anchored at the child's own extracted cost. The test-only CPU engine
+(oracle/mcts_ref.py) runs the same four calls on the reference's own EGraph / apply_rule /
+extractors, so ``optimize_mcts`` with either engine must produce the identical RunReport.
 
 SPEC's concurrency model allows simulations of distinct iterations to run in parallel on
 snapshots with the results applied to the tree serially: ``batch`` selections are
 made sequentially (a node/rule pair is reserved so one batch never expands it twice), the batch's
-expansions and simulations run as one device batch, and the updates are applied in selection
+expansions and simulations run as one engine batch, and the updates are applied in selection
 order. ``batch=1`` is the strictly sequential search.
+
+Engine contract (what both engines implement, state objects are engine-private):
+
+    initial(egraph)                     -> state
+    evaluate(states)                    -> (clean states, cost f64[L], nodes[L], classes[L], app bool[L,R])
+    expand(states, rules)               -> (child states, changed[L], cost, nodes, classes, app)
+    simulate(states, cost0, allowed, steps, node_limit, rng) -> reward f64[L]
+    final(state, method)                -> (cost, save_graph JSON text)
+
+A failed extraction yields cost ``inf``. In a rollout a step whose extraction failed adds no reward
+and leaves the anchor unchanged ("treat that step's improvement as 0"); a step right
+after a failed anchor only re-anchors.
 """
 
 from __future__ import annotations
 
 import math
 import random
+import time
+from collections import Counter
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -39,13 +57,14 @@ class MctsConfig:
     node_limit: int = 2000
     seed: int = 0
     main_extractor: str = "ocf"
+    final_extractor: str = "ocf"
     batch: int = 32
     headroom: int = 4096
 
 
 @dataclass
 class SearchNode:
-    state: LeafState
+    state: object
     cost: float
     n_nodes: int
     v: float = 0.0
@@ -56,6 +75,40 @@ class SearchNode:
     parent: "SearchNode | None" = None
     rule: int | None = None
     pending: set = field(default_factory=set)
+    exhausted: bool = False   # no rule left to expand anywhere below (selection prunes it)
+
+
+@dataclass
+class RunReport:
+    """SPEC.md:685-697 RunReport: costs, speedup, per-iteration rows (rule id, e-nodes, e-classes,
+    main-extractor cost) and the rule histogram; ``final_program`` is the optimized program as the
+    exact text ``save_graph`` writes (tensor_ir.py:487-504)."""
+
+    original_cost: float
+    optimized_cost: float
+    speedup_pct: float
+    wall_time_s: float
+    iterations: list
+    rule_histogram: dict
+    final_program: str | None
+    final_extractor: str = "ocf"
+
+    @property
+    def trace(self) -> list:
+        return [it[0] for it in self.iterations]
+
+    def to_json_dict(self) -> dict:
+        hexf = lambda x: float(x).hex()  # noqa: E731
+        return {"original_cost": hexf(self.original_cost), "optimized_cost": hexf(self.optimized_cost),
+                "speedup_pct": hexf(self.speedup_pct), "final_extractor": self.final_extractor,
+                "iterations": [[r, n, c, hexf(x)] for r, n, c, x in self.iterations],
+                "rule_histogram": {str(k): v for k, v in sorted(self.rule_histogram.items())},
+                "final_program": self.final_program}
+
+
+def speedup_pct(orig: float, opt: float) -> float:
+    """(orig - opt) / orig * 100 (SPEC.md:687)."""
+    return (orig - opt) / orig * 100.0 if orig else 0.0
 
 
 def ucb1(v: float, n: int, N: int, c: float) -> float:
@@ -84,6 +137,16 @@ def best_child(root: SearchNode):
     return best
 
 
+def rollout_rewards(reward, prev, live, cost) -> None:
+    """One rollout step's Eq. 3 update, in place (shared by every engine): a finite extraction
+    adds max(prev - cost, 0) when the anchor is finite and becomes the anchor; a failed one adds
+    nothing and keeps the anchor."""
+    good = live & np.isfinite(cost)
+    add = good & np.isfinite(prev)
+    reward[add] += np.maximum(prev[add] - cost[add], 0.0)
+    prev[good] = cost[good]
+
+
 class DeviceEngine:
     """Batched e-graph operations of the search on the device (one LeafPipeline per batch)."""
 
@@ -91,9 +154,11 @@ class DeviceEngine:
         self.ctx = ctx or native.Context(0)
         self.rules, self.symtab, self.language, self.cfg = rules, symtab, language, cost_config
         self.method, self.headroom = method, headroom
+        self.regrows = 0
 
-    def _open(self, states):
-        packed = Batch(states).pack_with_headroom(nodes=self.headroom)
+    # -- batch plumbing ---------------------------------------------------------------
+    def _open(self, states, headroom=None):
+        packed = Batch(states).pack_with_headroom(nodes=headroom or self.headroom)
         self.symtab.finalize()
         pipe = LeafPipeline(self.ctx, self.symtab.arrays(), self.rules,
                             lambda nm: self.symtab.name_id(nm, create=False), self.symtab.code, method=self.method,
@@ -101,17 +166,20 @@ class DeviceEngine:
         b = pipe.load(packed)
         b.set_counts(packed["n_cnt"], packed["u_cnt"])
         drv = ApplyDriver(pipe, self.symtab, self.language, self.cfg)
-        return packed, pipe, b, drv
+        return [packed, pipe, b, drv, headroom or self.headroom]
 
-    def _extract(self, pipe, b):
-        out = native.extract_with_retry(b, self.method, factor=32)
+    def _extract(self, b, method=None):
+        out = native.extract_with_retry(b, method or self.method, factor=32)
         cost = out["root_cost"].copy()
         cost[out["status"] != 0] = np.inf
-        return cost
+        return cost, out
 
-    def _clean_states(self, packed, b):
+    def _clean_states(self, packed, b, U=None):
+        """Every leaf's last rebuild as a LeafState (a snapshot, egraph.py:300-312). ``U`` are the
+        union-find id counts of that rebuild (default: the batch's live counts)."""
         reb = b.download_rebuild()
-        U = b.download_state()["U"]
+        if U is None:
+            U = b.live_counts()[1]
         out = []
         for l in range(packed["n_leaves"]):
             n0, k0, u0 = (int(packed[k][l]) for k in ("node_base", "kid_base", "id_base"))
@@ -121,11 +189,11 @@ class DeviceEngine:
                                  reb["hc_cid"][n0:n0 + n].copy(), reb["hc_cost"][n0:n0 + n].copy(),
                                  reb["uf_parent"][u0:u0 + int(U[l])].copy(), reb["uf_rank"][u0:u0 + int(U[l])].copy(),
                                  int(packed["root"][l])))
-        return out, reb["n"].copy()
+        return out
 
     def _applicable(self, pipe, b):
         """[L, R] is_rule_applicable: every source of the rule has a match (rewrite.py:579-589)."""
-        pipe.ematch()
+        pipe.match()
         cnt = {}
         for r in pipe.rules:
             for pid in r.pattern_ids:
@@ -133,40 +201,73 @@ class DeviceEngine:
                     cnt[pid] = b.download_matches(pid)[2]
         return np.stack([np.all([cnt[p] > 0 for p in r.pattern_ids], axis=0) for r in pipe.rules], axis=1)
 
+    def _apply(self, h, rules):
+        """esat_apply of rules[l] on every leaf of the rebuilt batch ``h``. A leaf that runs out of
+        arena headroom (ESAT_A_CAPACITY) leaves the rebuilt state intact on the device (k_apply
+        reads the rebuild's outputs and writes the batch input), so the whole batch is re-packed
+        from those rebuilt states with 4x the headroom and the same rules are re-applied: the
+        result is the one an unbounded arena gives."""
+        rules = np.asarray(rules, np.uint32)
+        while True:
+            packed, pipe, b, drv, head = h
+            U0 = b.live_counts()[1]
+            pipe.ematch()
+            res = drv.apply(rules)
+            st = res["status"]
+            if np.any(st == native.A_PROGRAM):
+                raise RuntimeError("k_apply: rule target program beyond device limits (ESAT_A_PROGRAM)")
+            if np.any((st != native.A_OK) & (st != native.A_CAPACITY)):
+                raise RuntimeError(f"k_apply: unexpected statuses {np.unique(st)}")
+            if not np.any(st == native.A_CAPACITY):
+                return res
+            clean = self._clean_states(packed, b, U0)
+            b.close()
+            self.regrows += 1
+            h[:] = self._open(clean, head * 4)
+            h[1].rebuild()
+
+    # -- engine contract ----------------------------------------------------------------
+    def initial(self, egraph):
+        from .arena import export_state
+
+        return export_state(egraph, self.symtab, self.cfg)
+
     def evaluate(self, states):
-        """Rebuild + extract + applicability of raw states: (clean states, costs, sizes, applicable)."""
-        packed, pipe, b, drv = self._open(states)
+        """Rebuild + extract + applicability of raw states."""
+        h = self._open(states)
+        packed, pipe, b = h[0], h[1], h[2]
         pipe.rebuild()
-        cost = self._extract(pipe, b)
-        clean, n = self._clean_states(packed, b)
+        cost, _ = self._extract(b)
+        n, c = b.rebuilt_sizes()
+        clean = self._clean_states(packed, b)
         app = self._applicable(pipe, b)
         b.close()
-        return clean, cost, n, app
+        return clean, cost, n, c, app
 
     def expand(self, states, rules):
-        """Apply rules[l] to states[l]: (child clean states, changed, costs, sizes, applicable)."""
-        packed, pipe, b, drv = self._open(states)
+        """Apply rules[l] to states[l]: (child clean states, changed, costs, sizes, classes, applicable)."""
+        h = self._open(states)
+        h[1].rebuild()
+        res = self._apply(h, rules)
+        changed = res["report"][:, 1] > 0
+        packed, pipe, b = h[0], h[1], h[2]
         pipe.rebuild()
-        pipe.ematch()
-        res = drv.apply(np.asarray(rules, np.uint32))
-        ok = res["status"] == native.A_OK
-        changed = (res["report"][:, 1] > 0) & ok
-        pipe.rebuild()
-        cost = self._extract(pipe, b)
-        clean, n = self._clean_states(packed, b)
+        cost, _ = self._extract(b)
+        n, c = b.rebuilt_sizes()
+        clean = self._clean_states(packed, b)
         app = self._applicable(pipe, b)
         b.close()
-        return clean, changed, cost, n, app
+        return clean, changed, cost, n, c, app
 
     def simulate(self, states, costs0, allowed, steps: int, node_limit: int, rng: random.Random):
         """Random rollouts: per step every live leaf applies a uniformly drawn
-        allowed rule, rebuilds and extracts; r += max(prev - cost, 0); a failed extraction adds 0."""
+        allowed rule, rebuilds and extracts (rollout_rewards); a leaf stops at the node limit."""
         L = len(states)
-        packed, pipe, b, drv = self._open(states)
+        h = self._open(states)
         reward = np.zeros(L)
         prev = np.asarray(costs0, np.float64).copy()
         live = np.ones(L, bool)
-        pipe.rebuild()
+        h[1].rebuild()
         for _ in range(steps):
             rules = np.full(L, NONE, np.uint32)
             for l in range(L):
@@ -176,38 +277,82 @@ class DeviceEngine:
                     live[l] = False
             if not live.any():
                 break
-            pipe.ematch()
-            res = drv.apply(rules)
-            live &= res["status"] == native.A_OK
-            pipe.rebuild()
-            cost = self._extract(pipe, b)
-            good = live & np.isfinite(cost)
-            reward[good] += np.maximum(prev[good] - cost[good], 0.0)
-            prev[good] = cost[good]
-            n = b.download_rebuild()["n"]
+            self._apply(h, rules)
+            h[1].rebuild()
+            cost, _ = self._extract(h[2])
+            rollout_rewards(reward, prev, live, cost)
+            n, _ = h[2].rebuilt_sizes()
             live &= n < node_limit
-        b.close()
+        h[2].close()
         return reward
 
+    def final(self, state, method: str):
+        """Final extraction of one state with ``method`` and the program it selects, as
+        save_graph text (extraction_to_graph, tensor_ir.py:316-352). Exact extraction runs the
+        host branch-and-bound seeded by the device OCF result (exact.py)."""
+        from .arena import to_egraph
+        from .extraction import ExtractionResult
+        from .tensor_ir import GraphFormatError, extraction_to_graph, graph_json
 
-def run_search(root: SearchNode, engine: DeviceEngine, n_rules: int, cfg: MctsConfig, rng: random.Random):
+        h = self._open([state], headroom=1)
+        packed, pipe, b = h[0], h[1], h[2]
+        pipe.rebuild()
+        cost, out = self._extract(b, "ocf" if method == "exact" else method)
+        clean = self._clean_states(packed, b)[0]
+        eg = to_egraph(clean, self.symtab, self.language)
+        if not np.isfinite(cost[0]):
+            b.close()
+            return float("inf"), None
+        chosen = _chosen_of(b, out, self.symtab)
+        b.close()
+        res = ExtractionResult(float(cost[0]), chosen, method)
+        if method == "exact":
+            from .cost_model import egraph_costs
+            from .exact import extract_exact
+
+            res = extract_exact(eg, egraph_costs(eg, self.cfg), seed=res)
+        if type(self.language).__name__ != "TensorLanguage":
+            return res.total_cost, None
+        try:
+            return res.total_cost, graph_json(extraction_to_graph(eg, res))
+        except GraphFormatError:
+            return res.total_cost, None
+
+
+def _chosen_of(b, out, symtab) -> dict:
+    """{class id: ENode} of leaf 0's reachable chosen nodes (extraction.py:106-115)."""
+    from .egraph import ENode
+
+    v = b.download_view()
+    C = int(v["C"][0])
+    cls_id = v["cls_id"][:C]
+    nko = v["nd_koff"]
+    chosen = {}
+    for k in np.nonzero(out["reachable"][:C])[0]:
+        j = int(out["choice"][k])
+        kids = tuple(int(cls_id[p]) for p in v["nd_kpos"][nko[j]:nko[j + 1]])
+        chosen[int(cls_id[k])] = ENode(symtab.symbols[int(v["nd_sym"][j])], kids)
+    return chosen
+
+
+def run_search(root: SearchNode, engine, n_rules: int, cfg: MctsConfig, rng: random.Random):
     """N select/expand/simulate/update iterations (Alg. 1 body), batched."""
     done = 0
     while done < cfg.budget:
         picks = []
-        while len(picks) < min(cfg.batch, cfg.budget - done) and not root.s:
+        while len(picks) < min(cfg.batch, cfg.budget - done) and not root.exhausted:
             node = root
             while True:   # selection (SPEC.md:583-591)
                 free = [r for r in range(n_rules)
                         if r not in node.b and r not in node.children and r not in node.pending]
-                kids = [ch for _, ch in sorted(node.children.items()) if not ch.s and ch.n > 0]
+                kids = [ch for _, ch in sorted(node.children.items()) if not ch.s and not ch.exhausted and ch.n > 0]
                 stop = rng.random() < cfg.stop_prob
                 if free and (stop or not kids):
                     break                      # expand here (progressive widening, SPEC.md:652)
                 if not kids:
                     if not node.pending:
-                        node.s = True          # nothing left to expand below: saturated
-                    node = None
+                        node.exhausted = True  # nothing left to expand below (not 'saturated': the
+                    node = None                # node still changed its parent's e-graph)
                     break
                 N = max(node.n, 1)
                 node = max(kids, key=lambda ch: ucb1(ch.v, ch.n, N, cfg.c))
@@ -219,7 +364,7 @@ def run_search(root: SearchNode, engine: DeviceEngine, n_rules: int, cfg: MctsCo
             picks.append((node, rule))
         if not picks:
             break
-        kids, changed, cost, n, app = engine.expand([p.state for p, _ in picks], [r for _, r in picks])
+        kids, changed, cost, n, _, app = engine.expand([p.state for p, _ in picks], [r for _, r in picks])
         sims, anchors, allowed = [], [], []
         for j, (node, rule) in enumerate(picks):
             node.pending.discard(rule)
@@ -246,29 +391,32 @@ def run_search(root: SearchNode, engine: DeviceEngine, n_rules: int, cfg: MctsCo
     return best_child(root)
 
 
-def optimize_mcts(egraph, rules, cfg: MctsConfig, cost_config, symtab=None, engine=None):
+def optimize_mcts(egraph, rules, cfg: MctsConfig, cost_config, symtab=None, engine=None) -> RunReport:
     """Alg. 1: search, apply the best rule to the root, repeat until saturation or
-    the node limit; returns (initial cost, final cost, applied rule ids)."""
-    from .arena import export_state
+    the node limit (checked before each search and after each application); final extraction with
+    ``cfg.final_extractor``. The RNG is one stream seeded by ``cfg.seed``."""
     from .symtab import SymbolTable
 
-    symtab = SymbolTable() if symtab is None else symtab
-    language = egraph.language
-    state = export_state(egraph, symtab, cost_config)
-    engine = engine if engine is not None else DeviceEngine(rules, symtab, language, cost_config, method=cfg.main_extractor,
-                                    headroom=cfg.headroom)
+    t0 = time.monotonic()
+    if engine is None:
+        symtab = SymbolTable() if symtab is None else symtab
+        engine = DeviceEngine(rules, symtab, egraph.language, cost_config, method=cfg.main_extractor,
+                              headroom=cfg.headroom)
     rng = random.Random(cfg.seed)
-    (state,), cost, n, app = engine.evaluate([state])
-    initial = float(cost[0])
-    trace = []
+    (state,), cost, n, c, app = engine.evaluate([engine.initial(egraph)])
+    first = state
+    iterations = []
     while int(n[0]) < cfg.node_limit:
         root = SearchNode(state, float(cost[0]), int(n[0]))
         root.b = {r for r in range(len(rules)) if not app[0, r]}
         best = run_search(root, engine, len(rules), cfg, rng)
         if best is None:
             break
-        trace.append(best)
-        (state,), changed, cost, n, app = engine.expand([state], [best])
+        (state,), changed, cost, n, c, app = engine.expand([state], [best])
+        iterations.append((int(best), int(n[0]), int(c[0]), float(cost[0])))
         if not changed[0]:
             break
-    return initial, float(cost[0]), trace
+    orig, _ = engine.final(first, cfg.final_extractor)
+    opt, program = engine.final(state, cfg.final_extractor)
+    return RunReport(orig, opt, speedup_pct(orig, opt), time.monotonic() - t0, iterations,
+                     dict(Counter(it[0] for it in iterations)), program, cfg.final_extractor)

@@ -250,6 +250,19 @@ class DeviceBatch:
             "n", "U", "hc_sym", "hc_koff", "hc_kids", "hc_cid", "hc_cost", "uf_parent", "uf_rank")]))
         return o
 
+    def live_counts(self):
+        """(n_cnt, u_cnt): live hashcons entries and union-find ids of the batch input per leaf."""
+        n, u = np.zeros(self.n_leaves, np.uint32), np.zeros(self.n_leaves, np.uint32)
+        self.ctx.check(self.L.esat_download_state(self.h, _p(n), _p(u), None, None, None, None, None, None, None))
+        return n, u
+
+    def rebuilt_sizes(self):
+        """(n, C): e-nodes and e-classes of every leaf's last rebuild (EGraph.size())."""
+        n, c = np.zeros(self.n_leaves, np.uint32), np.zeros(self.n_leaves, np.uint32)
+        self.ctx.check(self.L.esat_download_rebuild(self.h, _p(n), None, None, None, None, None, None, None, None))
+        self.ctx.check(self.L.esat_download_view(self.h, _p(c), None, None, None, None, None, None, None, None))
+        return n, c
+
     def set_pool(self, entries_per_node: float, bitsets_per_node: float | None = None):
         if bitsets_per_node is None:
             self.ctx.check(self.L.esat_batch_set_pool(self.h, C.c_double(entries_per_node)))
@@ -353,7 +366,7 @@ def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max
         batch.extract(method)
         out = batch.download_extract()
         over = out["status"] == X_CAPACITY
-        if method.startswith("ocf") and np.any(over) and factor < max_factor:
+        if method.startswith("ocf") and np.any(over) and factor < max_factor and bitsets < max_factor:
             mask = int(np.bitwise_or.reduce(out["err_class"][over]))
             if mask & 1 or not mask & 3:
                 bitsets *= 2

@@ -54,9 +54,9 @@ def main():
                          max_sim_steps=args.sim_steps)
         st = SymbolTable()
         engine = DeviceEngine(rules, st, eg.language, cost, ctx=ctx, method=cfg.main_extractor, headroom=cfg.headroom)
-        initial, final, trace = optimize_mcts(eg, rules, cfg, cost, symtab=st, engine=engine)
-        run_seed.initial = initial
-        return final, trace
+        rep = optimize_mcts(eg, rules, cfg, cost, symtab=st, engine=engine)
+        run_seed.initial = rep.original_cost
+        return rep.optimized_cost, rep.trace
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -124,3 +124,22 @@ def test_replay_reference_rollouts(group, model):
                 assert got == exp.get("cost", exp.get("msg")), (ref["name"], method)
             checked += 1
     assert checked > 0
+
+
+def test_extraction_costs_not_cached_across_calls():
+    """Two different cost dicts on the same (unchanged) e-graph, back to back, and a dict edited in
+    place: each extraction must use the costs it is given (no identity-keyed cache)."""
+    E, R, X, T = _api()
+    from paper_2410_05534_b200 import analogs
+    from paper_2410_05534_b200.cost_model import CostModelConfig, egraph_costs
+
+    eg = T.graph_to_egraph(analogs.build_analog("nasrnn", T.GraphBuilder))
+    unit = X.extract_ocf_greedy(eg, egraph_costs(eg, CostModelConfig(mode="unit"))).total_cost
+    flops = X.extract_ocf_greedy(eg, egraph_costs(eg, CostModelConfig(mode="analytic"))).total_cost
+    assert unit != flops
+    assert X.extract_ocf_greedy(eg, egraph_costs(eg, CostModelConfig(mode="unit"))).total_cost == unit
+    costs = egraph_costs(eg, CostModelConfig(mode="unit"))
+    base = X.extract_default_greedy(eg, costs).total_cost
+    for node in costs:
+        costs[node] *= 2.0
+    assert X.extract_default_greedy(eg, costs).total_cost == 2.0 * base

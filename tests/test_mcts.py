@@ -42,8 +42,9 @@ def test_toy_mcts_reaches_optimum():
 
     eg = T.toy_term_to_egraph(("div", ("mul", "a", 2), 2))
     cfg = MctsConfig(budget=64, node_limit=10, seed=0, batch=8, headroom=256)
-    initial, final, trace = optimize_mcts(eg, load_rules("toy_math"), cfg, CostModelConfig(mode="term"))
-    assert initial == 4.0 and final == 1.0, (initial, final, trace)   # 4 e-nodes (shared `2`) -> `a`
+    rep = optimize_mcts(eg, load_rules("toy_math"), cfg, CostModelConfig(mode="term"))
+    assert rep.original_cost == 4.0 and rep.optimized_cost == 1.0, rep   # 4 e-nodes (shared `2`) -> `a`
+    assert rep.speedup_pct == 75.0
 
 
 @pytest.mark.gpu
@@ -58,10 +59,11 @@ def test_analog_mcts_deterministic_and_improves():
     for _ in range(2):
         eg = T.graph_to_egraph(analogs.build_analog("nasrnn", T.GraphBuilder))
         cfg = MctsConfig(budget=32, node_limit=2000, seed=3, batch=16, max_sim_steps=4)
-        runs.append(optimize_mcts(eg, load_rules("taso_analog"), cfg, CostModelConfig()))
+        rep = optimize_mcts(eg, load_rules("taso_analog"), cfg, CostModelConfig())
+        runs.append(rep.to_json_dict())
     assert runs[0] == runs[1]
-    initial, final, trace = runs[0]
-    assert trace and final <= initial, runs[0]
+    assert rep.trace and rep.optimized_cost <= rep.original_cost, runs[0]
+    assert rep.final_program is not None
 
 
 @pytest.mark.gpu
@@ -79,8 +81,8 @@ def test_seed_sweep_single_rank():
     def run(seed):
         eg = T.graph_to_egraph(analogs.build_analog("nasnet_a", T.GraphBuilder))
         cfg = MctsConfig(budget=16, node_limit=2000, seed=seed, batch=8, max_sim_steps=3)
-        _, final, trace = optimize_mcts(eg, rules, cfg, CostModelConfig())
-        return final, trace
+        rep = optimize_mcts(eg, rules, cfg, CostModelConfig())
+        return rep.optimized_cost, rep.trace
 
     res, best = root_parallel_sweep(run, [0, 1])
     direct = [run(0), run(1)]

@@ -11,7 +11,7 @@ for model in sys.argv[1:] or ["nasrnn"]:
     eg = T.graph_to_egraph(analogs.build_analog(model, T.GraphBuilder))
     cfg = MctsConfig(budget=128, node_limit=2000, seed=0, batch=64, max_sim_steps=10)
     t = time.time()
-    initial, final, trace = optimize_mcts(eg, load_rules("taso_analog"), cfg, CostModelConfig())
+    rep = optimize_mcts(eg, load_rules("taso_analog"), cfg, CostModelConfig())
     dt = time.time() - t
-    print(f"{model}: cost {initial:.6g} -> {final:.6g} ({100*(initial-final)/initial:.2f}% better), "
-          f"{len(trace)} rules applied, {dt:.1f}s", flush=True)
+    print(f"{model}: cost {rep.original_cost:.6g} -> {rep.optimized_cost:.6g} ({rep.speedup_pct:.2f}% better), "
+          f"{len(rep.trace)} rules applied, {dt:.1f}s", flush=True)
