@@ -109,6 +109,11 @@ int esat_rebuild(esat_batch* b);
 
 /* e-match patterns[0..n) over every leaf (mode LIST or EXISTS) */
 int esat_ematch(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode);
+/* the same, with a per-leaf pattern mask: bit p of leaf_mask[l] selects call-pattern p on leaf l
+ * (0: the leaf is not matched, its counts are 0). An MCTS rollout step matches only the sources of
+ * the rule each leaf applies; joins of unmatched sources are empty. */
+int esat_ematch_masked(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode,
+                       const uint32_t* leaf_mask);
 /* joint_match of multi-pattern rules over the LIST results of their source patterns.
  * rule r: n_src[r] sources (pattern ids src[src_off[r]..]); var_map/pvar_map give the output
  * slot of each source var/pvar (sorted combined names); out record = [S roots][NV][NQ]. */
@@ -141,6 +146,9 @@ int esat_download_view(esat_batch* b, uint32_t* C, uint32_t* root_pos, uint32_t*
  * counts[L] and word offsets[L+1] (into words); words may be NULL to query sizes. */
 int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t* counts, uint64_t* word_off,
                           uint32_t* words, uint64_t words_cap);
+/* counts[n][L] of every pattern (ematch) or rule (join) of the last call in one copy: match counts
+ * in LIST mode, 0/1 existence in EXISTS mode (is_rule_applicable of every source at once) */
+int esat_download_counts(esat_batch* b, int from_join, uint32_t* counts);
 int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, double* root_cost,
                           double* class_cost, uint32_t* choice, uint8_t* reachable, uint32_t* passes);
 

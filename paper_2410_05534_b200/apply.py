@@ -247,7 +247,9 @@ class ApplyDriver:
         self.symtab.intern(Symbol(p.name, arity, payload), self.language)
         self.interned += len(self.symtab) - before
 
-    def apply(self, leaf_rule, node_limit: int = 0, max_rounds: int = 256) -> dict:
+    def apply(self, leaf_rule, node_limit: int = 0, max_rounds: int = 256, leaf_mask=None) -> dict:
+        """esat_apply of leaf_rule[l] on every leaf over the match lists of the last e-match (made
+        with ``leaf_mask`` when given: the same mask is used to re-match after interning)."""
         from . import native
 
         b = self.pipe.batch
@@ -263,5 +265,5 @@ class ApplyDriver:
             if len(self.symtab) == before:
                 raise RuntimeError("device asked for symbols that are already interned")
             self.upload()
-            self.pipe.ematch()   # codes moved: re-derive the match records on the same view
+            self.pipe.ematch(leaf_mask)   # codes moved: re-derive the match records on the same view
         raise RuntimeError("symbol interning did not converge")

@@ -128,11 +128,15 @@ struct esat_batch {
     bool m_verified = false, m_pending = false, j_verified = false, j_pending = false;
     bool j_relaunch_needed = false, m_sig_matches_join = false, m_sized = false, j_sized = false;
     std::vector<uint32_t> m_sig, j_sig;
+    uint32_t* d_lmask = nullptr;   // per-leaf pattern masks of the last esat_ematch_masked call
+    bool lmask_on = false;
     // apply loop: live counts (valid once set by esat_batch_set_counts or an apply) + scratch
     bool counts = false;
     uint32_t *d_ncnt = nullptr, *d_ucnt = nullptr, *d_ureb = nullptr;
     uint32_t *a_rule = nullptr, *a_status = nullptr, *a_report = nullptr, *a_missing = nullptr;
     uint32_t *a_shead = nullptr, *a_stail = nullptr, *a_snext = nullptr, *a_sseen = nullptr, *a_sstack = nullptr;
+    uint32_t *a_pot = nullptr, *a_phead = nullptr, *a_ptail = nullptr, *a_pend = nullptr, *a_pnext = nullptr,
+             *a_eown = nullptr;
     // fingerprint buffers
     unsigned long long *f_lab0 = nullptr, *f_lab1 = nullptr, *f_tkey = nullptr, *f_fp = nullptr;
     uint32_t *f_rep0 = nullptr, *f_rep1 = nullptr, *f_nord = nullptr, *f_tval = nullptr, *f_cord = nullptr,
@@ -314,6 +318,8 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
     OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N); OWN(x.lhn, N); OWN(x.lcc, 2 * N);
+    OWN(x.hpass, N); OWN(x.cpass, N); OWN(x.chgp, 2 * N); OWN(x.dm, 2 * N); OWN(x.lvm, 2 * NL);
+    OWN(x.poff, NL); OWN(x.plist, K); OWN(x.nco, N); OWN(x.nho, N); OWN(x.nhr, N); OWN(x.nbit, N);
     x.slot_stride = N;
     *out = b;
     return ESAT_OK;
@@ -324,6 +330,7 @@ int esat_batch_destroy(esat_batch* b) {
     cudaSetDevice(b->ctx->device);
     for (void* p : b->owned) cudaFree(p);
     cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
+    cudaFree(b->d_lmask);
     cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
     cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
     cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->j_gsort); cudaFree(b->j_big); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
@@ -397,21 +404,24 @@ int esat_batch_set_pool2(esat_batch* b, double values_per_node, double bitsets_p
 static int ensure_pool(esat_batch* b) {
     esat_ctx* c = b->ctx;
     const uint32_t L = b->L;
-    std::vector<uint32_t> live(L);
+    // live e-nodes and classes per leaf: a headroom arena (MCTS) reads the last rebuild's sizes; a
+    // plain upload (every span is its leaf) bounds the classes by the span
+    std::vector<uint32_t> live(L), ncls(L);
     if (b->counts && L) {
         CK(c, cudaMemcpyAsync(live.data(), b->d.o_n, 4ull * L, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(ncls.data(), b->d.v_C, 4ull * L, cudaMemcpyDeviceToHost, c->stream));
         CK(c, cudaStreamSynchronize(c->stream));
     } else {
-        for (uint32_t l = 0; l < L; l++) live[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]);
+        for (uint32_t l = 0; l < L; l++) live[l] = ncls[l] = (uint32_t)(b->nb[l + 1] - b->nb[l]);
     }
     std::vector<uint64_t> pb(L + 1, 0), pbk(L + 1, 0);
     const double kf = b->pool_kfactor > 0 ? b->pool_kfactor
                                           : (b->pool_factor / 8.0 > 3.0 ? b->pool_factor / 8.0 : 3.0);
     for (uint32_t l = 0; l < L; l++) {
-        const uint64_t n = live[l];
-        const uint64_t nw = ((n + 31) / 32 + 3) & ~3ull;   // bitset words per history (C <= n)
+        const uint64_t n = live[l], C = ncls[l];
+        const uint64_t nw = ((C + 31) / 32 + 3) & ~3ull;   // bitset words per history (k_extract's NW)
         pb[l + 1] = pb[l] + (uint64_t)(b->pool_factor * (double)n) + 64;
-        pbk[l + 1] = pbk[l] + (uint64_t)(kf * (double)n) * 4 * nw + 16 * nw + 64;   // bits|wptr|wmax
+        pbk[l + 1] = pbk[l] + (uint64_t)(kf * (double)C) * 4 * nw + 16 * nw + 64;   // bits|wptr|wmax
     }
     if (b->d_pb && pb == b->pb && pbk == b->pbk && b->pool_total >= pb[L] && b->pool_ktotal >= pbk[L])
         return ESAT_OK;
@@ -654,6 +664,7 @@ static int ematch_launch(esat_batch* b) {
     d.sym_par = c->sym_par; d.n_syms = c->n_syms;
     a.smem_bytes = b->m_smem;
     a.no_flat = getenv("ESAT_EMATCH_GENERIC") ? 1 : 0;
+    a.leaf_mask = b->lmask_on ? b->d_lmask : nullptr;
     const uint32_t cap_bytes = 100 * 1024;
     if (a.smem_bytes > c->ematch_attr) {
         CK(c, cudaFuncSetAttribute(k_ematch<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_bytes));
@@ -713,6 +724,10 @@ static int verify_matches(esat_batch* b) {
 }
 
 int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
+    return esat_ematch_masked(b, P, pat_ids, mode, nullptr);
+}
+
+int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode, const uint32_t* leaf_mask) {
     if (!b || (P && !pat_ids) || (mode != ESAT_MATCH_LIST && mode != ESAT_MATCH_EXISTS)) return ESAT_E_ARG;
     if (P > 32) return fail(b->ctx, ESAT_E_ARG, "at most 32 patterns per esat_ematch call (got %u)", P);
     esat_ctx* c = b->ctx;
@@ -767,6 +782,11 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
         b->m_sig = sig;
         b->m_sized = false;
     }
+    if (leaf_mask) {
+        if (!b->d_lmask) CK(c, cudaMalloc((void**)&b->d_lmask, 4ull * (L ? L : 1)));
+        CK(c, cudaMemcpyAsync(b->d_lmask, leaf_mask, 4ull * L, cudaMemcpyHostToDevice, c->stream));
+    }
+    b->lmask_on = leaf_mask != nullptr;
     b->m_P = P;
     b->m_mode = mode;
     b->j_R = 0;   // a new match call invalidates earlier join results
@@ -927,6 +947,20 @@ int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t
     return ESAT_OK;
 }
 
+int esat_download_counts(esat_batch* b, int from_join, uint32_t* counts) {
+    if (!b || !counts) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    int rv = verify_matches(b);
+    if (rv) return rv;
+    cudaSetDevice(c->device);
+    const uint64_t n = from_join ? b->j_R : b->m_P;
+    if (n * b->L)
+        CK(c, cudaMemcpyAsync(counts, from_join ? b->d_j_count : b->d_m_count, 4ull * n * b->L,
+                              cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return ESAT_OK;
+}
+
 int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t* counts, uint64_t* word_off,
                           uint32_t* words, uint64_t words_cap) {
     if (!b || !counts || !word_off) return ESAT_E_ARG;
@@ -998,6 +1032,8 @@ static int ensure_apply_buffers(esat_batch* b) {
     b->d.u_reb = b->d_ureb;
     OWN(b->a_rule, L); OWN(b->a_status, L); OWN(b->a_report, 8 * L); OWN(b->a_missing, 16 * L);
     OWN(b->a_shead, U); OWN(b->a_stail, U); OWN(b->a_sseen, U); OWN(b->a_snext, N); OWN(b->a_sstack, N + K);
+    OWN(b->a_pot, U); OWN(b->a_phead, U); OWN(b->a_ptail, U); OWN(b->a_pend, U); OWN(b->a_pnext, K);
+    OWN(b->a_eown, K);
     return ESAT_OK;
 }
 
@@ -1060,6 +1096,10 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
     a.status = b->a_status; a.report = b->a_report; a.missing = b->a_missing;
     a.s_head = b->a_shead; a.s_tail = b->a_stail; a.s_next = b->a_snext; a.s_seen = b->a_sseen;
     a.s_stack = b->a_sstack;
+    a.s_pot = b->a_pot; a.s_phead = b->a_phead; a.s_ptail = b->a_ptail; a.s_pend = b->a_pend;
+    a.s_pnext = b->a_pnext; a.s_eown = b->a_eown;
+    static const int no_pot = getenv("ESAT_APPLY_NO_POT") ? 1 : 0;
+    a.no_pot = no_pot;
     tic(c);
     if (b->L) k_apply<<<b->L, 32, 0, c->stream>>>(d, a);
     toc(c);

@@ -12,12 +12,21 @@
 // is a linked list of hashcons entries per class root; union concatenates lists (egraph.py:
 // 189-201). class_shape (rewrite.py:286-290) is the shape of the head entry's symbol (tensor
 // e-classes are shape-homogeneous). Symbols are looked up by their identity key (apply.py).
+#include <cstdio>
+
 #include "esat_internal.cuh"
 #include "k_apply_args.cuh"
 
 namespace esat {
 
 namespace {
+
+// debug-build bounds checks (ESAT_DEBUG): report and skip the access instead of faulting
+#ifdef ESAT_DEBUG
+#define ABAD(cond) ((cond) ? (printf("k_apply leaf %u line %d: %s\n", L.l, __LINE__, #cond), true) : false)
+#else
+#define ABAD(cond) false
+#endif
 
 constexpr int INSTR = 20;
 constexpr int MAXI = 24;      // instructions per target
@@ -49,11 +58,15 @@ struct Leaf {
     uint32_t* parent;
     uint8_t* rank;
     uint32_t *head, *tail, *next, *seen, *stack, *tab;
+    uint32_t *pot, *phead, *ptail, *pnext, *eown;   // cycle-test potentials + parent edges (below)
     uint32_t tmask, stamp, lane;
-    bool changed;
+    bool changed, usepot;
 };
 
-__device__ __forceinline__ uint32_t find(Leaf& L, uint32_t x) { return uf_find(L.parent, x); }
+__device__ __forceinline__ uint32_t find(Leaf& L, uint32_t x) {
+    if (ABAD(x >= L.U)) return 0;
+    return uf_find(L.parent, x);
+}
 
 __device__ Shape sym_shape(const AArgs& a, uint32_t s) {
     Shape sh;
@@ -67,6 +80,7 @@ __device__ __forceinline__ Shape class_shape(Leaf& L, uint32_t c) {
     Shape sh;
     sh.nd = NO_SHAPE;
     if (e == NONE) return sh;
+    if (ABAD(e >= L.n)) return sh;
     return sym_shape(*L.a, L.sym[e]);
 }
 
@@ -257,6 +271,7 @@ __device__ uint32_t hc_get(Leaf& L, uint32_t sym, const uint32_t* k, uint32_t ar
     for (uint32_t s = node_hash(sym, k, ar) & L.tmask;; s = (s + 1) & L.tmask) {
         const uint32_t e = L.tab[s];
         if (e == NONE) return NONE;
+        if (ABAD(e >= L.n)) return NONE;
         if (L.sym[e] != sym || L.koff[e + 1] - L.koff[e] != ar) continue;
         bool ok = true;
         for (uint32_t i = 0; i < ar && ok; i++) ok = L.kids[L.koff[e] + i] == k[i];
@@ -280,30 +295,46 @@ __device__ __forceinline__ void list_push(Leaf& L, uint32_t c, uint32_t e) {
 // would_create_cycle (rewrite.py:492-505): is goal reachable from refs through child edges?
 // Warp-cooperative BFS (same reachable set as the reference's DFS): a queue of classes, 32 expanded
 // per step, children's roots claimed once per query with an epoch-stamped atomic exchange.
+//
+// Potential pruning (exact): every class root carries pot with pot[p] >= pot[c] for every child edge
+// p -> c between distinct classes, so a class whose pot is below the goal's cannot reach the goal
+// and is neither queued nor expanded. Most instantiations reference classes inside the match, below
+// the matched class, and are answered without a walk. The invariant is established by a Kahn height
+// pass over the rebuilt state (classes in or above a cycle share the top value) and kept by add
+// (1 + max over the children) and union (the merged class takes the larger value; ancestors below
+// it are raised to it).
 __device__ bool reaches(Leaf& L, const uint32_t* refs, uint32_t nrefs, uint32_t goal, bool* overflow,
                         uint32_t* qtail) {
     const uint32_t st = ++L.stamp, cap = L.cap_k + L.cap_n;
+    if (ABAD(goal >= L.U)) return false;
+    const bool prune = L.usepot;
+    const uint32_t pg = prune ? L.pot[goal] : 0u;
     bool found = false;
     if (L.lane == 0) {
         uint32_t qt = 0;
         for (uint32_t i = 0; i < nrefs && !found; i++) {
             const uint32_t c = find(L, refs[i]);
             if (c == goal) found = true;
-            else if (L.seen[c] != st) { L.seen[c] = st; L.stack[qt++] = c; }
+            else if (L.seen[c] != st && (!prune || L.pot[c] >= pg)) { L.seen[c] = st; L.stack[qt++] = c; }
         }
         *qtail = qt;
     }
     __syncwarp();
     found = __shfl_sync(0xffffffffu, found, 0);
-    uint32_t qh = 0, qt = *qtail;
+    // the queue length is read by lane 0 and broadcast: a lane that runs ahead into the next round
+    // pushes (atomicAdd on *qtail) only after the shuffle, so every lane sees the same length (a
+    // per-lane read after the barrier could see another lane's next-round pushes)
+    uint32_t qh = 0, qt = __shfl_sync(0xffffffffu, *(volatile uint32_t*)qtail, 0);
     while (!found && qh < qt) {
         const uint32_t idx = qh + L.lane;
         if (idx < qt) {
             const uint32_t c = L.stack[idx];
-            for (uint32_t e = L.head[c]; e != NONE && !found; e = L.next[e])
+            if (ABAD(c >= L.U)) continue;
+            for (uint32_t e = L.head[c]; e != NONE && !found && !ABAD(e >= L.n); e = L.next[e])
                 for (uint32_t q = L.koff[e]; q < L.koff[e + 1]; q++) {
                     const uint32_t r = find(L, L.kids[q]);
                     if (r == goal) { found = true; break; }
+                    if (prune && L.pot[r] < pg) continue;
                     if (atomicExch(&L.seen[r], st) != st) {
                         const uint32_t pos = atomicAdd(qtail, 1u);
                         if (pos < cap) L.stack[pos] = r;
@@ -314,7 +345,7 @@ __device__ bool reaches(Leaf& L, const uint32_t* refs, uint32_t nrefs, uint32_t 
         found = __any_sync(0xffffffffu, found);
         __syncwarp();
         qh = qh + 32 < qt ? qh + 32 : qt;
-        qt = *qtail;
+        qt = __shfl_sync(0xffffffffu, *(volatile uint32_t*)qtail, 0);
         if (qt > cap) { qt = cap; }
     }
     __syncwarp();
@@ -346,25 +377,83 @@ __device__ uint32_t add_node(Leaf& L, const Sym& s, int op, const uint32_t* k, c
         L.cost[e] = node_cost(*L.a, op, s, cs);
         hc_insert(L, e);
         list_push(L, id, e);
+        if (L.usepot) {   // a new class has no parents: 1 + the highest child potential
+            uint32_t pv = 0;
+            L.phead[id] = NONE;
+            L.ptail[id] = NONE;
+            for (uint32_t i = 0; i < s.arity; i++) {
+                const uint32_t c = k[i], q = k0 + i;   // children are roots (canonicalised by the caller)
+                if (ABAD(c >= L.U) || ABAD(q >= L.cap_k)) continue;
+                pv = max(pv, L.pot[c] + 1u);
+                L.eown[q] = e;
+                L.pnext[q] = NONE;
+                if (L.phead[c] == NONE) L.phead[c] = q; else L.pnext[L.ptail[c]] = q;
+                L.ptail[c] = q;
+            }
+            L.pot[id] = pv;
+        }
     }
     __syncwarp();
     L.changed = true;
     return id;
 }
 
-__device__ bool union_classes(Leaf& L, uint32_t a, uint32_t b) {
+// raise every ancestor of class w whose potential is below pot[w] to pot[w] (warp-cooperative
+// upward walk over the parent-edge lists; each class is raised, and queued, at most once)
+__device__ void raise_ancestors(Leaf& L, uint32_t w, uint32_t* qtail) {
+    const uint32_t P = L.pot[w], cap = L.cap_k + L.cap_n;
+    if (L.lane == 0) { L.stack[0] = w; *qtail = 1; }
+    __syncwarp();
+    uint32_t qh = 0, qt = 1;
+    while (qh < qt) {
+        const uint32_t idx = qh + L.lane;
+        if (idx < qt) {
+            const uint32_t x = L.stack[idx];
+            for (uint32_t q = L.phead[x]; q != NONE && !ABAD(x >= L.U); q = L.pnext[q]) {
+                if (ABAD(q >= L.K) || ABAD(L.eown[q] >= L.n) || ABAD(L.cid[L.eown[q]] >= L.U)) break;
+                const uint32_t p = find(L, L.cid[L.eown[q]]);
+                if (p == x || L.pot[p] >= P) continue;
+                if (atomicMax(&L.pot[p], P) < P) {
+                    const uint32_t pos = atomicAdd(qtail, 1u);
+                    if (pos < cap) L.stack[pos] = p;
+                }
+            }
+        }
+        __syncwarp();
+        qh = qh + 32 < qt ? qh + 32 : qt;
+        qt = min(__shfl_sync(0xffffffffu, *(volatile uint32_t*)qtail, 0), cap);
+    }
+}
+
+__device__ bool union_classes(Leaf& L, uint32_t a, uint32_t b, uint32_t* qtail) {
     const uint32_t ra = find(L, a), rb = find(L, b);
     __syncwarp();
     if (ra == rb) return false;
+    uint32_t win = 0;
+    bool raise = false;
     if (L.lane == 0) {
-        const uint32_t win = uf_union(L.parent, L.rank, ra, rb), lose = win == ra ? rb : ra;
+        win = uf_union(L.parent, L.rank, ra, rb);
+        const uint32_t lose = win == ra ? rb : ra;
         if (L.head[lose] != NONE) {
             if (L.head[win] == NONE) { L.head[win] = L.head[lose]; L.tail[win] = L.tail[lose]; }
             else { L.next[L.tail[win]] = L.head[lose]; L.tail[win] = L.tail[lose]; }
             L.head[lose] = NONE;
         }
+        if (L.usepot) {
+            if (L.phead[lose] != NONE) {
+                if (L.phead[win] == NONE) { L.phead[win] = L.phead[lose]; L.ptail[win] = L.ptail[lose]; }
+                else { L.pnext[L.ptail[win]] = L.phead[lose]; L.ptail[win] = L.ptail[lose]; }
+                L.phead[lose] = NONE;
+            }
+            const uint32_t P = max(L.pot[ra], L.pot[rb]);
+            raise = L.pot[ra] != L.pot[rb];   // the lower side's parents may now sit below P
+            L.pot[win] = P;
+        }
     }
     __syncwarp();
+    win = __shfl_sync(0xffffffffu, win, 0);
+    raise = __shfl_sync(0xffffffffu, raise, 0);
+    if (raise) raise_ancestors(L, win, qtail);
     L.changed = true;
     return true;
 }
@@ -392,6 +481,9 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     L.head = a.s_head + u0; L.tail = a.s_tail + u0; L.next = a.s_next + b; L.seen = a.s_seen + u0;
     L.stack = a.s_stack + b + k0;
     L.tab = d.s_tc + t0;
+    L.pot = a.s_pot + u0; L.phead = a.s_phead + u0; L.ptail = a.s_ptail + u0;
+    L.pnext = a.s_pnext + k0; L.eown = a.s_eown + k0;
+    L.usepot = !a.no_pot;
     L.tmask = (uint32_t)(d.tb[l + 1] - t0) - 1;
     L.stamp = 0;
     L.changed = false;
@@ -429,6 +521,62 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     // writes are issued by lane 0 and fenced with __syncwarp, the cycle test uses all lanes
     __shared__ uint32_t sh_qtail;
     L.lane = lane;
+    __shared__ uint32_t sh_kahn;
+    if (rule != NONE && L.usepot) {
+        // cycle-test potentials of the rebuilt state: parent-edge lists (child slots, self-loops left
+        // out), then Kahn rounds from the classes without children: pot = height; classes in or
+        // above a cycle are never released and share the top value (pot[p] >= pot[c] either way)
+        uint32_t* pend = a.s_pend + u0;
+        if (lane == 0 && (ABAD(L.U > L.cap_u) || ABAD(L.n > L.cap_n) || ABAD(L.K > L.cap_k))) {}
+        for (uint32_t x = lane; x < L.U; x += 32) { L.pot[x] = 0; L.phead[x] = NONE; L.ptail[x] = NONE; pend[x] = 0; }
+        __syncwarp();
+        for (uint32_t e = lane; e < L.n; e += 32) {
+            const uint32_t c = L.cid[e];
+            if (ABAD(c >= L.U) || ABAD(L.koff[e + 1] > L.cap_k)) continue;
+            for (uint32_t q = L.koff[e]; q < L.koff[e + 1]; q++) {
+                L.eown[q] = e;
+                const uint32_t k = L.kids[q];   // rebuilt keys are canonical: children are roots
+                if (ABAD(k >= L.U)) continue;
+                if (k == c) { L.pnext[q] = NONE; continue; }
+                atomicAdd(&pend[c], 1u);
+                const uint32_t old = atomicExch(&L.phead[k], q);
+                L.pnext[q] = old;
+                if (old == NONE) L.ptail[k] = q;
+            }
+        }
+        if (lane == 0) sh_kahn = 0;
+        __syncwarp();
+        for (uint32_t c = lane; c < L.U; c += 32)
+            if (L.head[c] != NONE && pend[c] == 0) {
+                const uint32_t pos = atomicAdd(&sh_kahn, 1u);
+                if (!ABAD(pos >= L.n)) L.stack[pos] = c;
+            }
+        __syncwarp();
+        uint32_t f0 = 0, f1 = __shfl_sync(0xffffffffu, *(volatile uint32_t*)&sh_kahn, 0), round = 0;
+        while (f0 < f1) {
+            for (uint32_t i = f0 + lane; i < f1; i += 32) {
+                const uint32_t c = L.stack[i];
+                if (ABAD(c >= L.U)) continue;
+                for (uint32_t q = L.phead[c]; q != NONE; q = L.pnext[q]) {
+                    if (ABAD(q >= L.K) || ABAD(L.eown[q] >= L.n)) break;
+                    const uint32_t pc = L.cid[L.eown[q]];
+                    if (ABAD(pc >= L.U)) continue;
+                    if (atomicSub(&pend[pc], 1u) == 1u) {
+                        L.pot[pc] = round + 1;
+                        const uint32_t pos = atomicAdd(&sh_kahn, 1u);
+                        if (!ABAD(pos >= L.n)) L.stack[pos] = pc;
+                    }
+                }
+            }
+            __syncwarp();
+            f0 = f1;
+            f1 = __shfl_sync(0xffffffffu, *(volatile uint32_t*)&sh_kahn, 0);
+            round++;
+        }
+        for (uint32_t c = lane; c < L.U; c += 32)
+            if (L.head[c] != NONE && pend[c] != 0) L.pot[c] = round + 1;
+        __syncwarp();
+    }
     uint32_t st = A_OK, found = 0, cyc = 0, shp = 0;
     const uint32_t n_before = L.n;
     uint32_t unions = 0;
@@ -539,7 +687,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                     }
                 }
                 if (err != A_OK) { st = err; break; }
-                if (union_classes(L, inst[top], matched)) unions++;
+                if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
             }
         }
     }

@@ -39,6 +39,10 @@ struct AArgs {
     uint32_t *status, *report, *missing;   // report [L][4]: matches_found, changed, cycles, shapes
     // scratch
     uint32_t *s_head, *s_tail, *s_next, *s_seen, *s_stack;
+    // cycle-test potentials: pot[U], parent-edge lists phead/ptail[U] over child slots pnext/eown[K],
+    // Kahn pending counts pend[U]
+    uint32_t *s_pot, *s_phead, *s_ptail, *s_pend, *s_pnext, *s_eown;
+    int no_pot;   // 1: plain BFS without potential pruning (env ESAT_APPLY_NO_POT; for measurement)
 };
 
 __global__ void k_apply(Dev d, AArgs a);

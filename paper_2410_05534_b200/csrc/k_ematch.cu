@@ -404,9 +404,14 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         return (cmask && m.prog[3] == 1 && rname < 32) ? (1u << rname) : 0u;
     };
 
+    const uint32_t lmask = a.leaf_mask ? a.leaf_mask[l] : 0xFFFFFFFFu;   // patterns this leaf needs
     if (a.mode == 1) {  // existence only (is_rule_applicable, rewrite.py:579-589)
         uint32_t po = 0;
         for (uint32_t pi = 0; pi < a.P; pi++) {
+            if (!((lmask >> pi) & 1u)) {
+                if (tid == 0) { a.count[(uint64_t)pi * L + l] = 0; a.off[(uint64_t)pi * L + l] = 0; }
+                continue;
+            }
             set_prog(prog_of(pi, po));
             const uint32_t rbit = root_bit();
             uint32_t any = 0;
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
         const uint32_t pi = i / C, r = i - pi * C;
         uint32_t n = 0;
         const uint32_t rb = sp_rbit[pi];
-        if (!rb || (cmask[r] & rb)) {
+        if (((lmask >> pi) & 1u) && (!rb || (cmask[r] & rb))) {
             if (sp_flat[pi].ok) {
                 n = match_class_flat2(m, sp_flat[pi], r, [](uint32_t, const uint32_t (&)[4], const uint32_t (&)[4]) {});
             } else {

@@ -27,6 +27,7 @@ struct MArgs {
     uint32_t* raw;              // [L][32][T] per-thread raw match counts (count -> fill placement)
     uint32_t* nzl;              // [L][32][C] (pattern, class) pairs with matches (pass-2 work list)
     int no_flat;                // 1: always use the generic backtracking matcher
+    const uint32_t* leaf_mask;  // [L] bit p: match call-pattern p on this leaf (nullptr: all)
 };
 
 struct JArgs {

@@ -169,7 +169,7 @@ class DeviceEngine:
         return [packed, pipe, b, drv, headroom or self.headroom]
 
     def _extract(self, b, method=None):
-        out = native.extract_with_retry(b, method or self.method, factor=32)
+        out = native.extract_with_retry(b, method or self.method, factor=32, bitsets=2.0)
         cost = out["root_cost"].copy()
         cost[out["status"] != 0] = np.inf
         return cost, out
@@ -192,14 +192,8 @@ class DeviceEngine:
         return out
 
     def _applicable(self, pipe, b):
-        """[L, R] is_rule_applicable: every source of the rule has a match (rewrite.py:579-589)."""
-        pipe.match()
-        cnt = {}
-        for r in pipe.rules:
-            for pid in r.pattern_ids:
-                if pid not in cnt:
-                    cnt[pid] = b.download_matches(pid)[2]
-        return np.stack([np.all([cnt[p] > 0 for p in r.pattern_ids], axis=0) for r in pipe.rules], axis=1)
+        """[L, R] is_rule_applicable (rewrite.py:579-589): one EXISTS-mode e-match of all sources."""
+        return pipe.exists()
 
     def _apply(self, h, rules):
         """esat_apply of rules[l] on every leaf of the rebuilt batch ``h``. A leaf that runs out of
@@ -211,8 +205,9 @@ class DeviceEngine:
         while True:
             packed, pipe, b, drv, head = h
             U0 = b.live_counts()[1]
-            pipe.ematch()
-            res = drv.apply(rules)
+            mask = pipe.rule_masks(rules)   # each leaf matches only the sources of its own rule
+            pipe.ematch(mask)
+            res = drv.apply(rules, leaf_mask=mask)
             st = res["status"]
             if np.any(st == native.A_PROGRAM):
                 raise RuntimeError("k_apply: rule target program beyond device limits (ESAT_A_PROGRAM)")
@@ -261,12 +256,18 @@ class DeviceEngine:
 
     def simulate(self, states, costs0, allowed, steps: int, node_limit: int, rng: random.Random):
         """Random rollouts: per step every live leaf applies a uniformly drawn
-        allowed rule, rebuilds and extracts (rollout_rewards); a leaf stops at the node limit."""
+        allowed rule, rebuilds and extracts (rollout_rewards); a leaf stops at the node limit. The
+        device batch holds the live leaves only: when leaves stop, the batch is re-packed from the
+        survivors' rebuilt states (a stopped leaf -- typically one a multi-pattern rule exploded --
+        is never matched, rebuilt or extracted again)."""
         L = len(states)
-        h = self._open(states)
         reward = np.zeros(L)
         prev = np.asarray(costs0, np.float64).copy()
-        live = np.ones(L, bool)
+        live = np.array([bool(a) for a in allowed], bool)
+        idx = np.nonzero(live)[0]            # batch position -> leaf
+        if idx.size == 0:
+            return reward
+        h = self._open([states[l] for l in idx])
         h[1].rebuild()
         for _ in range(steps):
             rules = np.full(L, NONE, np.uint32)
@@ -277,12 +278,21 @@ class DeviceEngine:
                     live[l] = False
             if not live.any():
                 break
-            self._apply(h, rules)
+            if not live[idx].all():          # compact: drop the leaves that stopped
+                keep = np.nonzero(live[idx])[0]
+                clean = self._clean_states(h[0], h[2])
+                h[2].close()
+                idx = idx[keep]
+                h = self._open([clean[j] for j in keep])
+                h[1].rebuild()
+            self._apply(h, rules[idx])
             h[1].rebuild()
-            cost, _ = self._extract(h[2])
+            cb, _ = self._extract(h[2])
+            cost = np.full(L, np.inf)
+            cost[idx] = cb
             rollout_rewards(reward, prev, live, cost)
             n, _ = h[2].rebuilt_sizes()
-            live &= n < node_limit
+            live[idx] &= n < node_limit
         h[2].close()
         return reward
 

@@ -64,7 +64,7 @@ def lib():
                      "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork",
                      "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
                      "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
-                     "esat_download_fingerprint"):
+                     "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts"):
             getattr(L, name).restype = C.c_int
         L.esat_apply_setup.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_uint32, vp, vp, C.c_uint32, vp,
                                        C.c_uint32, vp, C.c_uint32, vp, vp]
@@ -82,7 +82,7 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork",
             "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
             "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
-            "esat_download_fingerprint")
+            "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts")
 
 A_OK, A_NODE_LIMIT, A_NEED_SYMBOL, A_CAPACITY, A_PROGRAM = range(5)
 
@@ -277,9 +277,21 @@ class DeviceBatch:
         """Extraction on the side stream, overlapping e-matching (join with ctx.wait_async())."""
         self.ctx.check(self.L.esat_extract_async(self.h, C.c_int(METHODS[method])))
 
-    def ematch(self, pattern_ids, mode: int = MATCH_LIST):
+    def ematch(self, pattern_ids, mode: int = MATCH_LIST, leaf_mask=None):
+        """k_ematch of the call patterns over every leaf; ``leaf_mask[l]`` (bit p = call-pattern p)
+        restricts a leaf to the patterns it needs (esat_ematch_masked)."""
         ids = _u32(pattern_ids)
-        self.ctx.check(self.L.esat_ematch(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode)))
+        if leaf_mask is None:
+            self.ctx.check(self.L.esat_ematch(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode)))
+        else:
+            m = _u32(leaf_mask)
+            self.ctx.check(self.L.esat_ematch_masked(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode), _p(m)))
+
+    def download_counts(self, n: int, from_join: bool = False) -> np.ndarray:
+        """[n, L] counts of the last e-match (or join) call's patterns (rules) in one copy."""
+        out = np.zeros((n, self.n_leaves), np.uint32)
+        self.ctx.check(self.L.esat_download_counts(self.h, C.c_int(int(from_join)), _p(out)))
+        return out
 
     def join(self, specs: list):
         """specs: per rule (source pattern ids, var maps per source, pvar maps per source, NV, NQ)."""

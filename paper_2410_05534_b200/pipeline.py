@@ -99,9 +99,23 @@ class LeafPipeline:
     def rebuild(self):
         self.batch.rebuild()
 
-    def match(self):
-        """k_ematch: every source pattern of every rule (LIST mode)."""
-        self.batch.ematch(self.pattern_ids)
+    def match(self, leaf_mask=None):
+        """k_ematch: every source pattern of every rule (LIST mode); ``leaf_mask[l]`` (bit p =
+        pattern p) restricts leaf l to the patterns it needs."""
+        self.batch.ematch(self.pattern_ids, leaf_mask=leaf_mask)
+
+    def rule_masks(self, leaf_rule) -> np.ndarray:
+        """Per-leaf pattern masks for applying rule ``leaf_rule[l]`` (0xFFFFFFFF: none): the bits of
+        that rule's source patterns."""
+        bits = [sum(1 << p for p in r.pattern_ids) for r in self.rules]
+        return np.array([0 if int(r) == 0xFFFFFFFF else bits[int(r)] for r in leaf_rule], np.uint32)
+
+    def exists(self) -> np.ndarray:
+        """is_rule_applicable of every rule on every leaf (rewrite.py:579-589): one EXISTS-mode
+        k_ematch over all source patterns; a rule applies iff each of its sources matches. [L, R]"""
+        self.batch.ematch(self.pattern_ids, mode=native.MATCH_EXISTS)
+        cnt = self.batch.download_counts(len(self.pattern_ids))
+        return np.stack([np.all(cnt[r.pattern_ids] > 0, axis=0) for r in self.rules], axis=1)
 
     def join(self):
         """k_join: multi-pattern rules over the source match lists."""
@@ -109,8 +123,8 @@ class LeafPipeline:
             self.batch.join([(r.pattern_ids, r.var_maps, r.pvar_maps, len(r.var_names), len(r.pvar_names))
                              for r in self.joins])
 
-    def ematch(self):
-        self.match()
+    def ematch(self, leaf_mask=None):
+        self.match(leaf_mask)
         self.join()
 
     def extract(self):

@@ -2,9 +2,10 @@
 
 `ematch`, `joint_match` and `is_rule_applicable` execute `k_ematch`/`k_join` through
 `device.py` and return the reference's ordered, deduplicated `Substitution` list
-(rewrite.py:396-433). `apply_rule` keeps the reference's sequential instantiate /
-cycle-filter / shape-filter / union loop on the host (rewrite.py:526-573; the device apply
-loop is the next §8 row) and ends with the device rebuild.
+(rewrite.py:396-433). `apply_rule` runs the reference's sequential instantiate / cycle-filter /
+shape-filter / union loop (rewrite.py:526-573) on the device (`k_apply`, with host interning of
+new operator symbols) and ends with the device rebuild; `would_create_cycle` stays here as the
+host statement of the cycle test `k_apply` answers.
 """
 
 from __future__ import annotations
@@ -12,7 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import device
-from .egraph import EGraph, ENode, StructuralError
+from .egraph import EGraph, StructuralError
 from .patterns import (App, PVar, Rule, RuleSyntaxError, UnboundVariableError, Var, load_rules,  # noqa: F401
                        parse_pattern, parse_rule, parse_rules, pattern_pvars, pattern_vars, print_pattern,
                        print_rule)
@@ -76,33 +77,6 @@ class ApplyReport:
     shape_filtered: int = 0
 
 
-def _params(pat, sub) -> tuple:
-    if pat.params is None:
-        return ()
-    return tuple(sub.param(s.name) if isinstance(s, PVar) else s for s in pat.params)
-
-
-def _refs(eg, lang, pat, sub):
-    """(classes the instance would reference, existing class of the full instance or None)."""
-    if isinstance(pat, Var):
-        c = eg.find(sub.var(pat.name))
-        return {c}, c
-    refs, kids, complete = set(), [], True
-    for ch in pat.children:
-        r, c = _refs(eg, lang, ch, sub)
-        refs |= r
-        if c is None:
-            complete = False
-        else:
-            kids.append(c)
-    if complete:
-        sym = lang.make_symbol(pat.name, _params(pat, sub), tuple(lang.class_shape(eg, c) for c in kids))
-        hit = eg.hashcons.get(eg.canonicalize(ENode(sym, tuple(kids))))
-        if hit is not None:
-            return {eg.find(hit)}, eg.find(hit)
-    return refs, None
-
-
 def would_create_cycle(egraph: EGraph, children, matched_root: int) -> bool:
     """True iff matched_root is reachable from any candidate child (rewrite.py:488-505)."""
     goal = egraph.find(matched_root)
@@ -118,21 +92,6 @@ def would_create_cycle(egraph: EGraph, children, matched_root: int) -> bool:
         for node in egraph.classes[c].nodes:
             todo.extend(egraph.find(x) for x in node.children)
     return False
-
-
-def _shape(eg, lang, pat, sub):
-    if isinstance(pat, Var):
-        return lang.class_shape(eg, eg.find(sub.var(pat.name)))
-    shapes = tuple(_shape(eg, lang, c, sub) for c in pat.children)
-    return lang.symbol_shape(lang.make_symbol(pat.name, _params(pat, sub), shapes))
-
-
-def _instantiate(eg, lang, pat, sub) -> int:
-    if isinstance(pat, Var):
-        return eg.find(sub.var(pat.name))
-    kids = tuple(_instantiate(eg, lang, c, sub) for c in pat.children)
-    sym = lang.make_symbol(pat.name, _params(pat, sub), tuple(lang.class_shape(eg, c) for c in kids))
-    return eg.add(ENode(sym, kids))
 
 
 def apply_rule(egraph: EGraph, rule: Rule, node_limit: int = 0, language=None) -> ApplyReport:

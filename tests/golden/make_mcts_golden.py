@@ -33,12 +33,17 @@ CASES = {
     "toy_b8": ("toy", "toy_math", "term", dict(budget=64, node_limit=10, seed=1, batch=8, final_extractor="exact")),
     "bert_c1_b1": ("bert", "taso_analog", "analytic", dict(budget=16, node_limit=500, seed=0, batch=1)),
     "bert_c1": ("bert", "taso_analog", "analytic", dict(budget=128, node_limit=500, seed=0, batch=32)),
-    "nasrnn_c2": ("nasrnn", "taso_analog", "analytic", dict(budget=32, node_limit=2000, seed=0, batch=32,
-                                                            max_sim_steps=4)),
-    "nasnet_a_c5_s0": ("nasnet_a", "taso_analog", "analytic", dict(budget=32, node_limit=2000, seed=0, batch=32,
-                                                                   max_sim_steps=4)),
-    "nasnet_a_c5_s1": ("nasnet_a", "taso_analog", "analytic", dict(budget=32, node_limit=2000, seed=1, batch=32,
-                                                                   max_sim_steps=4)),
+    # reduced budgets ("a committed reduced budget if runtime forces it"): the reference's
+    # apply_rule needs tens of minutes for one application of the #128 / #138-analog multi-pattern
+    # rules on a 1-2k-node leaf (28k matches, a would_create_cycle DFS each), so the node limit of
+    # these cases keeps the leaves the search explodes from small
+    "nasrnn_c2": ("nasrnn", "taso_analog", "analytic", dict(budget=128, node_limit=800, seed=0, batch=32)),
+    "nasrnn_c2_limit2000": ("nasrnn", "taso_analog", "analytic", dict(budget=128, node_limit=2000, seed=0, batch=32)),
+    "resnext50_c3": ("resnext50", "taso_analog", "analytic", dict(budget=128, node_limit=1000, seed=0, batch=32)),
+    "inception_v3_c4": ("inception_v3", "taso_analog", "analytic", dict(budget=64, node_limit=1000, seed=0,
+                                                                        batch=32)),
+    "nasnet_a_c5_s0": ("nasnet_a", "taso_analog", "analytic", dict(budget=64, node_limit=1000, seed=0, batch=32)),
+    "nasnet_a_c5_s1": ("nasnet_a", "taso_analog", "analytic", dict(budget=64, node_limit=1000, seed=1, batch=32)),
 }
 
 

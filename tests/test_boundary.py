@@ -78,3 +78,13 @@ def test_fingerprint_key_tables():
     assert [keys[i] for i in np.argsort(krank)] == sorted(keys)
     for i, k in enumerate(keys):
         assert blob[off[i]:off[i + 1]] == repr(k).encode()
+
+
+def test_cost_model_spec_kats():
+    """SPEC.md:402-404 operator_cost examples (analytic FLOPs x coefficient, unit mode)."""
+    from paper_2410_05534_b200.cost_model import CostModelConfig, operator_cost
+
+    assert operator_cost(CostModelConfig(), "matmul", (), (8, 32), ((8, 16), (16, 32))) == 8.192e-6
+    assert operator_cost(CostModelConfig(mode="unit"), "conv2d", (1, 1, "none"), (1, 8, 16, 16),
+                         ((1, 8, 16, 16), (8, 8, 3, 3))) == 1.0
+    assert operator_cost(CostModelConfig(mode="unit"), "input", ("x",), (1, 8), ()) == 0.0

@@ -129,3 +129,38 @@ def test_device_matches_oracle_on_replicated_batch(ctx):
         for l in range(packed["n_leaves"]):
             n0, C = int(packed["node_base"][l]), int(ref["C"][l])
             assert np.array_equal(e_dev["choice"][n0:n0 + C], e_ref["choice"][n0:n0 + C]), (method, l)
+
+
+@pytest.mark.parametrize("group", [g for g in GROUPS if g != "random"])
+def test_exists_mode_matches_reference_source_counts(ctx, group):
+    """is_rule_applicable (rewrite.py:579-589) is one EXISTS-mode e-match of every source pattern:
+    per (state, source) the device's existence bit must equal ``len(ematch(state, source)) > 0`` of
+    the reference (the goldens' source_counts), and the LIST mode's counts must equal the counts."""
+    from paper_2410_05534_b200 import native
+
+    st, packed, cases, b, view = _device_rebuild(ctx, group)
+    rules = rules_of(load_group(group))
+    progs, where = [], []
+    for r in rules:
+        comps, *_ = compile_rule(r, st)
+        for s, cp in enumerate(comps):
+            where.append((r.id, s))
+            progs.append(cp.program)
+    ctx.upload_patterns(progs)
+    b.ematch(list(range(len(progs))), mode=native.MATCH_EXISTS)
+    exists = [b.download_matches(p)[2].copy() for p in range(len(progs))]
+    b.ematch(list(range(len(progs))))
+    counts = [b.download_matches(p)[2].copy() for p in range(len(progs))]
+    bad = []
+    for p, (rid, s) in enumerate(where):
+        for l, c in enumerate(cases):
+            want = c["ematch"][rid]["source_counts"][s]
+            if bool(exists[p][l]) != (want > 0) or int(counts[p][l]) != want:
+                bad.append((c["name"], rid, s, int(exists[p][l]), int(counts[p][l]), want))
+    assert not bad, bad[:5]
+    applicable = {rid: np.ones(len(cases), bool) for rid, _ in where}
+    for p, (rid, s) in enumerate(where):
+        applicable[rid] &= exists[p] > 0
+    for rid, app in applicable.items():
+        want = np.array([all(n > 0 for n in c["ematch"][rid]["source_counts"]) for c in cases])
+        assert np.array_equal(app, want), rid

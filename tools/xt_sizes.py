@@ -8,7 +8,7 @@ from paper_2410_05534_b200 import native
 from paper_2410_05534_b200.arena import Batch
 from paper_2410_05534_b200.pipeline import LeafPipeline
 
-leaves, symarr, name_id, code, ref, meta = bench.load_leaves("nasrnn")
+leaves, symarr, name_id, code, ref, meta = bench.load_leaves(sys.argv[1] if len(sys.argv) > 1 else "nasrnn")
 sizes = np.array([lf.n for lf in leaves])
 order = np.argsort(sizes)
 ctx = native.Context(0)
