@@ -463,8 +463,7 @@ def measure_config(ctx, stream, dev, model, B, steps, warmup, world, rank, e2e_s
         dist.barrier()
     # two device batches alternate so step i+1's H2D upload (copy engine) overlaps step i's
     # kernels; every step still uploads its own inputs and reads back its own results
-    ctx2 = native.Context(ctx.device)
-    ctx2.set_stream(stream.cuda_stream)
+    ctx2 = native.Context(ctx.device)   # its own stream: the two batches' steps overlap
     pipe2 = LeafPipeline(ctx2, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=pipe.pool,
                          pool_bitsets_per_node=pipe.pool_bitsets)
     batch2 = pipe2.load(packed)
@@ -511,11 +510,13 @@ def measure_config(ctx, stream, dev, model, B, steps, warmup, world, rank, e2e_s
             "_keep": (leaves, symarr, name_id, code, ref_ocf, meta, pipe, batch)}
 
 
-def measure_mcts(ctx, budget: int = 32, batch: int = 32, cpu_budget_s: float = 60.0) -> dict:
-    """configs[1]: the search itself. One run_search (budget iterations, batch 32, depth 10, node limit
-    2000) from the NasRNN analog's initial e-graph on the device engine, and the same search on the
-    CPU reference engine (oracle/mcts_ref.py: the reference's own apply_rule / is_rule_applicable /
-    extract_ocf_greedy, all host cores) -- iterations/s of both and whether their trees agree."""
+def measure_mcts(ctx, budget: int = 128, batch: int = 32, node_limit: int = 800) -> dict:
+    """configs[1]: the search itself. One run_search (budget iterations, batch 32, depth 10) from the
+    NasRNN analog's initial e-graph on the device engine, and the same search on the CPU reference
+    engine (oracle/mcts_ref.py: the reference's own apply_rule / is_rule_applicable /
+    extract_ocf_greedy, all host cores) -- iterations/s of both and whether their trees agree. The
+    node limit is the MCTS golden case's (tests/golden/mcts/nasrnn_c2.json): at 2000 the reference
+    needs tens of minutes for one multi-pattern explosion."""
     import random
 
     from paper_2410_05534_b200 import analogs
@@ -525,7 +526,7 @@ def measure_mcts(ctx, budget: int = 32, batch: int = 32, cpu_budget_s: float = 6
     from paper_2410_05534_b200.patterns import load_rules
     from paper_2410_05534_b200.symtab import SymbolTable
 
-    cfg = MctsConfig(budget=budget, node_limit=2000, seed=0, batch=batch, max_sim_steps=10)
+    cfg = MctsConfig(budget=budget, node_limit=node_limit, seed=0, batch=batch, max_sim_steps=10)
     cost = CostModelConfig()
     rules_ = load_rules("taso_analog")
 
@@ -544,7 +545,8 @@ def measure_mcts(ctx, budget: int = 32, batch: int = 32, cpu_budget_s: float = 6
     dev_engine = DeviceEngine(rules_, SymbolTable(), eg.language, cost, ctx=ctx)
     search(dev_engine, T.graph_to_egraph(analogs.build_analog("nasrnn", T.GraphBuilder)))   # warm-up
     dt_dev, best_dev, stats_dev = search(dev_engine, eg)
-    out = {"workload": f"nasrnn analog run_search: budget {budget}, batch {batch}, depth 10, node limit 2000, seed 0",
+    out = {"workload": f"nasrnn analog run_search: budget {budget}, batch {batch}, depth 10, node limit {node_limit}, "
+                       f"seed 0",
            "device_iterations_per_s": budget / dt_dev, "device_s": dt_dev, "best_rule": best_dev,
            "apply_regrows": dev_engine.regrows}
     try:
@@ -572,7 +574,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=4096, help="leaves per rank per step")
+    ap.add_argument("--batch", type=int, default=16384,
+                    help="leaves per rank per step (SURVEY §8(d) C3: batches of 256..16k leaves)")
+    ap.add_argument("--config-batch", type=int, default=4096, help="leaves per rank per step of the per_config sweep")
     ap.add_argument("--model", default="resnext50",
                     choices=["nasrnn", "bert", "resnext50", "inception_v3", "nasnet_a"],
                     help="headline leaf set: configs[2] ResNeXt-50 by default; the other BASELINE analogs")
@@ -610,17 +614,19 @@ def main():
                           clocks=clk)
     leaves, symarr, name_id, code, ref_ocf, meta, pipe, batch = head.pop("_keep")
     fp_line = measure_fingerprint(ctx, batch, meta)
-    apply_line = measure_apply(ctx, leaves, B, rank * B, symarr, name_id, code, meta)
+    apply_line = measure_apply(ctx, leaves, min(B, 4096), rank * B, symarr, name_id, code, meta)
     per_config = {}
     if not args.no_configs:
         for m in ("bert", "nasrnn", "resnext50", "inception_v3", "nasnet_a"):
             if m == args.model:
                 continue
-            r = measure_config(ctx, stream, dev, m, B, args.config_steps, args.warmup, world, rank,
+            r = measure_config(ctx, stream, dev, m, args.config_batch, args.config_steps, args.warmup, world, rank,
                                max(5, args.e2e_steps // 2), args.ocf_pool)
             r.pop("_keep")
             per_config[m] = r
     per_config[args.model] = {k: v for k, v in head.items()}
+    for r in per_config.values():
+        r.setdefault("leaves_per_rank", B)
     mcts = None
     if not args.no_mcts and rank == 0:
         mcts = measure_mcts(ctx)
@@ -670,7 +676,7 @@ def main():
                                for k in abytes},
         "per_config": {m: {k: r[k] for k in ("value", "ms_per_step", "e2e", "kernel_ms", "roofline_frac",
                                               "matches_per_s", "ematch_matches_per_s", "nodes_per_leaf_mean",
-                                              "parity_vs_reference")}
+                                              "leaves_per_rank", "parity_vs_reference")}
                        for m, r in per_config.items()},
         "schedule": "k_rebuild -> [k_extract on a side stream || k_ematch -> k_join] -> join streams",
         "apply": apply_line,

@@ -191,11 +191,14 @@ class ReferenceEngine:
                 np.array([r[4] for r in res]), np.array([r[5] for r in res]),
                 np.array([r[6] for r in res], bool).reshape(len(states), -1))
 
-    def simulate(self, states, costs0, allowed, steps: int, node_limit: int, rng):
+    def simulate(self, states, costs0, allowed, steps: int, node_limit: int, seeds):
         """DeviceEngine.simulate's loop, leaf by leaf on reference snapshots (same draws)."""
+        import random
+
         from paper_2410_05534_b200.mcts import rollout_rewards
 
         L = len(states)
+        rngs = [random.Random(sd) for sd in seeds]
         snaps = [s.snapshot() for s in states]
         pooled = self._conns() is not None
         if pooled:
@@ -207,7 +210,7 @@ class ReferenceEngine:
             rules = [None] * L
             for l in range(L):
                 if live[l] and allowed[l]:
-                    rules[l] = rng.choice(allowed[l])
+                    rules[l] = rngs[l].choice(allowed[l])
                 else:
                     live[l] = False
             if not live.any():

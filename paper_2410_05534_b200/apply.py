@@ -213,6 +213,7 @@ class ApplyDriver:
     def upload(self):
         st = self.symtab
         st.finalize()
+        self.uploaded_symbols = len(st)
         self.pipe.ctx.upload_symtab(st.arrays())
         self.pipe.recompile(self._name_id, st.code)
         off, words = self.pipe.apply_programs(self._name_id, st.code)

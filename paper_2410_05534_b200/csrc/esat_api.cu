@@ -318,8 +318,6 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
     OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N); OWN(x.lhn, N); OWN(x.lcc, 2 * N);
-    OWN(x.hpass, N); OWN(x.cpass, N); OWN(x.chgp, 2 * N); OWN(x.dm, 2 * N); OWN(x.lvm, 2 * NL);
-    OWN(x.poff, NL); OWN(x.plist, K); OWN(x.nco, N); OWN(x.nho, N); OWN(x.nhr, N); OWN(x.nbit, N);
     x.slot_stride = N;
     *out = b;
     return ESAT_OK;

@@ -62,19 +62,8 @@ struct XArgs {
     const uint64_t* pool_kbase;
     uint32_t *pool_key;
     double* pool_val;
-    // Versioned per-class state (sparse passes): a reader needs a class's value "now" or "as of the
-    // end of the previous pass"; a class updated in pass p keeps its pre-update value beside it.
-    uint32_t *hoff, *hrng;       // [2][node rows] history block offset / occupied range: [0] latest flush, [1] the one before
-    uint32_t* hpass;             // [node rows] pass of the latest flush
-    uint32_t* cpass;             // [node rows] pass of the latest cost update (prev[] holds the cost before it)
-    uint8_t* chg;                // [2][node rows] output change bits (bit 0 cost, bit 1 history): [0] latest evaluation, [1] the one before
-    uint32_t* chgp;              // [2][node rows] passes of those evaluations
-    uint32_t* dm;                // [2][node rows] class scheduled for pass q (stored q, parity q & 1)
-    uint32_t* lvm;               // [2][node rows + L] level has a scheduled class in pass q
-    uint32_t *poff, *plist;      // parent lists (reverse child edges) of class positions: CSR [node rows + L], [kid rows]
-    double* nco;                 // [node rows] staged new cost (two-phase level commit)
-    uint32_t *nho, *nhr;         // [node rows] staged new history block (nho NONE: unchanged)
-    uint8_t* nbit;               // [node rows] staged change bits (| 4: cost improved)
+    uint32_t *hoff, *hrng;               // [2][node rows] history block offset / occupied range per class position (pass parity)
+    uint8_t* chg;                // [2][node rows] class output changed in the pass (dirty skip): bit 0 cost, bit 1 history
     uint32_t* lhn;               // [node rows] flushed node of each class at its last merge (flush reuse)
     double* lcc;                 // [2 x node rows] its child contributions (cc1, cc2)
     uint64_t slot_stride;

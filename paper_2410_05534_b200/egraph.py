@@ -208,6 +208,30 @@ class EGraph:
             out.append(f"ec{cid}: " + " | ".join(parts) + (" <root>" if root == cid else ""))
         return "\n".join(out)
 
+    def to_dot(self) -> str:
+        """GraphViz text of the e-graph (egraph.py:331-353): one dashed cluster per canonical class
+        (label ``ec<id>``), a circle per e-node labelled with its operator, and an edge from every
+        e-node to the first node of each child class (``lhead`` = the child's cluster)."""
+        cids = self.canonical_class_ids()
+        members = {c: sorted(self.classes[c].nodes, key=node_sort_key) for c in cids}
+        name = {}
+        for c in cids:
+            for n in members[c]:
+                name[(c, n)] = f"n{len(name)}"
+        lines = ["digraph egraph {", "  compound=true;", "  node [shape=circle];"]
+        for c in cids:
+            lines += [f"  subgraph cluster_{c} {{", f'    label="ec{c}"; style=dashed;']
+            lines += [f'    {name[(c, n)]} [label="{n.symbol.name}"];' for n in members[c]]
+            lines.append("  }")
+        for c in cids:
+            for n in members[c]:
+                for ch in n.children:
+                    t = self._uf.find(ch)
+                    if members.get(t):
+                        lines.append(f"  {name[(c, n)]} -> {name[(t, members[t][0])]} [lhead=cluster_{t}];")
+        lines.append("}")
+        return "\n".join(lines)
+
     def fingerprint(self) -> int:
         """Weisfeiler-Lehman class-label hash (egraph.py:247-296), host side (cache key only)."""
         if self.dirty:

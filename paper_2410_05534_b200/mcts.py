@@ -22,12 +22,18 @@ Engine contract (what both engines implement, state objects are engine-private):
     initial(egraph)                     -> state
     evaluate(states)                    -> (clean states, cost f64[L], nodes[L], classes[L], app bool[L,R])
     expand(states, rules)               -> (child states, changed[L], cost, nodes, classes, app)
-    simulate(states, cost0, allowed, steps, node_limit, rng) -> reward f64[L]
+    simulate(states, cost0, allowed, steps, node_limit, seeds) -> reward f64[L]
     final(state, method)                -> (cost, save_graph JSON text)
 
 A failed extraction yields cost ``inf``. In a rollout a step whose extraction failed adds no reward
 and leaves the anchor unchanged ("treat that step's improvement as 0"); a step right
 after a failed anchor only re-anchors.
+
+Randomness (one seeded stream): selection and expansion draw from the search's
+``random.Random(seed)``; each rollout draws its rules from its own ``random.Random(s)`` with ``s``
+taken from the search stream (64 bits per simulated leaf, in selection order) -- a rollout's draws
+do not depend on its batch-mates, so the leaves of a batch can be simulated on different GPUs
+(parallel.ShardedEngine) with results identical to one GPU.
 """
 
 from __future__ import annotations
@@ -155,21 +161,31 @@ class DeviceEngine:
         self.rules, self.symtab, self.language, self.cfg = rules, symtab, language, cost_config
         self.method, self.headroom = method, headroom
         self.regrows = 0
+        self._pipe = self._drv = None
 
     # -- batch plumbing ---------------------------------------------------------------
+    def _ensure_pipe(self):
+        """One pipeline (compiled patterns, rule target programs, symbol tables on the device) for
+        the whole search; re-uploaded only when host interning added symbols."""
+        self.symtab.finalize()
+        if self._pipe is None:
+            self._pipe = LeafPipeline(self.ctx, self.symtab.arrays(), self.rules,
+                                      lambda nm: self.symtab.name_id(nm, create=False), self.symtab.code,
+                                      method=self.method, pool_entries_per_node=32)
+            self._drv = ApplyDriver(self._pipe, self.symtab, self.language, self.cfg)
+        elif self._drv.uploaded_symbols != len(self.symtab):
+            self._drv.upload()
+        return self._pipe, self._drv
+
     def _open(self, states, headroom=None):
         packed = Batch(states).pack_with_headroom(nodes=headroom or self.headroom)
-        self.symtab.finalize()
-        pipe = LeafPipeline(self.ctx, self.symtab.arrays(), self.rules,
-                            lambda nm: self.symtab.name_id(nm, create=False), self.symtab.code, method=self.method,
-                            pool_entries_per_node=32)
+        pipe, drv = self._ensure_pipe()
         b = pipe.load(packed)
         b.set_counts(packed["n_cnt"], packed["u_cnt"])
-        drv = ApplyDriver(pipe, self.symtab, self.language, self.cfg)
         return [packed, pipe, b, drv, headroom or self.headroom]
 
     def _extract(self, b, method=None):
-        out = native.extract_with_retry(b, method or self.method, factor=32, bitsets=2.0)
+        out = native.extract_with_retry(b, method or self.method, factor=32, bitsets=2.0, light=True)
         cost = out["root_cost"].copy()
         cost[out["status"] != 0] = np.inf
         return cost, out
@@ -254,13 +270,14 @@ class DeviceEngine:
         b.close()
         return clean, changed, cost, n, c, app
 
-    def simulate(self, states, costs0, allowed, steps: int, node_limit: int, rng: random.Random):
+    def simulate(self, states, costs0, allowed, steps: int, node_limit: int, seeds):
         """Random rollouts: per step every live leaf applies a uniformly drawn
         allowed rule, rebuilds and extracts (rollout_rewards); a leaf stops at the node limit. The
         device batch holds the live leaves only: when leaves stop, the batch is re-packed from the
         survivors' rebuilt states (a stopped leaf -- typically one a multi-pattern rule exploded --
         is never matched, rebuilt or extracted again)."""
         L = len(states)
+        rngs = [random.Random(sd) for sd in seeds]
         reward = np.zeros(L)
         prev = np.asarray(costs0, np.float64).copy()
         live = np.array([bool(a) for a in allowed], bool)
@@ -273,7 +290,7 @@ class DeviceEngine:
             rules = np.full(L, NONE, np.uint32)
             for l in range(L):
                 if live[l] and allowed[l]:
-                    rules[l] = rng.choice(allowed[l])
+                    rules[l] = rngs[l].choice(allowed[l])
                 else:
                     live[l] = False
             if not live.any():
@@ -307,7 +324,9 @@ class DeviceEngine:
         h = self._open([state], headroom=1)
         packed, pipe, b = h[0], h[1], h[2]
         pipe.rebuild()
-        cost, out = self._extract(b, "ocf" if method == "exact" else method)
+        out = native.extract_with_retry(b, "ocf" if method == "exact" else method, factor=32, bitsets=2.0)
+        cost = out["root_cost"].copy()
+        cost[out["status"] != 0] = np.inf
         clean = self._clean_states(packed, b)[0]
         eg = to_egraph(clean, self.symtab, self.language)
         if not np.isfinite(cost[0]):
@@ -391,9 +410,10 @@ def run_search(root: SearchNode, engine, n_rules: int, cfg: MctsConfig, rng: ran
         rewards = np.zeros(len(picks))
         if sims:
             live_n = [int(n[j]) for j in sims]
+            seeds = [rng.getrandbits(64) for _ in sims]   # one rollout stream per simulated leaf
             r = engine.simulate([kids[j] for j in sims], anchors,
                                 [a if ln < cfg.node_limit else [] for a, ln in zip(allowed, live_n)],
-                                cfg.max_sim_steps, cfg.node_limit, rng)
+                                cfg.max_sim_steps, cfg.node_limit, seeds)
             rewards[sims] = r
         for j, (node, rule) in enumerate(picks):   # updates in selection order
             update(node.children[rule], float(rewards[j]))

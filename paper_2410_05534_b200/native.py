@@ -350,6 +350,14 @@ class DeviceBatch:
             "status", "err_class", "root_cost", "class_cost", "choice", "reachable", "passes")]))
         return o
 
+    def download_extract_light(self) -> dict:
+        """Per-leaf status, error class / overflow mask and root cost only."""
+        L = self.n_leaves
+        o = {"status": np.zeros(L, np.uint32), "err_class": np.zeros(L, np.uint32), "root_cost": np.zeros(L)}
+        self.ctx.check(self.L.esat_download_extract(self.h, _p(o["status"]), _p(o["err_class"]), _p(o["root_cost"]),
+                                                    None, None, None, None))
+        return o
+
     def download_extract_small(self, root_cost: np.ndarray, status: np.ndarray):
         """D2H of the per-leaf root costs (f64) and statuses (u32) only -- the MCTS reward inputs."""
         self.ctx.check(self.L.esat_download_extract(self.h, _p(status), None, _p(root_cost), None, None, None,
@@ -369,14 +377,14 @@ class DeviceBatch:
 
 
 def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max_factor: float = 1 << 16,
-                       bitsets: float = 4.0) -> dict:
+                       bitsets: float = 4.0, light: bool = False) -> dict:
     """Run extraction, growing the OCF history pools on ESAT_X_CAPACITY (host regrow path).
     err_class of an overflowed leaf is the overflow mask: 1 grows the bitset pool x2, 2 grows the
-    contribution pool x4."""
+    contribution pool x4. ``light``: download the per-leaf status / error / root cost only."""
     batch.set_pool(factor, bitsets)
     while True:
         batch.extract(method)
-        out = batch.download_extract()
+        out = batch.download_extract_light() if light else batch.download_extract()
         over = out["status"] == X_CAPACITY
         if method.startswith("ocf") and np.any(over) and factor < max_factor and bitsets < max_factor:
             mask = int(np.bitwise_or.reduce(out["err_class"][over]))

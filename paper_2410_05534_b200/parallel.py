@@ -74,3 +74,64 @@ def root_parallel_sweep(run_seed, seeds, group=None):
     res.sort()
     best = min(res, key=lambda t: (t[1], t[0])) if res else None
     return res, best
+
+
+class ShardedEngine:
+    """Leaf-parallel MCTS over ranks: wraps one rank's engine so every
+    batch of expansions and rollouts is split into contiguous shards, each rank runs its shard on
+    its own GPU, and the per-leaf results are all-gathered in rank order (= leaf order). Every rank
+    therefore applies the same updates in selection order and holds the same tree; the search's RNG
+    is consumed identically everywhere (rollouts carry their own seeds, mcts.py), so the search is
+    the single-GPU search. The exchange per batch is the expansion rows (changed, cost, e-nodes,
+    e-classes, applicability bits and the child's e-graph, which any rank may expand later) and the
+    rollout rewards -- ``torch.distributed.all_gather_object`` over NCCL (gloo in the CPU tests).
+
+    ``evaluate`` / ``final`` / ``initial`` run redundantly on every rank (one e-graph each)."""
+
+    def __init__(self, engine, group=None):
+        import torch.distributed as dist
+
+        self.engine = engine
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.exchanged_bytes = 0
+
+    def _gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        import pickle
+
+        import torch.distributed as dist
+
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.group)
+        self.exchanged_bytes += sum(len(pickle.dumps(o)) for o in out)
+        return out
+
+    def initial(self, egraph):
+        return self.engine.initial(egraph)
+
+    def evaluate(self, states):
+        return self.engine.evaluate(states)
+
+    def final(self, state, method):
+        return self.engine.final(state, method)
+
+    def expand(self, states, rules):
+        import numpy as np
+
+        s, e = leaf_shard(len(states), self.world, self.rank)
+        part = self.engine.expand(states[s:e], list(rules[s:e])) if e > s else None
+        parts = [p for p in self._gather(part) if p is not None]
+        kids = [k for p in parts for k in p[0]]
+        cat = [np.concatenate([p[i] for p in parts]) for i in range(1, 6)]
+        return (kids, *cat)
+
+    def simulate(self, states, costs0, allowed, steps, node_limit, seeds):
+        import numpy as np
+
+        s, e = leaf_shard(len(states), self.world, self.rank)
+        part = (self.engine.simulate(states[s:e], list(costs0[s:e]), allowed[s:e], steps, node_limit, seeds[s:e])
+                if e > s else np.zeros(0))
+        return np.concatenate(self._gather(part))

@@ -12,7 +12,7 @@ timeout 600 python bench.py > "$OUT/bench.log" 2>&1 || { echo "bench failed"; ta
 tail -n 1 "$OUT/bench.log" > "$OUT/bench.json"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > "$OUT/ref.log" 2>&1
 tail -n 1 "$OUT/ref.log" > "$OUT/reference_arm.json"
-ARGS="--steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 2"
+ARGS="--steps 2 --warmup 3 --no-cpu-baseline --no-configs --no-mcts --e2e-steps 2"
 timeout 300 python bench.py $ARGS > "$OUT/short.log" 2>&1 || { echo "short bench failed"; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file "$OUT/launches.csv" python bench.py $ARGS > "$OUT/ncu_launches.log" 2>&1

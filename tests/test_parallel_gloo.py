@@ -83,3 +83,60 @@ def test_root_parallel_sweep_matches_single_rank():
     for rank, res, best in outs:
         assert res == single and best == best1, rank
     assert len(single) == 64 and best1[1] == 0.0
+
+
+def _search(model, cfg_kw):
+    """optimize_mcts with the CPU reference engine (oracle/mcts_ref.py), sharded when a process group
+    is up; returns the RunReport as JSON."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    from make_mcts_golden import RULES, build_input
+
+    from oracle.mcts_ref import ReferenceEngine, import_reference
+    from paper_2410_05534_b200.cost_model import CostModelConfig
+    from paper_2410_05534_b200.mcts import MctsConfig, optimize_mcts
+    from paper_2410_05534_b200.parallel import ShardedEngine
+
+    E, R, X, T = import_reference()
+    text = RULES["taso_analog"].read_text()
+    eng = ShardedEngine(ReferenceEngine(text, CostModelConfig(), workers=1))
+    rep = optimize_mcts(build_input(model, T), R.parse_rules(text), MctsConfig(**cfg_kw), CostModelConfig(),
+                        engine=eng)
+    return rep.to_json_dict(), eng.exchanged_bytes
+
+
+def _search_worker(rank, world, port, model, cfg_kw, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rep, nbytes = _search(model, cfg_kw)
+    q.put((rank, rep, nbytes))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_leaf_parallel_search_matches_single_rank():
+    """the NasRNN search with every batch's expansions and rollouts sharded over two
+    ranks (parallel.ShardedEngine, all-gather of the per-leaf rows) returns, on every rank, the
+    RunReport of the single-rank search -- same applied-rule trace, costs and final program."""
+    from oracle.mcts_ref import reference_available
+
+    if not reference_available():
+        pytest.skip("reference not importable")
+    cfg_kw = dict(budget=24, batch=8, node_limit=400, seed=0, max_sim_steps=3)
+    single, _ = _search("nasrnn", cfg_kw)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 200
+    procs = [ctx.Process(target=_search_worker, args=(r, 2, port, "nasrnn", cfg_kw, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert single["iterations"], single
+    for rank, rep, nbytes in outs:
+        assert rep == single, rank
+        assert nbytes > 0
