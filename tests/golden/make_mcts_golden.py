@@ -31,7 +31,8 @@ RULES = {"taso_analog": REPO / "paper_2410_05534_b200" / "rules" / "taso_analog.
 CASES = {
     "toy_b1": ("toy", "toy_math", "term", dict(budget=64, node_limit=10, seed=0, batch=1, final_extractor="ocf")),
     "toy_b8": ("toy", "toy_math", "term", dict(budget=64, node_limit=10, seed=1, batch=8, final_extractor="exact")),
-    "bert_c1_b1": ("bert", "taso_analog", "analytic", dict(budget=16, node_limit=500, seed=0, batch=1)),
+    "bert_c1_b1": ("bert", "taso_analog", "analytic", dict(budget=8, node_limit=500, seed=0, batch=1,
+                                                          max_sim_steps=4)),
     "bert_c1": ("bert", "taso_analog", "analytic", dict(budget=128, node_limit=500, seed=0, batch=32)),
     # reduced budgets ("a committed reduced budget if runtime forces it"): the reference's
     # apply_rule needs tens of minutes for one application of the #128 / #138-analog multi-pattern
