@@ -9,7 +9,7 @@
 #include "esat_internal.cuh"
 
 namespace esat {
-template <int T> __global__ void k_rebuild(Dev);
+template <int T> __global__ void k_rebuild(Dev, uint32_t);
 template <int T> __global__ void k_extract(Dev, XArgs);
 }  // namespace esat
 #include "k_ematch_args.cuh"
@@ -147,11 +147,18 @@ struct esat_batch {
 
 namespace {
 
+// Batch buffers come from the device's stream-ordered memory pool (cudaMallocAsync, release
+// threshold raised at context creation): a batch per MCTS call is created and destroyed without
+// the device-wide synchronisation and unmapping of cudaMalloc / cudaFree.
+static inline void afree(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 template <typename T>
 int own(esat_batch* b, T** p, size_t n) {
     *p = nullptr;
     // +64 B: TMA bulk copies read 16-B aligned spans that may round past the last element
-    CK(b->ctx, cudaMalloc((void**)p, sizeof(T) * (n ? n : 1) + 64));
+    CK(b->ctx, cudaMallocAsync((void**)p, sizeof(T) * (n ? n : 1) + 64, b->ctx->stream));
     b->owned.push_back((void*)*p);
     return ESAT_OK;
 }
@@ -191,6 +198,12 @@ int esat_ctx_create(int device, esat_ctx** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev_s0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev_s1);
+    if (e == cudaSuccess) {   // keep freed batch memory in the device pool (stream-ordered reuse)
+        cudaMemPool_t pool;
+        e = cudaDeviceGetDefaultMemPool(&pool, device);
+        uint64_t keep = ~0ull;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     if (e != cudaSuccess) {
         *out = nullptr;
         delete c;
@@ -325,13 +338,16 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
 
 int esat_batch_destroy(esat_batch* b) {
     if (!b) return ESAT_OK;
-    cudaSetDevice(b->ctx->device);
-    for (void* p : b->owned) cudaFree(p);
-    cudaFree(b->d_pb); cudaFree(b->d_pbk); cudaFree(b->pool_key); cudaFree(b->pool_val);
-    cudaFree(b->d_lmask);
-    cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_W); cudaFree(b->d_j_count);
-    cudaFree(b->d_m_off); cudaFree(b->d_j_off); cudaFree(b->stage); cudaFree(b->m_out); cudaFree(b->j_out);
-    cudaFree(b->d_over); cudaFree(b->j_gkeys); cudaFree(b->j_gsort); cudaFree(b->j_big); cudaFree(b->d_tops); cudaFree(b->d_jspec); cudaFree(b->d_raw);
+    esat_ctx* c = b->ctx;
+    cudaSetDevice(c->device);
+    if (c->side) cudaStreamSynchronize(c->side);   // an extraction of this batch may still run there
+    cudaStream_t s = c->stream;
+    for (void* p : b->owned) afree(p, s);
+    afree(b->d_pb, c->stream); afree(b->d_pbk, c->stream); afree(b->pool_key, c->stream); afree(b->pool_val, c->stream);
+    afree(b->d_lmask, c->stream);
+    afree(b->d_pat_ids, c->stream); afree(b->d_m_count, c->stream); afree(b->d_m_W, c->stream); afree(b->d_j_count, c->stream);
+    afree(b->d_m_off, c->stream); afree(b->d_j_off, c->stream); afree(b->stage, c->stream); afree(b->m_out, c->stream); afree(b->j_out, c->stream);
+    afree(b->d_over, c->stream); afree(b->j_gkeys, c->stream); afree(b->j_gsort, c->stream); afree(b->j_big, c->stream); afree(b->d_tops, c->stream); afree(b->d_jspec, c->stream); afree(b->d_raw, c->stream);
     delete b;
     return ESAT_OK;
 }
@@ -371,7 +387,11 @@ int esat_rebuild(esat_batch* b) {
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
     d.sym_par = c->sym_par; d.n_syms = c->n_syms;
     tic(c);
-    if (b->L) k_rebuild<256><<<b->L, 256, 0, c->stream>>>(d);
+    // the pass's two hash tables live in shared memory (16-bit positions) for leaves with
+    // 2 * next_pow2(2n) <= REBUILD_SMEM_SLOTS entries (n <= 4096); larger leaves use global scratch
+    constexpr uint32_t REBUILD_SMEM_SLOTS = 16384;   // 32 KB
+    static const uint32_t slots = getenv("ESAT_REBUILD_GLOBAL_TABLES") ? 0u : REBUILD_SMEM_SLOTS;
+    if (b->L) k_rebuild<256><<<b->L, 256, 2 * slots, c->stream>>>(d, slots);
     toc(c);
     int r = launch_check(c, "k_rebuild");
     if (r) return r;
@@ -424,19 +444,19 @@ static int ensure_pool(esat_batch* b) {
     if (b->d_pb && pb == b->pb && pbk == b->pbk && b->pool_total >= pb[L] && b->pool_ktotal >= pbk[L])
         return ESAT_OK;
     if (!b->d_pb) {
-        CK(c, cudaMalloc((void**)&b->d_pb, 8ull * (L + 1)));
-        CK(c, cudaMalloc((void**)&b->d_pbk, 8ull * (L + 1)));
+        CK(c, cudaMallocAsync((void**)&b->d_pb, 8ull * (L + 1), c->stream));
+        CK(c, cudaMallocAsync((void**)&b->d_pbk, 8ull * (L + 1), c->stream));
     }
     if (b->pool_total < pb[L] || b->pool_ktotal < pbk[L]) {
         const uint64_t want = pb[L] > b->pool_total ? pb[L] : b->pool_total;
         const uint64_t kwant = pbk[L] > b->pool_ktotal ? pbk[L] : b->pool_ktotal;
         CK(c, cudaStreamSynchronize(c->stream));
         if (c->side) CK(c, cudaStreamSynchronize(c->side));
-        cudaFree(b->pool_key); cudaFree(b->pool_val);
+        afree(b->pool_key, c->stream); afree(b->pool_val, c->stream);
         b->pool_key = nullptr; b->pool_val = nullptr;
         b->pool_total = 0; b->pool_ktotal = 0;
-        CK(c, cudaMalloc((void**)&b->pool_key, 4ull * kwant + 64));
-        CK(c, cudaMalloc((void**)&b->pool_val, 8ull * want + 64));
+        CK(c, cudaMallocAsync((void**)&b->pool_key, 4ull * kwant + 64, c->stream));
+        CK(c, cudaMallocAsync((void**)&b->pool_val, 8ull * want + 64, c->stream));
         b->pool_total = want;
         b->pool_ktotal = kwant;
     }
@@ -627,17 +647,17 @@ template <typename T>
 int regrow(esat_ctx* c, T** p, uint64_t* cap, uint64_t need) {
     if (*cap >= need && *p) return ESAT_OK;
     uint64_t n = need + need / 4 + 1024;
-    cudaFree(*p);
+    afree(*p, c->stream);
     *p = nullptr;
-    CK(c, cudaMalloc((void**)p, sizeof(T) * n));
+    CK(c, cudaMallocAsync((void**)p, sizeof(T) * n, c->stream));
     *cap = n;
     return ESAT_OK;
 }
 
 int ensure_match_meta(esat_batch* b) {
     esat_ctx* c = b->ctx;
-    if (!b->d_tops) CK(c, cudaMalloc((void**)&b->d_tops, 8 * sizeof(unsigned long long)));
-    if (!b->d_over) CK(c, cudaMalloc((void**)&b->d_over, 2 * sizeof(uint32_t)));
+    if (!b->d_tops) CK(c, cudaMallocAsync((void**)&b->d_tops, 8 * sizeof(unsigned long long), c->stream));
+    if (!b->d_over) CK(c, cudaMallocAsync((void**)&b->d_over, 2 * sizeof(uint32_t), c->stream));
     return ESAT_OK;
 }
 
@@ -745,12 +765,12 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
     sig.push_back(c->sym_gen);
     if (sig != b->m_sig) {
         if (P > b->m_Pcap) {
-            cudaFree(b->d_pat_ids); cudaFree(b->d_m_count); cudaFree(b->d_m_off); cudaFree(b->d_m_W);
+            afree(b->d_pat_ids, c->stream); afree(b->d_m_count, c->stream); afree(b->d_m_off, c->stream); afree(b->d_m_W, c->stream);
             b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
-            CK(c, cudaMalloc((void**)&b->d_pat_ids, 4ull * 32));
-            CK(c, cudaMalloc((void**)&b->d_m_count, 4ull * 32 * (L ? L : 1)));
-            CK(c, cudaMalloc((void**)&b->d_m_off, 8ull * 32 * (L ? L : 1)));
-            CK(c, cudaMalloc((void**)&b->d_m_W, 4ull * 32));
+            CK(c, cudaMallocAsync((void**)&b->d_pat_ids, 4ull * 32, c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_count, 4ull * 32 * (L ? L : 1), c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_off, 8ull * 32 * (L ? L : 1), c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_W, 4ull * 32, c->stream));
             b->m_Pcap = 32;
         }
         b->m_W.resize(P);
@@ -762,7 +782,7 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
         }
         CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
         CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
-        if (!b->d_raw) CK(c, cudaMalloc((void**)&b->d_raw, 8ull * (b->N + 1) * 32 + 64));   // [leaf][32][C] counts + work list
+        if (!b->d_raw) CK(c, cudaMallocAsync((void**)&b->d_raw, 8ull * (b->N + 1) * 32 + 64, c->stream));   // [leaf][32][C] counts + work list
         if (!b->stage_cap) {
             if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
             if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
@@ -781,7 +801,7 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
         b->m_sized = false;
     }
     if (leaf_mask) {
-        if (!b->d_lmask) CK(c, cudaMalloc((void**)&b->d_lmask, 4ull * (L ? L : 1)));
+        if (!b->d_lmask) CK(c, cudaMallocAsync((void**)&b->d_lmask, 4ull * (L ? L : 1), c->stream));
         CK(c, cudaMemcpyAsync(b->d_lmask, leaf_mask, 4ull * L, cudaMemcpyHostToDevice, c->stream));
     }
     b->lmask_on = leaf_mask != nullptr;
@@ -918,10 +938,10 @@ int esat_join(esat_batch* b, uint32_t R, const uint32_t* src_off, const uint32_t
         if ((r_ = regrow(c, &b->d_jspec, &b->jspec_cap, spec.size()))) return r_;
         CK(c, cudaMemcpyAsync(b->d_jspec, spec.data(), 4 * spec.size(), cudaMemcpyHostToDevice, c->stream));
         if (R > b->j_Rcap) {
-            cudaFree(b->d_j_count); cudaFree(b->d_j_off);
+            afree(b->d_j_count, c->stream); afree(b->d_j_off, c->stream);
             b->d_j_count = nullptr; b->d_j_off = nullptr;
-            CK(c, cudaMalloc((void**)&b->d_j_count, 4ull * R * (L ? L : 1)));
-            CK(c, cudaMalloc((void**)&b->d_j_off, 8ull * R * (L ? L : 1)));
+            CK(c, cudaMallocAsync((void**)&b->d_j_count, 4ull * R * (L ? L : 1), c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_j_off, 8ull * R * (L ? L : 1), c->stream));
             b->j_Rcap = R;
         }
         if (!b->j_cap && (r_ = regrow(c, &b->j_out, &b->j_cap, 4 * b->N + 4096))) return r_;

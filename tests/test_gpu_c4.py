@@ -75,5 +75,16 @@ def test_c4_full_size_vs_oracle(c4):
     rec = w[: int(off[-1])].reshape(-1, W)
     _, sizes = np.unique(rec[:, 2:], axis=0, return_counts=True)
     assert int(counts[pipe.rules.index(conv), 0]) == int((sizes.astype(np.int64) ** 2).sum()) == 132828819
+    # element for element: the device's 132.8M joined records (4.25 GB) hash to the CPU oracle's
+    # (tests/golden/make_c4_join_hash.py; the oracle is pinned to the reference's joint_match)
+    import hashlib
+    import json
+    from pathlib import Path
+
+    want = json.loads((Path(__file__).resolve().parent / "golden" / "c4_join_sha256.json").read_text())
+    jw, joff, jcnt = b.download_matches(pipe.joins.index(conv), from_join=True)
+    assert int(jcnt[0]) == want["records"]
+    got = hashlib.sha256(np.ascontiguousarray(jw[: int(joff[-1])], np.uint32).tobytes()).hexdigest()
+    assert got == want["sha256_u32_le"]
     b.close()
     ctx.close()
