@@ -91,11 +91,11 @@ def _worker(conn, rules_text, cost_config, method):
             for l, eg in msg[1]:
                 leaves[l] = eg
             conn.send(None)
-        elif kind == "step":          # [(l, rule)] -> [(l, cost, n)]
+        elif kind == "step":          # [(l, rule, want fingerprint)] -> [(l, cost, n, fingerprint)]
             out = []
-            for l, rule in msg[1]:
+            for l, rule, want_fp in msg[1]:
                 ops.apply(leaves[l], rule)
-                out.append((l, ops.extract(leaves[l]), leaves[l].size()[0]))
+                out.append((l, ops.extract(leaves[l]), leaves[l].size()[0], leaves[l].fingerprint() if want_fp else 0))
             conn.send(out)
         elif kind == "expand":        # [(l, egraph, rule)] -> [(l, child, changed, cost, n, c, app)]
             out = []
@@ -116,6 +116,13 @@ class ReferenceEngine:
         self.rules_text, self.cfg, self.method = rules_text, cost_config, method
         self.workers = max(1, int(workers))
         self._pool = None
+        self.cache = None
+
+    def configure(self, cfg):
+        from paper_2410_05534_b200.mcts import ExtractionCache
+
+        self.method = self.ops.method = cfg.main_extractor
+        self.cache = ExtractionCache() if cfg.extraction_cache else None
 
     # -- worker pool (fork; leaves pinned to workers) ------------------------------------
     def _conns(self):
@@ -217,14 +224,19 @@ class ReferenceEngine:
                 break
             cost = np.full(L, math.inf)
             n = np.zeros(L, np.int64)
-            todo = [(l, rules[l]) for l in range(L) if live[l]]
+            fps = np.zeros(L, np.uint64)
+            todo = [(l, rules[l], self.cache is not None) for l in range(L) if live[l]]
             if pooled:
-                for l, cst, nn in self._scatter("step", todo):
-                    cost[l], n[l] = cst, nn
+                for l, cst, nn, fp in self._scatter("step", todo):
+                    cost[l], n[l], fps[l] = cst, nn, fp
             else:
-                for l, r in todo:
+                for l, r, _ in todo:
                     self.ops.apply(snaps[l], r)
                     cost[l], n[l] = self.ops.extract(snaps[l]), snaps[l].size()[0]
+                    if self.cache is not None:
+                        fps[l] = snaps[l].fingerprint()   # the reference's own WL hash (egraph.py:247)
+            if self.cache is not None:
+                cost = self.cache.resolve(fps, live, cost)
             rollout_rewards(reward, prev, live, cost)
             live &= n < node_limit
         if pooled:

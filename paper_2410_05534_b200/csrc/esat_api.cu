@@ -9,7 +9,7 @@
 #include "esat_internal.cuh"
 
 namespace esat {
-template <int T> __global__ void k_rebuild(Dev, uint32_t);
+template <int T> __global__ void k_rebuild(Dev);
 template <int T> __global__ void k_extract(Dev, XArgs);
 }  // namespace esat
 #include "k_ematch_args.cuh"
@@ -387,11 +387,7 @@ int esat_rebuild(esat_batch* b) {
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
     d.sym_par = c->sym_par; d.n_syms = c->n_syms;
     tic(c);
-    // the pass's two hash tables live in shared memory (16-bit positions) for leaves with
-    // 2 * next_pow2(2n) <= REBUILD_SMEM_SLOTS entries (n <= 4096); larger leaves use global scratch
-    constexpr uint32_t REBUILD_SMEM_SLOTS = 16384;   // 32 KB
-    static const uint32_t slots = getenv("ESAT_REBUILD_GLOBAL_TABLES") ? 0u : REBUILD_SMEM_SLOTS;
-    if (b->L) k_rebuild<256><<<b->L, 256, 2 * slots, c->stream>>>(d, slots);
+    if (b->L) k_rebuild<256><<<b->L, 256, 0, c->stream>>>(d);
     toc(c);
     int r = launch_check(c, "k_rebuild");
     if (r) return r;

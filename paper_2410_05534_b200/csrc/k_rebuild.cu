@@ -55,63 +55,23 @@ __device__ __forceinline__ bool node_less(const uint32_t* rank, const uint32_t* 
     return na < nb;
 }
 
-// A pass's two hash tables (committed Tc, speculative Ts): in shared memory as 16-bit positions
-// when the leaf is small enough (the common case: no DRAM traffic, SMEM latency on every probe),
-// else the leaf's global u32 scratch tables.
-struct Tab {
-    uint32_t* g;
-    unsigned short* s;
-    uint32_t mask;
-    bool sm;
-    static constexpr unsigned short NONE16 = 0xFFFFu;
-    __device__ __forceinline__ uint32_t ld(uint32_t i) const {
-        if (!sm) return g[i];
-        const uint32_t v = s[i];
-        return v == NONE16 ? NONE : v;
-    }
-    __device__ __forceinline__ void clear(uint32_t i) {
-        if (sm) s[i] = NONE16;
-        else g[i] = NONE;
-    }
-    // insert position v into an empty slot; returns the slot's previous content (NONE: inserted)
-    __device__ __forceinline__ uint32_t cas_empty(uint32_t i, uint32_t v) {
-        if (!sm) return atomicCAS(&g[i], NONE, v);
-        const unsigned short o = atomicCAS(&s[i], NONE16, (unsigned short)v);
-        return o == NONE16 ? NONE : (uint32_t)o;
-    }
-    __device__ __forceinline__ void amin(uint32_t i, uint32_t v) {
-        if (!sm) { atomicMin(&g[i], v); return; }
-        unsigned short old = s[i];
-        while (v < old) {
-            const unsigned short prev = atomicCAS(&s[i], old, (unsigned short)v);
-            if (prev == old) break;
-            old = prev;
-        }
-    }
-};
-
 }  // namespace
 
 template <int T>
-__global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
+__global__ void __launch_bounds__(T) k_rebuild(Dev d) {
     const uint32_t l = blockIdx.x;
     const uint32_t tid = threadIdx.x;
     const uint64_t b = d.nb[l], k0 = d.kb[l], u0 = d.ub[l], t0 = d.tb[l];
     const uint32_t n0 = d.n_cnt ? d.n_cnt[l] : (uint32_t)(d.nb[l + 1] - b);
     const uint32_t U = d.n_cnt ? d.u_cnt[l] : (uint32_t)(d.ub[l + 1] - u0);
-    extern __shared__ __align__(16) unsigned short dtab[];
-    // table size: SMEM (16-bit positions) for 2 * next_pow2(2 n) <= smem_slots, else global
-    uint32_t tsz_s = 2;
-    while (tsz_s < 2 * n0) tsz_s <<= 1;
-    const bool sm = 2 * tsz_s <= smem_slots && n0 < 0xFFFFu;
-    const uint32_t tsz = sm ? tsz_s : (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
+    const uint32_t tsz = (uint32_t)(d.tb[l + 1] - t0), tmask = tsz - 1;
     uint32_t* parent = d.uf_parent + u0;
     uint8_t* rank = d.uf_rank + u0;
 
     uint32_t *ksym = d.s_ksym + b, *kkids = d.s_kkids + k0, *cval = d.s_cval + b, *val = d.s_val + b,
              *first = d.s_first + b;
     uint8_t* flag = d.s_flag + b;
-    Tab tc{d.s_tc + t0, dtab, tmask, sm}, ts{d.s_ts + t0, dtab + tsz_s, tmask, sm};
+    uint32_t *tc = d.s_tc + t0, *ts = d.s_ts + t0;
     uint32_t *osym = d.o_sym + b, *okoff = d.o_koff + b + l, *okids = d.o_kids + k0, *ocid = d.o_cid + b;
     double* ocost = d.o_cost + b;
 
@@ -126,7 +86,7 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
     __syncthreads();
 
     for (;;) {  // ---------------- pass (egraph.py:206-225) ----------------
-        for (uint32_t s = tid; s < tsz; s += T) { tc.clear(s); ts.clear(s); }
+        for (uint32_t s = tid; s < tsz; s += T) { tc[s] = NONE; ts[s] = NONE; }
         if (tid == 0) sh_merged = 0;
         __syncthreads();
         uint32_t p0 = 0;
@@ -146,19 +106,19 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
                 const uint32_t h = key_hash(ksym[i], kkids + ko, a);
                 uint32_t s = h & tmask, f = NONE;
                 for (;; s = (s + 1) & tmask) {
-                    uint32_t e = tc.ld(s);
+                    uint32_t e = tc[s];
                     if (e == NONE) break;
                     if (key_eq(ksym, kkids, in.koff, e, i)) { f = e; break; }
                 }
                 first[i] = f;
                 if (f != NONE) continue;
                 for (s = h & tmask;; s = (s + 1) & tmask) {
-                    uint32_t e = ts.ld(s);
+                    uint32_t e = ts[s];
                     if (e == NONE) {
-                        e = ts.cas_empty(s, i);
+                        e = atomicCAS(&ts[s], NONE, i);
                         if (e == NONE) break;
                     }
-                    if (key_eq(ksym, kkids, in.koff, e, i)) { ts.amin(s, i); break; }
+                    if (key_eq(ksym, kkids, in.koff, e, i)) { atomicMin(&ts[s], i); break; }
                 }
             }
             __syncthreads();
@@ -169,7 +129,7 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
                     const uint32_t ko = in.koff[i], a = in.koff[i + 1] - ko;
                     const uint32_t h = key_hash(ksym[i], kkids + ko, a);
                     for (uint32_t s = h & tmask;; s = (s + 1) & tmask) {
-                        uint32_t e = ts.ld(s);
+                        uint32_t e = ts[s];
                         if (key_eq(ksym, kkids, in.koff, e, i)) { f = e; break; }
                     }
                     first[i] = f;
@@ -187,7 +147,7 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
                     const uint32_t ko = in.koff[i], a = in.koff[i + 1] - ko;
                     const uint32_t h = key_hash(ksym[i], kkids + ko, a);
                     for (uint32_t s = h & tmask;; s = (s + 1) & tmask)
-                        if (tc.cas_empty(s, i) == NONE) break;
+                        if (atomicCAS(&tc[s], NONE, i) == NONE) break;
                     val[i] = cval[i];
                     flag[i] = 1;
                 } else {
@@ -203,7 +163,7 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
                 sh_merges++;
                 sh_merged = 1;
             }
-            for (uint32_t s = tid; s < tsz; s += T) ts.clear(s);
+            for (uint32_t s = tid; s < tsz; s += T) ts[s] = NONE;
             p0 = pstar + 1;
             __syncthreads();
         }
@@ -336,6 +296,6 @@ __global__ void __launch_bounds__(T) k_rebuild(Dev d, uint32_t smem_slots) {
     }
 }
 
-template __global__ void k_rebuild<256>(Dev, uint32_t);
+template __global__ void k_rebuild<256>(Dev);
 
 }  // namespace esat

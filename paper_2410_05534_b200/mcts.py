@@ -24,6 +24,7 @@ Engine contract (what both engines implement, state objects are engine-private):
     expand(states, rules)               -> (child states, changed[L], cost, nodes, classes, app)
     simulate(states, cost0, allowed, steps, node_limit, seeds) -> reward f64[L]
     final(state, method)                -> (cost, save_graph JSON text)
+    configure(cfg)                      -> None (start of a run: extractor, extraction cache reset)
 
 A failed extraction yields cost ``inf``. In a rollout a step whose extraction failed adds no reward
 and leaves the anchor unchanged ("treat that step's improvement as 0"); a step right
@@ -66,6 +67,10 @@ class MctsConfig:
     final_extractor: str = "ocf"
     batch: int = 32
     headroom: int = 4096
+    # SPEC.md:655 / PAPER §4.3: rollouts reuse extracted costs by e-graph fingerprint (egraph.py:247)
+    # for the whole optimization run. Off by default on the device: the WL fingerprint costs more
+    # than the extraction it would save there (bench.py `fingerprint` vs `kernel_ms.extract`).
+    extraction_cache: bool = False
 
 
 @dataclass
@@ -98,6 +103,7 @@ class RunReport:
     rule_histogram: dict
     final_program: str | None
     final_extractor: str = "ocf"
+    extraction_cache: dict | None = None   # {"lookups", "hits"} of the run-wide rollout cache
 
     @property
     def trace(self) -> list:
@@ -109,7 +115,8 @@ class RunReport:
                 "speedup_pct": hexf(self.speedup_pct), "final_extractor": self.final_extractor,
                 "iterations": [[r, n, c, hexf(x)] for r, n, c, x in self.iterations],
                 "rule_histogram": {str(k): v for k, v in sorted(self.rule_histogram.items())},
-                "final_program": self.final_program}
+                "final_program": self.final_program,
+                **({"extraction_cache": self.extraction_cache} if self.extraction_cache is not None else {})}
 
 
 def speedup_pct(orig: float, opt: float) -> float:
@@ -153,6 +160,30 @@ def rollout_rewards(reward, prev, live, cost) -> None:
     prev[good] = cost[good]
 
 
+class ExtractionCache:
+    """Run-wide rollout extraction cache keyed by the e-graph fingerprint. Leaves
+    are consulted in leaf order within a step, so a fingerprint first seen in this step is a hit for
+    a later leaf of the same step -- the same rule in every engine."""
+
+    def __init__(self):
+        self.table, self.lookups, self.hits = {}, 0, 0
+
+    def resolve(self, fps, live, extracted):
+        """Per live leaf: the cached cost of its fingerprint, else its own extraction (then cached)."""
+        cost = np.full(len(fps), np.inf)
+        for l in range(len(fps)):
+            if not live[l]:
+                continue
+            self.lookups += 1
+            fp = int(fps[l])
+            if fp in self.table:
+                self.hits += 1
+                cost[l] = self.table[fp]
+            else:
+                cost[l] = self.table[fp] = float(extracted[l])
+        return cost
+
+
 class DeviceEngine:
     """Batched e-graph operations of the search on the device (one LeafPipeline per batch)."""
 
@@ -162,6 +193,25 @@ class DeviceEngine:
         self.method, self.headroom = method, headroom
         self.regrows = 0
         self._pipe = self._drv = None
+        self.cache = None
+        self._fp_symbols = -1
+
+    def configure(self, cfg):
+        self.method = cfg.main_extractor
+        self.cache = ExtractionCache() if cfg.extraction_cache else None
+
+    def _fingerprints(self, b):
+        """k_fingerprint of every leaf of the rebuilt batch (egraph.py:247-296, bit-exact)."""
+        from .fingerprint import symtab_key_tables
+
+        if self._fp_symbols != len(self.symtab):
+            self.ctx.fingerprint_setup(*symtab_key_tables(self.symtab))
+            self._fp_symbols = len(self.symtab)
+        b.fingerprint()
+        fp, st = b.download_fingerprint()
+        if np.any(st != 0):
+            raise RuntimeError("k_fingerprint failed on a leaf")
+        return fp
 
     # -- batch plumbing ---------------------------------------------------------------
     def _ensure_pipe(self):
@@ -307,6 +357,10 @@ class DeviceEngine:
             cb, _ = self._extract(h[2])
             cost = np.full(L, np.inf)
             cost[idx] = cb
+            if self.cache is not None:
+                fps = np.zeros(L, np.uint64)
+                fps[idx] = self._fingerprints(h[2])
+                cost = self.cache.resolve(fps, live, cost)
             rollout_rewards(reward, prev, live, cost)
             n, _ = h[2].rebuilt_sizes()
             live[idx] &= n < node_limit
@@ -433,6 +487,8 @@ def optimize_mcts(egraph, rules, cfg: MctsConfig, cost_config, symtab=None, engi
         engine = DeviceEngine(rules, symtab, egraph.language, cost_config, method=cfg.main_extractor,
                               headroom=cfg.headroom)
     rng = random.Random(cfg.seed)
+    if hasattr(engine, "configure"):
+        engine.configure(cfg)
     (state,), cost, n, c, app = engine.evaluate([engine.initial(egraph)])
     first = state
     iterations = []
@@ -448,5 +504,7 @@ def optimize_mcts(egraph, rules, cfg: MctsConfig, cost_config, symtab=None, engi
             break
     orig, _ = engine.final(first, cfg.final_extractor)
     opt, program = engine.final(state, cfg.final_extractor)
+    cache = getattr(engine, "cache", None) or getattr(getattr(engine, "engine", None), "cache", None)
+    stats = {"lookups": cache.lookups, "hits": cache.hits} if cache is not None else None
     return RunReport(orig, opt, speedup_pct(orig, opt), time.monotonic() - t0, iterations,
-                     dict(Counter(it[0] for it in iterations)), program, cfg.final_extractor)
+                     dict(Counter(it[0] for it in iterations)), program, cfg.final_extractor, stats)

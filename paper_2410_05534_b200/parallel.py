@@ -109,6 +109,12 @@ class ShardedEngine:
         self.exchanged_bytes += sum(len(pickle.dumps(o)) for o in out)
         return out
 
+    def configure(self, cfg):
+        if cfg.extraction_cache and self.world > 1:
+            raise ValueError("the run-wide extraction cache is per engine: not supported with sharded rollouts")
+        if hasattr(self.engine, "configure"):
+            self.engine.configure(cfg)
+
     def initial(self, egraph):
         return self.engine.initial(egraph)
 

@@ -39,6 +39,8 @@ CASES = {
     # rules on a 1-2k-node leaf (28k matches, a would_create_cycle DFS each), so the node limit of
     # these cases keeps the leaves the search explodes from small
     "nasrnn_c2": ("nasrnn", "taso_analog", "analytic", dict(budget=128, node_limit=800, seed=0, batch=32)),
+    "nasrnn_c2_cache": ("nasrnn", "taso_analog", "analytic", dict(budget=128, node_limit=800, seed=0, batch=32,
+                                                                  extraction_cache=True)),
     "nasrnn_c2_limit2000": ("nasrnn", "taso_analog", "analytic", dict(budget=128, node_limit=2000, seed=0, batch=32)),
     "resnext50_c3": ("resnext50", "taso_analog", "analytic", dict(budget=128, node_limit=1000, seed=0, batch=32)),
     "inception_v3_c4": ("inception_v3", "taso_analog", "analytic", dict(budget=64, node_limit=1000, seed=0,
