@@ -49,11 +49,10 @@ COST_TERM, COST_UNIT, COST_ANALYTIC = 0, 1, 2
 
 
 def key_hash(words) -> int:
+    """Word-wise FNV-1a over the key words (k_apply's sym_lookup computes the same)."""
     h = 2166136261
     for w in words:
-        for s in (0, 8, 16, 24):
-            h ^= (int(w) >> s) & 0xFF
-            h = (h * 16777619) & 0xFFFFFFFF
+        h = ((h ^ (int(w) & 0xFFFFFFFF)) * 16777619) & 0xFFFFFFFF
     return h
 
 

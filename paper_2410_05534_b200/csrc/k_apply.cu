@@ -171,9 +171,8 @@ __device__ bool infer_shape(int op, const Sym& s, const Shape* in, uint32_t nin,
     }
 }
 
-__device__ __forceinline__ uint32_t fnv(uint32_t h, uint32_t w) {
-    for (int s = 0; s < 32; s += 8) { h ^= (w >> s) & 0xFFu; h *= 16777619u; }
-    return h;
+__device__ __forceinline__ uint32_t fnv(uint32_t h, uint32_t w) {   // word-wise FNV-1a (apply.key_hash)
+    return (h ^ w) * 16777619u;
 }
 
 // symbol id of s, NONE if it was never interned (apply.py symbol_key_words / key_hash)
