@@ -100,7 +100,9 @@ def main():
     from paper_2410_05534_b200.symtab import SymbolTable
     from esat import rewrite as R
 
-    n_leaves = 256
+    import os
+
+    n_leaves = int(os.environ.get("ESAT_BENCH_LEAVES", "256"))   # seeds 0..n-1 (a prefix of a larger set)
     for model in models:
         t0 = time.time()
         with mp.Pool(mp.cpu_count()) as pool:
