@@ -30,6 +30,9 @@ namespace {
 
 constexpr int INSTR = 20;
 constexpr int MAXI = 24;      // instructions per target
+constexpr uint32_t PLAN_CH = 32, PLAN_T = 2;   // matches planned per chunk (one per lane); targets per match
+constexpr uint32_t PLAN_FAIL = 0xFFFFFFFDu;    // make_symbol fails (or, with PLAN_SLOW, is not interned)
+constexpr uint32_t PLAN_SLOW = 1u, PLAN_SHAPE_ERR = 2u, PLAN_SHAPE_MISMATCH = 4u;
 constexpr uint32_t NO_SHAPE = 255;
 enum Op : int { OP_UNK = 0, OP_INPUT, OP_WEIGHT, OP_EWADD, OP_EWMUL, OP_MATMUL, OP_CONV2D, OP_RELU, OP_TANH,
                 OP_SIGMOID, OP_CONCAT, OP_SPLIT, OP_MAXPOOL, OP_TRANSPOSE, OP_NOOP };
@@ -424,6 +427,58 @@ __device__ void raise_ancestors(Leaf& L, uint32_t w, uint32_t* qtail) {
     }
 }
 
+// add of an instruction planned in advance: symbol id known (the symbol and its shape depend only on
+// class shapes, which no union inside an apply changes -- every union joins classes of one shape),
+// node cost from the symbol's shape and attributes
+__device__ uint32_t add_node_sid(Leaf& L, uint32_t sid, int op, uint32_t ar, const uint32_t* k, const Shape* cs,
+                                 uint32_t* err) {
+    const uint32_t e0 = hc_get(L, sid, k, ar);
+    if (e0 != NONE) return find(L, L.cid[e0]);
+    if (L.n + 1 > L.cap_n || L.K + ar > L.cap_k || L.U + 1 > L.cap_u) { *err = A_CAPACITY; return NONE; }
+    Sym s;
+    s.name = 0; s.arity = ar; s.np = 0;
+    s.shape = sym_shape(*L.a, sid);
+    s.ival[0] = INT_NONE;
+    if (op == OP_MAXPOOL) {
+        const uint32_t code = (uint32_t)L.d->sym_par[L.d->sym_poff[sid]];
+        s.ival[0] = code < L.a->n_values ? L.a->val_int[code] : INT_NONE;
+    }
+    const uint32_t id = L.U++;
+    const uint32_t e = L.n++;
+    const uint32_t k0 = L.K;
+    L.K += ar;
+    if (L.lane == 0) {
+        L.parent[id] = id;
+        L.rank[id] = 0;
+        L.head[id] = NONE;
+        L.seen[id] = 0;
+        L.sym[e] = sid;
+        for (uint32_t i = 0; i < ar; i++) L.kids[k0 + i] = k[i];
+        L.koff[e + 1] = L.K;
+        L.cid[e] = id;
+        L.cost[e] = node_cost(*L.a, op, s, cs);
+        hc_insert(L, e);
+        list_push(L, id, e);
+        if (L.usepot) {
+            uint32_t pv = 0;
+            L.phead[id] = NONE;
+            L.ptail[id] = NONE;
+            for (uint32_t i = 0; i < ar; i++) {
+                const uint32_t c = k[i], q = k0 + i;
+                pv = max(pv, L.pot[c] + 1u);
+                L.eown[q] = e;
+                L.pnext[q] = NONE;
+                if (L.phead[c] == NONE) L.phead[c] = q; else L.pnext[L.ptail[c]] = q;
+                L.ptail[c] = q;
+            }
+            L.pot[id] = pv;
+        }
+    }
+    __syncwarp();
+    L.changed = true;
+    return id;
+}
+
 __device__ bool union_classes(Leaf& L, uint32_t a, uint32_t b, uint32_t* qtail) {
     const uint32_t ra = find(L, a), rb = find(L, b);
     __syncwarp();
@@ -519,6 +574,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     // from here every lane runs the same sequential replay (identical values in registers); state
     // writes are issued by lane 0 and fenced with __syncwarp, the cycle test uses all lanes
     __shared__ uint32_t sh_qtail;
+    __shared__ uint32_t sh_plan[PLAN_CH][PLAN_T][MAXI + 1];
     L.lane = lane;
     __shared__ uint32_t sh_kahn;
     if (rule != NONE && L.usepot) {
@@ -587,12 +643,63 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
         const uint32_t* words = from_join ? a.j_words + a.j_off[mi] : a.m_words + a.m_off[mi];
         const uint32_t cnt = from_join ? a.j_count[mi] : a.m_count[mi];
         found = cnt;
-        for (uint32_t m = 0; m < cnt && st == A_OK; m++) {
+        // Matches are replayed in order in chunks of PLAN_CH. Before a chunk, each lane plans one
+        // match: for every target instruction the symbol make_symbol / infer_shape would build and
+        // its id (sym_lookup), plus the _instance_shape outcome and the matched-class shape test.
+        // These depend only on class shapes, which no union of an apply changes (the shape test
+        // admits only same-shape unions; rebuilt classes are shape-homogeneous), so the ordered
+        // replay reads them instead of recomputing -- it keeps every state-dependent step (finds,
+        // hashcons probes, the cycle test, adds, unions) and the reference's order. A target whose
+        // plan hit a symbol the table lacks replays the full path (host interning, below).
+        const bool planned = NT <= PLAN_T;
+        for (uint32_t m0 = 0; m0 < cnt && st == A_OK; m0 += PLAN_CH) {
+          const uint32_t m1 = min(cnt, m0 + PLAN_CH);
+          if (planned) {
+            __syncwarp();
+            if (m0 + lane < m1) {
+                const uint32_t* prec = words + (uint64_t)(m0 + lane) * W;
+                for (int32_t t = 0; t < NT; t++) {
+                    const int32_t* tp = rp + rp[7 + t];
+                    const uint32_t ni = (uint32_t)tp[0];
+                    uint32_t* pl = sh_plan[lane][t];
+                    uint32_t flags = 0;
+                    if (ni > MAXI) { pl[MAXI] = PLAN_SLOW; continue; }
+                    Shape shs[MAXI];
+                    bool bad = false;
+                    for (uint32_t i = 0; i < ni; i++) {
+                        const int32_t* ins = tp + 1 + INSTR * i;
+                        if (ins[0] == 0) { shs[i] = class_shape(L, prec[ins[1]]); continue; }
+                        pl[i] = PLAN_FAIL;
+                        if (bad) continue;   // _instance_shape stops at its first failure
+                        const uint32_t ar = (uint32_t)ins[3];
+                        Shape cs[4];
+                        for (uint32_t j = 0; j < ar; j++) cs[j] = shs[ins[5 + j]];
+                        Sym ps;
+                        if (!make_symbol(a, ins, prec, cs, ar, ps)) { bad = true; flags |= PLAN_SHAPE_ERR; continue; }
+                        shs[i] = ps.shape;
+                        const uint32_t sid = sym_lookup(d, a, ps);
+                        if (sid == NONE) flags |= PLAN_SLOW;
+                        pl[i] = sid == NONE ? PLAN_FAIL : sid;
+                    }
+                    if (!bad) {
+                        const Shape msh = class_shape(L, find(L, prec[t]));
+                        if (shs[ni - 1].nd != NO_SHAPE && msh.nd != NO_SHAPE && !shape_eq(shs[ni - 1], msh))
+                            flags |= PLAN_SHAPE_MISMATCH;
+                    }
+                    pl[MAXI] = flags;
+                }
+            }
+            __syncwarp();
+          }
+          for (uint32_t m = m0; m < m1 && st == A_OK; m++) {
             const uint32_t* rec = words + (uint64_t)m * W;
             for (int32_t t = 0; t < NT && st == A_OK; t++) {
                 const int32_t* tp = rp + rp[7 + t];
                 const uint32_t ni = (uint32_t)tp[0];
                 if (ni > MAXI) { st = A_PROGRAM; break; }
+                const uint32_t* pl = planned ? sh_plan[m - m0][t] : nullptr;
+                const uint32_t pflags = planned ? pl[MAXI] : PLAN_SLOW;
+                const bool fast = !(pflags & PLAN_SLOW);
                 const uint32_t matched = find(L, rec[t]);
                 // _target_refs (rewrite.py:463-489): refs set, existing instance class
                 uint32_t cid[MAXI];          // class of instruction i (NONE: not existing)
@@ -623,11 +730,17 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                     }
                     cid[i] = NONE;
                     if (all) {
-                        Shape cs[4];
-                        for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, kc[j]);
-                        Sym s;
-                        if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
-                        const uint32_t sid = sym_lookup(d, a, s);
+                        uint32_t sid;
+                        if (fast) {
+                            sid = pl[i];
+                            if (sid == PLAN_FAIL) { inst_err = true; break; }
+                        } else {
+                            Shape cs[4];
+                            for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, kc[j]);
+                            Sym s;
+                            if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
+                            sid = sym_lookup(d, a, s);
+                        }
                         const uint32_t e = sid == NONE ? NONE : hc_get(L, sid, kc, ar);
                         if (e != NONE) {
                             const uint32_t c = find(L, L.cid[e]);
@@ -648,6 +761,23 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                 ovf = __any_sync(0xffffffffu, ovf);
                 if (ovf) { st = A_CAPACITY; break; }
                 // _instance_shape (rewrite.py:508-514) then the matched-class shape test
+                if (fast) {
+                    if (pflags & (PLAN_SHAPE_ERR | PLAN_SHAPE_MISMATCH)) { shp++; continue; }
+                    uint32_t inst[MAXI];
+                    uint32_t err = A_OK;
+                    for (uint32_t i = 0; i < ni && err == A_OK; i++) {
+                        const int32_t* ins = tp + 1 + INSTR * i;
+                        if (ins[0] == 0) { inst[i] = find(L, rec[ins[1]]); continue; }
+                        const uint32_t ar = (uint32_t)ins[3];
+                        uint32_t kc[4];
+                        Shape cs[4];
+                        for (uint32_t j = 0; j < ar; j++) { kc[j] = find(L, inst[ins[5 + j]]); cs[j] = class_shape(L, kc[j]); }
+                        inst[i] = add_node_sid(L, pl[i], ins[2], ar, kc, cs, &err);
+                    }
+                    if (err != A_OK) { st = err; break; }
+                    if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
+                    continue;
+                }
                 Shape sh[MAXI];
                 for (uint32_t i = 0; i < ni && !inst_err; i++) {
                     const int32_t* ins = tp + 1 + INSTR * i;
@@ -688,6 +818,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                 if (err != A_OK) { st = err; break; }
                 if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
             }
+          }
         }
     }
     if (lane != 0) return;
