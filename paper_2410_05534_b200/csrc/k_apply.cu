@@ -262,10 +262,12 @@ __device__ double node_cost(const AArgs& a, int op, const Sym& s, const Shape* i
     return a.coeff * f;
 }
 
+// hashcons key hash of k_apply's own lookup table (built at staging, probed / extended by the replay):
+// a 32-bit multiply-xorshift per child is enough for linear probing at load <= 1/2
 __device__ __forceinline__ uint32_t node_hash(uint32_t sym, const uint32_t* k, uint32_t ar) {
-    uint64_t h = mix64(0x9e3779b97f4a7c15ull ^ sym);
-    for (uint32_t i = 0; i < ar; i++) h = mix64(h ^ ((uint64_t)k[i] + 0x632be59bd9b4e019ull * (i + 1)));
-    return (uint32_t)h;
+    uint32_t h = (sym + 0x7f4a7c15u) * 0x9e3779b1u;
+    for (uint32_t i = 0; i < ar; i++) h = ((h ^ (h >> 15)) + k[i]) * 0x85ebca77u;
+    return h ^ (h >> 13);
 }
 
 // hashcons.get(node): the entry whose stored key equals (sym, kids), NONE if absent
@@ -430,11 +432,15 @@ __device__ void raise_ancestors(Leaf& L, uint32_t w, uint32_t* qtail) {
 // add of an instruction planned in advance: symbol id known (the symbol and its shape depend only on
 // class shapes, which no union inside an apply changes -- every union joins classes of one shape),
 // node cost from the symbol's shape and attributes
-__device__ uint32_t add_node_sid(Leaf& L, uint32_t sid, int op, uint32_t ar, const uint32_t* k, const Shape* cs,
-                                 uint32_t* err) {
-    const uint32_t e0 = hc_get(L, sid, k, ar);
-    if (e0 != NONE) return find(L, L.cid[e0]);
+__device__ uint32_t add_node_sid(Leaf& L, uint32_t sid, int op, uint32_t ar, const uint32_t* k, uint32_t* err,
+                                 bool known_absent) {
+    if (!known_absent) {
+        const uint32_t e0 = hc_get(L, sid, k, ar);
+        if (e0 != NONE) return find(L, L.cid[e0]);
+    }
     if (L.n + 1 > L.cap_n || L.K + ar > L.cap_k || L.U + 1 > L.cap_u) { *err = A_CAPACITY; return NONE; }
+    Shape cs[4];   // child class shapes: only the node cost needs them
+    for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, k[j]);
     Sym s;
     s.name = 0; s.arity = ar; s.np = 0;
     s.shape = sym_shape(*L.a, sid);
@@ -703,6 +709,8 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                 const uint32_t matched = find(L, rec[t]);
                 // _target_refs (rewrite.py:463-489): refs set, existing instance class
                 uint32_t cid[MAXI];          // class of instruction i (NONE: not existing)
+                uint32_t vcls[MAXI];         // root of a var instruction's binding
+                uint8_t rmiss[MAXI];         // _target_refs probed instruction i (all children existed) and missed
                 uint32_t rbeg[MAXI], rend[MAXI];
                 uint32_t refs[64];
                 uint32_t nref = 0;
@@ -712,6 +720,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                     if (ins[0] == 0) {
                         const uint32_t c = find(L, rec[ins[1]]);
                         cid[i] = c;
+                        vcls[i] = c;
                         rbeg[i] = nref;
                         if (nref < 64) refs[nref++] = c;
                         rend[i] = nref;
@@ -729,6 +738,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                         else kc[j] = cid[ci];
                     }
                     cid[i] = NONE;
+                    rmiss[i] = 0;
                     if (all) {
                         uint32_t sid;
                         if (fast) {
@@ -747,6 +757,8 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                             cid[i] = c;
                             nref = b0;
                             refs[nref++] = c;
+                        } else {
+                            rmiss[i] = 1;
                         }
                     }
                     rbeg[i] = b0;
@@ -765,14 +777,22 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                     if (pflags & (PLAN_SHAPE_ERR | PLAN_SHAPE_MISMATCH)) { shp++; continue; }
                     uint32_t inst[MAXI];
                     uint32_t err = A_OK;
+                    // every inst[] is a root (a var's find from _target_refs -- adds do not move roots --,
+                    // a hashcons hit's find, or a new id) and no union happens before the top one
+                    // an instruction _target_refs found reuses that class (adds never remove a node and
+                    // move no root); one it probed and missed is still missing unless this target
+                    // already added a node (two instructions of one target may build the same node)
+                    bool added = false;
                     for (uint32_t i = 0; i < ni && err == A_OK; i++) {
                         const int32_t* ins = tp + 1 + INSTR * i;
-                        if (ins[0] == 0) { inst[i] = find(L, rec[ins[1]]); continue; }
+                        if (ins[0] == 0) { inst[i] = vcls[i]; continue; }
+                        if (cid[i] != NONE) { inst[i] = cid[i]; continue; }
                         const uint32_t ar = (uint32_t)ins[3];
                         uint32_t kc[4];
-                        Shape cs[4];
-                        for (uint32_t j = 0; j < ar; j++) { kc[j] = find(L, inst[ins[5 + j]]); cs[j] = class_shape(L, kc[j]); }
-                        inst[i] = add_node_sid(L, pl[i], ins[2], ar, kc, cs, &err);
+                        for (uint32_t j = 0; j < ar; j++) kc[j] = inst[ins[5 + j]];
+                        const uint32_t n0 = L.n;
+                        inst[i] = add_node_sid(L, pl[i], ins[2], ar, kc, &err, rmiss[i] && !added);
+                        added = added || L.n != n0;
                     }
                     if (err != A_OK) { st = err; break; }
                     if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
