@@ -140,3 +140,50 @@ def test_leaf_parallel_search_matches_single_rank():
     for rank, rep, nbytes in outs:
         assert rep == single, rank
         assert nbytes > 0
+
+
+def _bench_shard_worker(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    leaves = list(range(37))            # stand-ins: make_batch only indexes the leaf list
+    B = 16
+    from paper_2410_05534_b200.arena import Batch
+
+    orig = Batch.pack
+    Batch.pack = lambda self: {"n_leaves": len(self.leaves)}
+    try:
+        packed, src = bench.make_batch(leaves, B, rotate=rank * B)
+    finally:
+        Batch.pack = orig
+    # the bench's exchange: per-leaf (root cost, status) all-gathered in rank order
+    cost = torch.tensor([float(s) for s in src], dtype=torch.float64)
+    stat = torch.tensor(src, dtype=torch.int32)
+    c, st = allgather_leaf_results(cost, stat)
+    q.put((rank, src, c.tolist(), st.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_leaf_shards_and_gather():
+    """bench.py --gpus N (C3): rank r takes the contiguous shard [r*B, (r+1)*B) of the global leaf
+    sequence and the per-leaf results all-gathered over the ranks are that sequence in order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29800 + os.getpid() % 100
+    procs = [ctx.Process(target=_bench_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    glob = [i % 37 for i in range(32)]
+    assert outs[0][1] == glob[:16] and outs[1][1] == glob[16:]
+    for _, _, c, st in outs:
+        assert st == glob and c == [float(x) for x in glob]
