@@ -14,6 +14,7 @@
  *                         extract_ocf_greedy              extraction.py:229-242
  *                         (+ validate_extraction / _reachable_chosen, extraction.py:67-115)
  *   esat_batch_upload  <- EGraph.snapshot into device slots (egraph.py:300-312)
+ *   esat_store_save / esat_batch_load_slots <- EGraph.snapshot kept on the device (D2D)
  *
  * Plain C types only. All functions return ESAT_OK (0) or an ESAT_E_* code; the message
  * is available from esat_last_error(ctx). Threading: one host thread per context (the
@@ -201,6 +202,29 @@ int esat_download_fingerprint(esat_batch* b, uint64_t* fp, uint32_t* status);
 /* the batch input (dirty) arena with live counts: hashcons + union-find, spans as created */
 int esat_download_state(esat_batch* b, uint32_t* n_cnt, uint32_t* u_cnt, uint32_t* sym, uint32_t* koff,
                         uint32_t* kids, uint32_t* cid, double* cost, uint32_t* parent, uint8_t* rank);
+
+/* ---- device snapshot store: EGraph.snapshot (egraph.py:300-312) as D2D copies into slots ---- */
+typedef struct esat_store esat_store;
+int esat_store_create(esat_ctx* ctx, esat_store** out);
+int esat_store_destroy(esat_store* st);
+/* number of slots; slots are append-only, esat_store_truncate drops the newest */
+uint32_t esat_store_size(const esat_store* st);
+int esat_store_truncate(esat_store* st, uint32_t count);
+/* copy the last rebuild of batch leaves[0..count) (clean hashcons + union-find + raw root) into
+ * new slots (device to device); their ids go to slots_out */
+int esat_store_save(esat_store* st, esat_batch* b, uint32_t count, const uint32_t* leaves, uint32_t* slots_out);
+/* one host leaf state (the batch-arena format of one leaf, koff with n+1 entries) into a new slot */
+int esat_store_put(esat_store* st, uint32_t n, uint32_t K, uint32_t U, uint32_t root, const uint32_t* sym,
+                   const uint32_t* koff, const uint32_t* kids, const uint32_t* cid, const double* cost,
+                   const uint32_t* parent, const uint8_t* rank, uint32_t* slot_out);
+/* sizes of slots: hashcons entries, child slots, union-find ids, raw root (any pointer may be NULL) */
+int esat_store_info(const esat_store* st, uint32_t count, const uint32_t* slots, uint32_t* n, uint32_t* K,
+                    uint32_t* U, uint32_t* root);
+int esat_store_download(esat_store* st, uint32_t slot, uint32_t* sym, uint32_t* koff, uint32_t* kids, uint32_t* cid,
+                        double* cost, uint32_t* parent, uint8_t* rank);
+/* fill the input arena of b (leaf l's spans must hold slot slots[l]) from the store, device to
+ * device, and set the live counts (as esat_batch_upload + esat_batch_set_counts) */
+int esat_batch_load_slots(esat_batch* b, esat_store* st, const uint32_t* slots);
 
 #ifdef __cplusplus
 }

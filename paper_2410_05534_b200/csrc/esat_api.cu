@@ -1224,3 +1224,299 @@ int esat_download_fingerprint(esat_batch* b, uint64_t* fp, uint32_t* status) {
 }
 
 }  // extern "C"
+
+// ---- device snapshot store (EGraph.snapshot, egraph.py:300-312) -------------------
+// An append-only device arena of leaf e-graph states ("slots"): esat_store_save copies the last
+// rebuild of batch leaves into new slots (D2D), esat_batch_load_slots fills a batch's input arena
+// from slots (D2D) -- an MCTS tree keeps every node's e-graph on the device, and expansions /
+// rollouts start from device copies instead of host re-packs. A slot is the leaf's clean
+// hashcons (order, symbols, children, classes, costs) + union-find + raw root, the same content
+// as the host LeafState (arena.py).
+struct esat_store {
+    esat_ctx* ctx = nullptr;
+    struct Slot { uint64_t on, of, ok, ou; uint32_t n, K, U, root; };
+    std::vector<Slot> slots;
+    uint64_t capN = 0, capF = 0, capK = 0, capU = 0;   // capacities: nodes, koff entries, kids, ids
+    uint32_t *sym = nullptr, *koff = nullptr, *kids = nullptr, *cid = nullptr, *parent = nullptr;
+    double* cost = nullptr;
+    uint8_t* rank = nullptr;
+    uint32_t* d_job = nullptr;   // copy jobs
+    uint64_t job_cap = 0;
+    uint64_t useN() const { return slots.empty() ? 0 : slots.back().on + slots.back().n; }
+    uint64_t useF() const { return slots.empty() ? 0 : slots.back().of + slots.back().n + 1; }
+    uint64_t useK() const { return slots.empty() ? 0 : slots.back().ok + slots.back().K; }
+    uint64_t useU() const { return slots.empty() ? 0 : slots.back().ou + slots.back().U; }
+};
+
+namespace esat {
+
+// job j (16 u32): leaf, slot n, K, U, then node/koff/kid/id offsets on the store side as u64 pairs
+struct SlotJob { uint32_t leaf, n, K, U; uint64_t on, of, ok, ou; };
+
+// sizes of the last rebuild of leaves[j]: n, K (= koff[n]), U (rebuilt ids), raw root
+__global__ void k_store_sizes(Dev d, const uint32_t* leaves, uint32_t count, uint32_t* out) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= count) return;
+    const uint32_t l = leaves[j];
+    const uint32_t n = d.o_n[l];
+    out[4 * j] = n;
+    out[4 * j + 1] = d.o_koff[d.nb[l] + l + n];
+    out[4 * j + 2] = d.u_reb ? d.u_reb[l] : (uint32_t)(d.ub[l + 1] - d.ub[l]);
+    out[4 * j + 3] = d.root[l];
+}
+
+// one CTA per job: batch leaf's rebuild outputs -> store slot (save) or store slot -> batch input
+// arena (load)
+template <bool SAVE>
+__global__ void k_store_copy(Dev d, const SlotJob* jobs, uint32_t* sym, uint32_t* koff, uint32_t* kids,
+                             uint32_t* cid, double* cost, uint32_t* parent, uint8_t* rank, uint32_t* in_sym,
+                             uint32_t* in_koff, uint32_t* in_kids, uint32_t* in_cid, double* in_cost,
+                             uint32_t* in_parent, uint8_t* in_rank) {
+    const SlotJob jb = jobs[blockIdx.x];
+    const uint32_t l = jb.leaf;
+    const uint64_t n0 = d.nb[l], k0 = d.kb[l], u0 = d.ub[l];
+    for (uint32_t i = threadIdx.x; i < jb.n; i += blockDim.x) {
+        if (SAVE) {
+            sym[jb.on + i] = d.o_sym[n0 + i];
+            cid[jb.on + i] = d.o_cid[n0 + i];
+            cost[jb.on + i] = d.o_cost[n0 + i];
+        } else {
+            in_sym[n0 + i] = sym[jb.on + i];
+            in_cid[n0 + i] = cid[jb.on + i];
+            in_cost[n0 + i] = cost[jb.on + i];
+        }
+    }
+    for (uint32_t i = threadIdx.x; i <= jb.n; i += blockDim.x) {
+        if (SAVE) koff[jb.of + i] = d.o_koff[n0 + l + i];
+        else in_koff[n0 + l + i] = koff[jb.of + i];
+    }
+    for (uint32_t i = threadIdx.x; i < jb.K; i += blockDim.x) {
+        if (SAVE) kids[jb.ok + i] = d.o_kids[k0 + i];
+        else in_kids[k0 + i] = kids[jb.ok + i];
+    }
+    for (uint32_t i = threadIdx.x; i < jb.U; i += blockDim.x) {
+        if (SAVE) { parent[jb.ou + i] = d.uf_parent[u0 + i]; rank[jb.ou + i] = d.uf_rank[u0 + i]; }
+        else { in_parent[u0 + i] = parent[jb.ou + i]; in_rank[u0 + i] = rank[jb.ou + i]; }
+    }
+}
+
+}  // namespace esat
+
+namespace {
+
+template <typename T>
+int store_grow(esat_store* st, T** p, uint64_t* cap, uint64_t used, uint64_t need) {
+    if (need <= *cap && *p) return ESAT_OK;
+    esat_ctx* c = st->ctx;
+    uint64_t nc = *cap ? *cap : 4096;
+    while (nc < need) nc *= 2;
+    T* q = nullptr;
+    CK(c, cudaMallocAsync((void**)&q, sizeof(T) * nc, c->stream));
+    if (*p && used) CK(c, cudaMemcpyAsync(q, *p, sizeof(T) * used, cudaMemcpyDeviceToDevice, c->stream));
+    afree(*p, c->stream);
+    *p = q;
+    *cap = nc;
+    return ESAT_OK;
+}
+
+int store_reserve(esat_store* st, uint64_t n, uint64_t f, uint64_t k, uint64_t u) {
+    int r;
+    const uint64_t un = st->useN(), uf = st->useF(), uk = st->useK(), uu = st->useU();
+    uint64_t cn = st->capN, cn2 = st->capN, cn3 = st->capN, cu = st->capU;
+    if ((r = store_grow(st, &st->sym, &cn, un, un + n)) || (r = store_grow(st, &st->cid, &cn2, un, un + n)) ||
+        (r = store_grow(st, &st->cost, &cn3, un, un + n)))
+        return r;
+    st->capN = cn;
+    if ((r = store_grow(st, &st->koff, &st->capF, uf, uf + f))) return r;
+    if ((r = store_grow(st, &st->kids, &st->capK, uk, uk + k))) return r;
+    uint64_t cu2 = st->capU;
+    if ((r = store_grow(st, &st->parent, &cu, uu, uu + u)) || (r = store_grow(st, &st->rank, &cu2, uu, uu + u)))
+        return r;
+    st->capU = cu;
+    return ESAT_OK;
+}
+
+int store_jobs(esat_store* st, const std::vector<SlotJob>& jobs) {
+    esat_ctx* c = st->ctx;
+    const uint64_t words = (sizeof(SlotJob) * jobs.size() + 3) / 4;
+    if (words > st->job_cap) {
+        afree(st->d_job, c->stream);
+        st->d_job = nullptr;
+        CK(c, cudaMallocAsync((void**)&st->d_job, 4 * words, c->stream));
+        st->job_cap = words;
+    }
+    CK(c, cudaMemcpyAsync(st->d_job, jobs.data(), sizeof(SlotJob) * jobs.size(), cudaMemcpyHostToDevice, c->stream));
+    return ESAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int esat_store_create(esat_ctx* c, esat_store** out) {
+    if (!c || !out) return ESAT_E_ARG;
+    esat_store* st = new esat_store();
+    st->ctx = c;
+    *out = st;
+    return ESAT_OK;
+}
+
+int esat_store_destroy(esat_store* st) {
+    if (!st) return ESAT_OK;
+    esat_ctx* c = st->ctx;
+    cudaSetDevice(c->device);
+    afree(st->sym, c->stream); afree(st->koff, c->stream); afree(st->kids, c->stream); afree(st->cid, c->stream);
+    afree(st->cost, c->stream); afree(st->parent, c->stream); afree(st->rank, c->stream); afree(st->d_job, c->stream);
+    delete st;
+    return ESAT_OK;
+}
+
+uint32_t esat_store_size(const esat_store* st) { return st ? (uint32_t)st->slots.size() : 0u; }
+
+int esat_store_truncate(esat_store* st, uint32_t count) {
+    if (!st || count > st->slots.size()) return ESAT_E_ARG;
+    st->slots.resize(count);
+    return ESAT_OK;
+}
+
+int esat_store_info(const esat_store* st, uint32_t count, const uint32_t* slots, uint32_t* n, uint32_t* K,
+                    uint32_t* U, uint32_t* root) {
+    if (!st || (count && !slots)) return ESAT_E_ARG;
+    for (uint32_t j = 0; j < count; j++) {
+        if (slots[j] >= st->slots.size()) return fail(st->ctx, ESAT_E_ARG, "slot %u out of range", slots[j]);
+        const esat_store::Slot& s = st->slots[slots[j]];
+        if (n) n[j] = s.n;
+        if (K) K[j] = s.K;
+        if (U) U[j] = s.U;
+        if (root) root[j] = s.root;
+    }
+    return ESAT_OK;
+}
+
+int esat_store_save(esat_store* st, esat_batch* b, uint32_t count, const uint32_t* leaves, uint32_t* slots_out) {
+    if (!st || !b || b->ctx != st->ctx || (count && (!leaves || !slots_out))) return ESAT_E_ARG;
+    esat_ctx* c = st->ctx;
+    if (!b->rebuilt) return fail(c, ESAT_E_STATE, "snapshot save requires a rebuilt batch");
+    if (!count) return ESAT_OK;
+    for (uint32_t j = 0; j < count; j++)
+        if (leaves[j] >= b->L) return fail(c, ESAT_E_ARG, "leaf %u out of range", leaves[j]);
+    cudaSetDevice(c->device);
+    uint32_t *d_leaves = nullptr, *d_sz = nullptr;
+    CK(c, cudaMallocAsync((void**)&d_leaves, 4ull * count, c->stream));
+    CK(c, cudaMallocAsync((void**)&d_sz, 16ull * count, c->stream));
+    CK(c, cudaMemcpyAsync(d_leaves, leaves, 4ull * count, cudaMemcpyHostToDevice, c->stream));
+    Dev d = b->d;
+    if (!b->counts) d.u_reb = nullptr;
+    k_store_sizes<<<(count + 127) / 128, 128, 0, c->stream>>>(d, d_leaves, count, d_sz);
+    std::vector<uint32_t> sz(4ull * count);
+    CK(c, cudaMemcpyAsync(sz.data(), d_sz, 16ull * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    afree(d_leaves, c->stream);
+    afree(d_sz, c->stream);
+    uint64_t tn = 0, tk = 0, tu = 0;
+    for (uint32_t j = 0; j < count; j++) { tn += sz[4 * j]; tk += sz[4 * j + 1]; tu += sz[4 * j + 2]; }
+    int r;
+    if ((r = store_reserve(st, tn, tn + count, tk, tu))) return r;
+    std::vector<SlotJob> jobs(count);
+    for (uint32_t j = 0; j < count; j++) {
+        esat_store::Slot s{st->useN(), st->useF(), st->useK(), st->useU(), sz[4 * j], sz[4 * j + 1], sz[4 * j + 2],
+                           sz[4 * j + 3]};
+        jobs[j] = SlotJob{leaves[j], s.n, s.K, s.U, s.on, s.of, s.ok, s.ou};
+        slots_out[j] = (uint32_t)st->slots.size();
+        st->slots.push_back(s);
+    }
+    if ((r = store_jobs(st, jobs))) return r;
+    k_store_copy<true><<<count, 256, 0, c->stream>>>(b->d, reinterpret_cast<const SlotJob*>(st->d_job), st->sym,
+                                                     st->koff, st->kids, st->cid, st->cost, st->parent, st->rank,
+                                                     nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    return launch_check(c, "k_store_copy");
+}
+
+int esat_store_put(esat_store* st, uint32_t n, uint32_t K, uint32_t U, uint32_t root, const uint32_t* sym,
+                   const uint32_t* koff, const uint32_t* kids, const uint32_t* cid, const double* cost,
+                   const uint32_t* parent, const uint8_t* rank, uint32_t* slot_out) {
+    if (!st || !slot_out || !koff || (n && (!sym || !cid || !cost)) || (K && !kids) || (U && (!parent || !rank)))
+        return ESAT_E_ARG;
+    esat_ctx* c = st->ctx;
+    cudaSetDevice(c->device);
+    int r;
+    if ((r = store_reserve(st, n, n + 1, K, U))) return r;
+    esat_store::Slot s{st->useN(), st->useF(), st->useK(), st->useU(), n, K, U, root};
+    cudaStream_t q = c->stream;
+    if (n) {
+        CK(c, cudaMemcpyAsync(st->sym + s.on, sym, 4ull * n, cudaMemcpyHostToDevice, q));
+        CK(c, cudaMemcpyAsync(st->cid + s.on, cid, 4ull * n, cudaMemcpyHostToDevice, q));
+        CK(c, cudaMemcpyAsync(st->cost + s.on, cost, 8ull * n, cudaMemcpyHostToDevice, q));
+    }
+    CK(c, cudaMemcpyAsync(st->koff + s.of, koff, 4ull * (n + 1), cudaMemcpyHostToDevice, q));
+    if (K) CK(c, cudaMemcpyAsync(st->kids + s.ok, kids, 4ull * K, cudaMemcpyHostToDevice, q));
+    if (U) {
+        CK(c, cudaMemcpyAsync(st->parent + s.ou, parent, 4ull * U, cudaMemcpyHostToDevice, q));
+        CK(c, cudaMemcpyAsync(st->rank + s.ou, rank, U, cudaMemcpyHostToDevice, q));
+    }
+    CK(c, cudaStreamSynchronize(q));   // the host arrays may be released on return
+    *slot_out = (uint32_t)st->slots.size();
+    st->slots.push_back(s);
+    return ESAT_OK;
+}
+
+int esat_store_download(esat_store* st, uint32_t slot, uint32_t* sym, uint32_t* koff, uint32_t* kids, uint32_t* cid,
+                        double* cost, uint32_t* parent, uint8_t* rank) {
+    if (!st || slot >= st->slots.size()) return ESAT_E_ARG;
+    esat_ctx* c = st->ctx;
+    cudaSetDevice(c->device);
+    const esat_store::Slot& s = st->slots[slot];
+    cudaStream_t q = c->stream;
+    if (sym && s.n) CK(c, cudaMemcpyAsync(sym, st->sym + s.on, 4ull * s.n, cudaMemcpyDeviceToHost, q));
+    if (cid && s.n) CK(c, cudaMemcpyAsync(cid, st->cid + s.on, 4ull * s.n, cudaMemcpyDeviceToHost, q));
+    if (cost && s.n) CK(c, cudaMemcpyAsync(cost, st->cost + s.on, 8ull * s.n, cudaMemcpyDeviceToHost, q));
+    if (koff) CK(c, cudaMemcpyAsync(koff, st->koff + s.of, 4ull * (s.n + 1), cudaMemcpyDeviceToHost, q));
+    if (kids && s.K) CK(c, cudaMemcpyAsync(kids, st->kids + s.ok, 4ull * s.K, cudaMemcpyDeviceToHost, q));
+    if (parent && s.U) CK(c, cudaMemcpyAsync(parent, st->parent + s.ou, 4ull * s.U, cudaMemcpyDeviceToHost, q));
+    if (rank && s.U) CK(c, cudaMemcpyAsync(rank, st->rank + s.ou, s.U, cudaMemcpyDeviceToHost, q));
+    CK(c, cudaStreamSynchronize(q));
+    return ESAT_OK;
+}
+
+int esat_batch_load_slots(esat_batch* b, esat_store* st, const uint32_t* slots) {
+    if (!b || !st || b->ctx != st->ctx || (b->L && !slots)) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    cudaSetDevice(c->device);
+    std::vector<SlotJob> jobs(b->L);
+    std::vector<uint32_t> ncnt(b->L), ucnt(b->L), root(b->L);
+    for (uint32_t l = 0; l < b->L; l++) {
+        if (slots[l] >= st->slots.size()) return fail(c, ESAT_E_ARG, "slot %u out of range", slots[l]);
+        const esat_store::Slot& s = st->slots[slots[l]];
+        if (s.n > b->nb[l + 1] - b->nb[l] || s.K > b->kb[l + 1] - b->kb[l] || s.U > b->ub[l + 1] - b->ub[l])
+            return fail(c, ESAT_E_ARG, "leaf %u: slot %u exceeds the arena span", l, slots[l]);
+        jobs[l] = SlotJob{l, s.n, s.K, s.U, s.on, s.of, s.ok, s.ou};
+        ncnt[l] = s.n; ucnt[l] = s.U; root[l] = s.root;
+    }
+    cudaStream_t q = c->stream;
+    const uint64_t N = b->N, K = b->K, U = b->U, L = b->L;
+    // unused span entries are zero, as in a host pack (arena.py pack_with_headroom)
+    CK(c, cudaMemsetAsync((void*)b->d.hc_sym, 0, 4 * N, q));
+    CK(c, cudaMemsetAsync((void*)b->d.hc_koff, 0, 4 * (N + L), q));
+    CK(c, cudaMemsetAsync((void*)b->d.hc_kids, 0, 4 * K, q));
+    CK(c, cudaMemsetAsync((void*)b->d.hc_cid, 0, 4 * N, q));
+    CK(c, cudaMemsetAsync((void*)b->d.hc_cost, 0, 8 * N, q));
+    CK(c, cudaMemsetAsync((void*)b->d.uf_parent_in, 0, 4 * U, q));
+    CK(c, cudaMemsetAsync((void*)b->d.uf_rank_in, 0, U, q));
+    CK(c, cudaMemcpyAsync((void*)b->d.root, root.data(), 4 * L, cudaMemcpyHostToDevice, q));
+    int r;
+    if (L) {
+        if ((r = store_jobs(st, jobs))) return r;
+        k_store_copy<false><<<b->L, 256, 0, q>>>(
+            b->d, reinterpret_cast<const SlotJob*>(st->d_job), st->sym, st->koff, st->kids, st->cid, st->cost,
+            st->parent, st->rank, const_cast<uint32_t*>(b->d.hc_sym), const_cast<uint32_t*>(b->d.hc_koff),
+            const_cast<uint32_t*>(b->d.hc_kids), const_cast<uint32_t*>(b->d.hc_cid), const_cast<double*>(b->d.hc_cost),
+            const_cast<uint32_t*>(b->d.uf_parent_in), const_cast<uint8_t*>(b->d.uf_rank_in));
+        if ((r = launch_check(c, "k_store_copy"))) return r;
+    }
+    b->uploaded = true;
+    b->rebuilt = false;
+    b->upload_gen++;
+    return esat_batch_set_counts(b, ncnt.data(), ucnt.data());   // synchronises the stream
+}
+
+}  // extern "C"

@@ -49,7 +49,6 @@ import numpy as np
 
 from . import native
 from .apply import ApplyDriver
-from .arena import Batch, LeafState
 from .pipeline import LeafPipeline
 
 NONE = 0xFFFFFFFF
@@ -185,7 +184,10 @@ class ExtractionCache:
 
 
 class DeviceEngine:
-    """Batched e-graph operations of the search on the device (one LeafPipeline per batch)."""
+    """Batched e-graph operations of the search on the device: one LeafPipeline for the whole
+    search, and every search state (tree node e-graph, rollout survivor) a slot of a device
+    SnapshotStore (EGraph.snapshot, egraph.py:300-312) -- batches are filled from slots and saved
+    back to slots device to device; host copies only for ``final`` and ``export_states``."""
 
     def __init__(self, rules, symtab, language, cost_config, ctx=None, method: str = "ocf", headroom: int = 4096):
         self.ctx = ctx or native.Context(0)
@@ -193,6 +195,7 @@ class DeviceEngine:
         self.method, self.headroom = method, headroom
         self.regrows = 0
         self._pipe = self._drv = None
+        self.store = None
         self.cache = None
         self._fp_symbols = -1
 
@@ -219,6 +222,7 @@ class DeviceEngine:
         the whole search; re-uploaded only when host interning added symbols."""
         self.symtab.finalize()
         if self._pipe is None:
+            self.store = native.SnapshotStore(self.ctx)
             self._pipe = LeafPipeline(self.ctx, self.symtab.arrays(), self.rules,
                                       lambda nm: self.symtab.name_id(nm, create=False), self.symtab.code,
                                       method=self.method, pool_entries_per_node=32)
@@ -228,11 +232,22 @@ class DeviceEngine:
         return self._pipe, self._drv
 
     def _open(self, states, headroom=None):
-        packed = Batch(states).pack_with_headroom(nodes=headroom or self.headroom)
+        """A batch of ``states`` (slots of this engine's store; host LeafStates are put into slots
+        first) with ``headroom`` spare e-nodes per leaf."""
         pipe, drv = self._ensure_pipe()
-        b = pipe.load(packed)
-        b.set_counts(packed["n_cnt"], packed["u_cnt"])
-        return [packed, pipe, b, drv, headroom or self.headroom]
+        slots = self.import_states(states)
+        layout, b = pipe.load_slots(self.store, slots, headroom or self.headroom)
+        return [layout, pipe, b, drv, headroom or self.headroom]
+
+    def import_states(self, states):
+        """Host LeafStates as slots of this engine's store (slots of this store pass through)."""
+        self._ensure_pipe()
+        sid = self.store.id
+        return [s if isinstance(s, native.Slot) and s.store == sid else self.store.put(s) for s in states]
+
+    def export_states(self, states):
+        """Slots as host LeafStates (for the multi-rank exchange, parallel.ShardedEngine)."""
+        return [self.store.download(s) if isinstance(s, native.Slot) else s for s in states]
 
     def _extract(self, b, method=None):
         out = native.extract_with_retry(b, method or self.method, factor=32, bitsets=2.0, light=True)
@@ -240,22 +255,9 @@ class DeviceEngine:
         cost[out["status"] != 0] = np.inf
         return cost, out
 
-    def _clean_states(self, packed, b, U=None):
-        """Every leaf's last rebuild as a LeafState (a snapshot, egraph.py:300-312). ``U`` are the
-        union-find id counts of that rebuild (default: the batch's live counts)."""
-        reb = b.download_rebuild()
-        if U is None:
-            U = b.live_counts()[1]
-        out = []
-        for l in range(packed["n_leaves"]):
-            n0, k0, u0 = (int(packed[k][l]) for k in ("node_base", "kid_base", "id_base"))
-            n = int(reb["n"][l])
-            koff = reb["hc_koff"][n0 + l:n0 + l + n + 1].copy()
-            out.append(LeafState(reb["hc_sym"][n0:n0 + n].copy(), koff, reb["hc_kids"][k0:k0 + int(koff[-1])].copy(),
-                                 reb["hc_cid"][n0:n0 + n].copy(), reb["hc_cost"][n0:n0 + n].copy(),
-                                 reb["uf_parent"][u0:u0 + int(U[l])].copy(), reb["uf_rank"][u0:u0 + int(U[l])].copy(),
-                                 int(packed["root"][l])))
-        return out
+    def _clean_states(self, packed, b):
+        """Every leaf's last rebuild as a new device slot (a snapshot, egraph.py:300-312; D2D)."""
+        return self.store.save(b, range(packed["n_leaves"]))
 
     def _applicable(self, pipe, b):
         """[L, R] is_rule_applicable (rewrite.py:579-589): one EXISTS-mode e-match of all sources."""
@@ -270,7 +272,6 @@ class DeviceEngine:
         rules = np.asarray(rules, np.uint32)
         while True:
             packed, pipe, b, drv, head = h
-            U0 = b.live_counts()[1]
             mask = pipe.rule_masks(rules)   # each leaf matches only the sources of its own rule
             pipe.ematch(mask)
             res = drv.apply(rules, leaf_mask=mask)
@@ -281,10 +282,12 @@ class DeviceEngine:
                 raise RuntimeError(f"k_apply: unexpected statuses {np.unique(st)}")
             if not np.any(st == native.A_CAPACITY):
                 return res
-            clean = self._clean_states(packed, b, U0)
+            mark = len(self.store)
+            clean = self._clean_states(packed, b)   # the rebuild k_apply read is left intact
             b.close()
             self.regrows += 1
             h[:] = self._open(clean, head * 4)
+            self.store.truncate(mark)               # the batch holds them now
             h[1].rebuild()
 
     # -- engine contract ----------------------------------------------------------------
@@ -347,10 +350,12 @@ class DeviceEngine:
                 break
             if not live[idx].all():          # compact: drop the leaves that stopped
                 keep = np.nonzero(live[idx])[0]
-                clean = self._clean_states(h[0], h[2])
+                mark = len(self.store)
+                clean = self.store.save(h[2], keep)
                 h[2].close()
                 idx = idx[keep]
-                h = self._open([clean[j] for j in keep])
+                h = self._open(clean)
+                self.store.truncate(mark)
                 h[1].rebuild()
             self._apply(h, rules[idx])
             h[1].rebuild()
@@ -381,7 +386,9 @@ class DeviceEngine:
         out = native.extract_with_retry(b, "ocf" if method == "exact" else method, factor=32, bitsets=2.0)
         cost = out["root_cost"].copy()
         cost[out["status"] != 0] = np.inf
-        clean = self._clean_states(packed, b)[0]
+        mark = len(self.store)
+        clean = self.store.download(self._clean_states(packed, b)[0])
+        self.store.truncate(mark)
         eg = to_egraph(clean, self.symtab, self.language)
         if not np.isfinite(cost[0]):
             b.close()

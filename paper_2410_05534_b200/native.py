@@ -9,7 +9,9 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from pathlib import Path
+from typing import NamedTuple
 
 import numpy as np
 
@@ -64,8 +66,19 @@ def lib():
                      "esat_copy_results", "esat_extract_async", "esat_wait_async", "esat_fork",
                      "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
                      "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
-                     "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts"):
+                     "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts",
+                     "esat_store_create", "esat_store_destroy", "esat_store_truncate", "esat_store_save",
+                     "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots"):
             getattr(L, name).restype = C.c_int
+        u32 = C.c_uint32
+        L.esat_store_size.restype = u32
+        L.esat_store_size.argtypes = [vp]
+        L.esat_store_truncate.argtypes = [vp, u32]
+        L.esat_store_save.argtypes = [vp, vp, u32, vp, vp]
+        L.esat_store_put.argtypes = [vp, u32, u32, u32, u32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.esat_store_info.argtypes = [vp, u32, vp, vp, vp, vp, vp]
+        L.esat_store_download.argtypes = [vp, u32, vp, vp, vp, vp, vp, vp, vp]
+        L.esat_batch_load_slots.argtypes = [vp, vp, vp]
         L.esat_apply_setup.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_uint32, vp, vp, C.c_uint32, vp,
                                        C.c_uint32, vp, C.c_uint32, vp, vp]
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
@@ -82,7 +95,9 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_extract_async", "esat_wait_async", "esat_last_async_ms", "esat_fork",
             "esat_batch_set_pool2", "esat_apply_setup", "esat_batch_set_counts", "esat_apply",
             "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
-            "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts")
+            "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts",
+            "esat_store_create", "esat_store_destroy", "esat_store_size", "esat_store_truncate", "esat_store_save",
+            "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots")
 
 A_OK, A_NODE_LIMIT, A_NEED_SYMBOL, A_CAPACITY, A_PROGRAM = range(5)
 
@@ -106,6 +121,7 @@ class Context:
             raise NativeUnavailable(f"esat_ctx_create(device={device}) failed with code {rc}: no usable B200")
         self.device = device
         self.symtab_version = None
+        self._children = weakref.WeakSet()   # batches / stores: released before the context
 
     def check(self, rc: int):
         if rc != OK:
@@ -113,6 +129,8 @@ class Context:
 
     def close(self):
         if self.h:
+            for ch in list(self._children):
+                ch.close()
             self.L.esat_ctx_destroy(self.h)
             self.h = None
 
@@ -184,6 +202,7 @@ class DeviceBatch:
         self.h = C.c_void_p()
         ctx.check(self.L.esat_batch_create(ctx.h, C.c_uint32(self.n_leaves), _p(self.nb), _p(self.kb), _p(self.ub),
                                            C.byref(self.h)))
+        ctx._children.add(self)
 
     def close(self):
         if self.h:
@@ -395,6 +414,102 @@ def extract_with_retry(batch: DeviceBatch, method: str, factor: float = 8.0, max
             batch.set_pool(factor, bitsets)
             continue
         return out
+
+
+class Slot(NamedTuple):
+    """A leaf e-graph state held in a device SnapshotStore (hashcons entries n, child slots K,
+    union-find ids U, raw root) -- the device counterpart of arena.LeafState."""
+    store: int
+    index: int
+    n: int
+    K: int
+    U: int
+    root: int
+
+    @property
+    def n_ids(self) -> int:
+        return self.U
+
+
+class SnapshotStore:
+    """EGraph.snapshot (egraph.py:300-312) on the device (esat_store): an append-only slot arena of
+    leaf states. ``save`` copies the last rebuild of batch leaves into new slots, ``load`` fills a
+    batch's input arena from slots -- both device to device."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self.L = ctx.L
+        self.h = C.c_void_p()
+        ctx.check(self.L.esat_store_create(ctx.h, C.byref(self.h)))
+        ctx._children.add(self)
+        self.id = id(self)
+
+    def close(self):
+        if self.h:
+            self.L.esat_store_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __len__(self):
+        return int(self.L.esat_store_size(self.h))
+
+    def truncate(self, count: int):
+        self.ctx.check(self.L.esat_store_truncate(self.h, count))
+
+    def _slots(self, idx) -> list:
+        idx = _u32(idx)
+        n, K, U, root = (np.zeros(len(idx), np.uint32) for _ in range(4))
+        self.ctx.check(self.L.esat_store_info(self.h, len(idx), _p(idx), _p(n), _p(K), _p(U), _p(root)))
+        return [Slot(self.id, int(i), int(a), int(b), int(c), int(r)) for i, a, b, c, r in zip(idx, n, K, U, root)]
+
+    def save(self, batch: "DeviceBatch", leaves) -> list:
+        leaves = _u32(leaves)
+        out = np.zeros(len(leaves), np.uint32)
+        self.ctx.check(self.L.esat_store_save(self.h, batch.h, len(leaves), _p(leaves), _p(out)))
+        return self._slots(out)
+
+    def put(self, st) -> Slot:
+        """A host LeafState into a new slot."""
+        arrs = [_u32(st.hc_sym), _u32(st.hc_koff), _u32(st.hc_kids), _u32(st.hc_cid),
+                np.ascontiguousarray(st.hc_cost, np.float64), _u32(st.uf_parent), np.ascontiguousarray(st.uf_rank, np.uint8)]
+        out = C.c_uint32()
+        self.ctx.check(self.L.esat_store_put(self.h, st.n, st.n_kids, st.n_ids, st.root & 0xFFFFFFFF,
+                                             *[_p(a) for a in arrs], C.byref(out)))
+        return self._slots([out.value])[0]
+
+    def download(self, slot: Slot):
+        """The slot as a host LeafState."""
+        from .arena import LeafState
+
+        o = [np.zeros(slot.n, np.uint32), np.zeros(slot.n + 1, np.uint32), np.zeros(slot.K, np.uint32),
+             np.zeros(slot.n, np.uint32), np.zeros(slot.n, np.float64), np.zeros(slot.U, np.uint32),
+             np.zeros(slot.U, np.uint8)]
+        self.ctx.check(self.L.esat_store_download(self.h, slot.index, *[_p(a) for a in o]))
+        return LeafState(*o, slot.root)
+
+    def layout(self, slots, nodes: int) -> dict:
+        """Arena bases for a batch of ``slots`` with ``nodes`` spare e-nodes per leaf (2x child slots,
+        1x ids), as arena.Batch.pack_with_headroom lays them out."""
+        L = len(slots)
+        nb, kb, ub = (np.zeros(L + 1, np.uint64) for _ in range(3))
+        nb[1:] = np.cumsum([s.n + nodes for s in slots])
+        kb[1:] = np.cumsum([s.K + 2 * nodes for s in slots])
+        ub[1:] = np.cumsum([s.U + nodes for s in slots])
+        return {"n_leaves": L, "node_base": nb, "kid_base": kb, "id_base": ub,
+                "root": np.array([s.root for s in slots], np.uint32),
+                "n_cnt": np.array([s.n for s in slots], np.uint32), "u_cnt": np.array([s.U for s in slots], np.uint32)}
+
+    def load(self, batch: "DeviceBatch", slots):
+        if any(s.store != self.id for s in slots):
+            raise ValueError("slot of another store")
+        idx = _u32([s.index for s in slots])
+        batch._slot_keep = idx
+        self.ctx.check(self.L.esat_batch_load_slots(batch.h, self.h, _p(idx)))
 
 
 def available() -> bool:

@@ -83,8 +83,9 @@ class ShardedEngine:
     therefore applies the same updates in selection order and holds the same tree; the search's RNG
     is consumed identically everywhere (rollouts carry their own seeds, mcts.py), so the search is
     the single-GPU search. The exchange per batch is the expansion rows (changed, cost, e-nodes,
-    e-classes, applicability bits and the child's e-graph, which any rank may expand later) and the
-    rollout rewards -- ``torch.distributed.all_gather_object`` over NCCL (gloo in the CPU tests).
+    e-classes, applicability bits and the child's e-graph, which any rank may expand later -- a device
+    engine's snapshot slots are exported to host states for the exchange and imported into every
+    rank's own store) and the rollout rewards -- ``torch.distributed.all_gather_object`` over NCCL (gloo in the CPU tests).
 
     ``evaluate`` / ``final`` / ``initial`` run redundantly on every rank (one e-graph each)."""
 
@@ -129,8 +130,13 @@ class ShardedEngine:
 
         s, e = leaf_shard(len(states), self.world, self.rank)
         part = self.engine.expand(states[s:e], list(rules[s:e])) if e > s else None
+        dev = self.world > 1 and hasattr(self.engine, "export_states")   # device snapshots travel as host states
+        if part is not None and dev:
+            part = (self.engine.export_states(part[0]), *part[1:])
         parts = [p for p in self._gather(part) if p is not None]
         kids = [k for p in parts for k in p[0]]
+        if dev:
+            kids = self.engine.import_states(kids)
         cat = [np.concatenate([p[i] for p in parts]) for i in range(1, 6)]
         return (kids, *cat)
 

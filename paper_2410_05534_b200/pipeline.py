@@ -81,6 +81,17 @@ class LeafPipeline:
         self.batch.upload(packed)
         return self.batch
 
+    def load_slots(self, store, slots, nodes: int):
+        """A batch of device snapshot slots with ``nodes`` spare e-nodes per leaf (D2D, no host
+        arena): native.SnapshotStore.layout + esat_batch_load_slots."""
+        if self.batch is not None:
+            self.batch.close()
+        layout = store.layout(slots, nodes)
+        self.batch = native.DeviceBatch(self.ctx, layout)
+        self.batch.set_pool(self.pool, self.pool_bitsets)
+        store.load(self.batch, slots)
+        return layout, self.batch
+
     def grow_pool(self, ext: dict) -> bool:
         """After an extraction that overflowed (ESAT_X_CAPACITY), grow the pool(s) named by the
         overflow mask in err_class. Returns False when nothing overflowed."""

@@ -14,7 +14,7 @@ def test_header_symbols_exported():
     from paper_2410_05534_b200 import native
 
     header = (ROOT / "include" / "esat_b200.h").read_text()
-    declared = set(re.findall(r"^(?:int|const char\*|float)\s+(esat_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^(?:int|uint32_t|const char\*|float)\s+(esat_\w+)\(", header, re.M))
     assert declared, "no declarations parsed"
     lib = native.lib()  # loads the sm_100a .so (no GPU needed to dlopen)
     missing = sorted(s for s in declared if not hasattr(lib, s))
