@@ -548,7 +548,7 @@ def measure_mcts(ctx, budget: int = 128, batch: int = 32, node_limit: int = 800)
     out = {"workload": f"nasrnn analog run_search: budget {budget}, batch {batch}, depth 10, node limit {node_limit}, "
                        f"seed 0",
            "device_iterations_per_s": budget / dt_dev, "device_s": dt_dev, "best_rule": best_dev,
-           "apply_regrows": dev_engine.regrows}
+           "apply_regrows": dev_engine.regrows, "apply_presized": dev_engine.presized}
     try:
         from oracle.mcts_ref import ReferenceEngine, import_reference
         from oracle.ref_pipeline import host_cores

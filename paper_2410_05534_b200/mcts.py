@@ -183,6 +183,9 @@ class ExtractionCache:
         return cost
 
 
+GROWTH_CAP = 1 << 22   # largest per-leaf growth bound an apply is pre-sized for (e-nodes)
+
+
 class DeviceEngine:
     """Batched e-graph operations of the search on the device: one LeafPipeline for the whole
     search, and every search state (tree node e-graph, rollout survivor) a slot of a device
@@ -193,7 +196,7 @@ class DeviceEngine:
         self.ctx = ctx or native.Context(0)
         self.rules, self.symtab, self.language, self.cfg = rules, symtab, language, cost_config
         self.method, self.headroom = method, headroom
-        self.regrows = 0
+        self.regrows = self.presized = 0
         self._pipe = self._drv = None
         self.store = None
         self.cache = None
@@ -231,13 +234,15 @@ class DeviceEngine:
             self._drv.upload()
         return self._pipe, self._drv
 
-    def _open(self, states, headroom=None):
+    def _open(self, states, headroom=None, kids=None):
         """A batch of ``states`` (slots of this engine's store; host LeafStates are put into slots
-        first) with ``headroom`` spare e-nodes per leaf."""
+        first) with ``headroom`` spare e-nodes per leaf (an int or one per leaf; ``kids`` spare child
+        slots, default 2x)."""
         pipe, drv = self._ensure_pipe()
         slots = self.import_states(states)
-        layout, b = pipe.load_slots(self.store, slots, headroom or self.headroom)
-        return [layout, pipe, b, drv, headroom or self.headroom]
+        head = self.headroom if headroom is None else headroom
+        layout, b = pipe.load_slots(self.store, slots, head, kids)
+        return [layout, pipe, b, drv, int(np.max(head)) if np.size(head) else self.headroom]
 
     def import_states(self, states):
         """Host LeafStates as slots of this engine's store (slots of this store pass through)."""
@@ -270,10 +275,33 @@ class DeviceEngine:
         from those rebuilt states with 4x the headroom and the same rules are re-applied: the
         result is the one an unbounded arena gives."""
         rules = np.asarray(rules, np.uint32)
+        sized = False
         while True:
             packed, pipe, b, drv, head = h
             mask = pipe.rule_masks(rules)   # each leaf matches only the sources of its own rule
             pipe.ematch(mask)
+            if not sized:
+                # a leaf whose matches could outgrow its spans (a multi-pattern explosion: tens of
+                # thousands of matches) is re-opened once with spans for the bound, so the apply
+                # runs once instead of failing at capacity on a ladder of growing arenas
+                sized = True
+                need_n, need_k = pipe.growth_bound(rules)
+                nb, kb, ub = (np.diff(packed[k].astype(np.int64)) for k in ("node_base", "kid_base", "id_base"))
+                spare_n = nb - packed["n_cnt"].astype(np.int64)
+                spare_k = kb - packed["k_cnt"].astype(np.int64)
+                spare_u = ub - packed["u_cnt"].astype(np.int64)
+                grow = (need_n > spare_n) | (need_k > spare_k) | (need_n > spare_u)
+                if np.any(grow) and int(need_n.max()) <= GROWTH_CAP:
+                    clean = self._clean_states(packed, b)
+                    b.close()
+                    mark = len(self.store) - len(clean)
+                    nodes = np.where(grow, np.maximum(need_n, head), head)
+                    kids = np.where(grow, np.maximum(need_k, 2 * nodes), 2 * nodes)
+                    h[:] = self._open(clean, nodes, kids)
+                    self.store.truncate(mark)
+                    self.presized += 1
+                    h[1].rebuild()
+                    continue
             res = drv.apply(rules, leaf_mask=mask)
             st = res["status"]
             if np.any(st == native.A_PROGRAM):

@@ -492,17 +492,21 @@ class SnapshotStore:
         self.ctx.check(self.L.esat_store_download(self.h, slot.index, *[_p(a) for a in o]))
         return LeafState(*o, slot.root)
 
-    def layout(self, slots, nodes: int) -> dict:
-        """Arena bases for a batch of ``slots`` with ``nodes`` spare e-nodes per leaf (2x child slots,
-        1x ids), as arena.Batch.pack_with_headroom lays them out."""
+    def layout(self, slots, nodes, kids=None) -> dict:
+        """Arena bases for a batch of ``slots`` with ``nodes`` spare e-nodes per leaf (an int or one
+        per leaf), ``kids`` spare child slots (default 2x nodes) and 1x nodes spare ids, as
+        arena.Batch.pack_with_headroom lays them out."""
         L = len(slots)
+        nodes = np.broadcast_to(np.asarray(nodes, np.int64), (L,))
+        kids = 2 * nodes if kids is None else np.broadcast_to(np.asarray(kids, np.int64), (L,))
         nb, kb, ub = (np.zeros(L + 1, np.uint64) for _ in range(3))
-        nb[1:] = np.cumsum([s.n + nodes for s in slots])
-        kb[1:] = np.cumsum([s.K + 2 * nodes for s in slots])
-        ub[1:] = np.cumsum([s.U + nodes for s in slots])
+        nb[1:] = np.cumsum([s.n + int(x) for s, x in zip(slots, nodes)])
+        kb[1:] = np.cumsum([s.K + int(x) for s, x in zip(slots, kids)])
+        ub[1:] = np.cumsum([s.U + int(x) for s, x in zip(slots, nodes)])
         return {"n_leaves": L, "node_base": nb, "kid_base": kb, "id_base": ub,
                 "root": np.array([s.root for s in slots], np.uint32),
-                "n_cnt": np.array([s.n for s in slots], np.uint32), "u_cnt": np.array([s.U for s in slots], np.uint32)}
+                "n_cnt": np.array([s.n for s in slots], np.uint32), "u_cnt": np.array([s.U for s in slots], np.uint32),
+                "k_cnt": np.array([s.K for s in slots], np.uint32)}
 
     def load(self, batch: "DeviceBatch", slots):
         if any(s.store != self.id for s in slots):

@@ -81,12 +81,12 @@ class LeafPipeline:
         self.batch.upload(packed)
         return self.batch
 
-    def load_slots(self, store, slots, nodes: int):
+    def load_slots(self, store, slots, nodes, kids=None):
         """A batch of device snapshot slots with ``nodes`` spare e-nodes per leaf (D2D, no host
         arena): native.SnapshotStore.layout + esat_batch_load_slots."""
         if self.batch is not None:
             self.batch.close()
-        layout = store.layout(slots, nodes)
+        layout = store.layout(slots, nodes, kids)
         self.batch = native.DeviceBatch(self.ctx, layout)
         self.batch.set_pool(self.pool, self.pool_bitsets)
         store.load(self.batch, slots)
@@ -166,6 +166,38 @@ class LeafPipeline:
             else:
                 progs.append(compile_rule_targets(r.rule, name_id, code, None, 0, r.pattern_ids[0]))
         return pack_rules(progs)
+
+    def leaf_rule_counts(self, leaf_rule) -> np.ndarray:
+        """Matches of leaf l's own rule ``leaf_rule[l]`` in the last e-match + join (0 for none): [L]."""
+        P = self.batch.download_counts(len(self.pattern_ids))
+        J = self.batch.download_counts(len(self.joins), from_join=True) if self.joins else None
+        out = np.zeros(len(leaf_rule), np.int64)
+        for l, r in enumerate(leaf_rule):
+            if int(r) == 0xFFFFFFFF:
+                continue
+            cr = self.rules[int(r)]
+            out[l] = J[self.joins.index(cr), l] if cr.multi else P[cr.pattern_ids[0], l]
+        return out
+
+    def growth_bound(self, leaf_rule) -> tuple:
+        """Upper bounds of the e-nodes and child slots applying ``leaf_rule[l]`` can add to leaf l:
+        its matches x the operator nodes (and their children) of the rule's targets -- an
+        instantiation adds at most one e-node per target operator (rewrite.py:517-523). [L] x 2"""
+        def apps(p):
+            if not hasattr(p, "children"):
+                return 0, 0
+            n, k = 1, len(p.children)
+            for ch in p.children:
+                a, b = apps(ch)
+                n, k = n + a, k + b
+            return n, k
+
+        per = [tuple(map(sum, zip(*[apps(t) for t in r.rule.targets]))) if r.rule.targets else (0, 0)
+               for r in self.rules]
+        cnt = self.leaf_rule_counts(leaf_rule)
+        nodes = np.array([0 if int(r) == 0xFFFFFFFF else per[int(r)][0] for r in leaf_rule], np.int64) * cnt
+        kids = np.array([0 if int(r) == 0xFFFFFFFF else per[int(r)][1] for r in leaf_rule], np.int64) * cnt
+        return nodes, kids
 
     def match_counts(self) -> np.ndarray:
         """Unique matches per rule per leaf of the last step: [rules, leaves]."""
