@@ -26,6 +26,7 @@ struct esat_ctx {
     // side stream: extraction overlaps e-matching (both only read the rebuilt view)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_done = nullptr, ev_s0 = nullptr, ev_s1 = nullptr;
+    cudaEvent_t ev_afork = nullptr, ev_ajoin = nullptr;   // esat_apply's two concurrent launches
     bool side_timed = false, side_pending = false, fork_armed = false;
     bool timed = false;
     // max-dynamic-SMEM attributes are per device: tracked per context (one context per device)
@@ -220,6 +221,8 @@ int esat_ctx_destroy(esat_ctx* c) {
     cudaFree(c->sym_par); cudaFree(c->d_pat); cudaFree(c->d_pat_off);
     if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_afork) cudaEventDestroy(c->ev_afork);
+    if (c->ev_ajoin) cudaEventDestroy(c->ev_ajoin);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     if (c->ev_s0) cudaEventDestroy(c->ev_s0);
     if (c->ev_s1) cudaEventDestroy(c->ev_s1);
@@ -1114,8 +1117,28 @@ int esat_apply(esat_batch* b, const uint32_t* leaf_rule, uint32_t node_limit) {
     a.s_pnext = b->a_pnext; a.s_eown = b->a_eown;
     static const int no_pot = getenv("ESAT_APPLY_NO_POT") ? 1 : 0;
     a.no_pot = no_pot;
+    // leaves with very many matches (multi-pattern explosions: tens of thousands) get a planner warp
+    // beside the replay warp; the rest run one warp each (16 resident leaves per SM) -- the two
+    // launches run concurrently. Measured (tools/ap_sweep.sh): a threshold of 256 gains 5 % on the
+    // NasRNN rollout step and loses 10 % on ResNeXt's (its many 256..600-match leaves fill the
+    // two-warp launch's 4 slots per SM), so only explosions take the two-warp path.
+    static const uint32_t heavy = getenv("ESAT_APPLY_HEAVY") ? (uint32_t)atoi(getenv("ESAT_APPLY_HEAVY")) : 2048u;
+    if (!c->ev_afork) {
+        CK(c, cudaEventCreateWithFlags(&c->ev_afork, cudaEventDisableTiming));
+        CK(c, cudaEventCreateWithFlags(&c->ev_ajoin, cudaEventDisableTiming));
+    }
     tic(c);
-    if (b->L) k_apply<<<b->L, 32, 0, c->stream>>>(d, a);
+    if (b->L) {
+        AArgs ah = a;
+        ah.sel_lo = heavy; ah.sel_hi = 0xFFFFFFFFu;
+        a.sel_lo = 0; a.sel_hi = heavy;
+        CK(c, cudaEventRecord(c->ev_afork, c->stream));
+        CK(c, cudaStreamWaitEvent(c->side, c->ev_afork, 0));
+        k_apply<2><<<b->L, 64, 0, c->side>>>(d, ah);
+        CK(c, cudaEventRecord(c->ev_ajoin, c->side));
+        k_apply<1><<<b->L, 32, 0, c->stream>>>(d, a);
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_ajoin, 0));
+    }
     toc(c);
     if ((r = launch_check(c, "k_apply"))) return r;
     b->counts = true;

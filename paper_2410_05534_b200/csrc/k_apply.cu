@@ -31,6 +31,8 @@ namespace {
 constexpr int INSTR = 20;
 constexpr int MAXI = 24;      // instructions per target
 constexpr uint32_t PLAN_CH = 32, PLAN_T = 2;   // matches planned per chunk (one per lane); targets per match
+constexpr uint32_t PMAX = 12;                  // instructions per target planned by the planner warp
+constexpr uint32_t PW = 3 * PMAX + 1;          // its plan words per target: symbol ids, f64 node costs, flags
 constexpr uint32_t PLAN_FAIL = 0xFFFFFFFDu;    // make_symbol fails (or, with PLAN_SLOW, is not interned)
 constexpr uint32_t PLAN_SLOW = 1u, PLAN_SHAPE_ERR = 2u, PLAN_SHAPE_MISMATCH = 4u;
 constexpr uint32_t NO_SHAPE = 255;
@@ -433,21 +435,27 @@ __device__ void raise_ancestors(Leaf& L, uint32_t w, uint32_t* qtail) {
 // class shapes, which no union inside an apply changes -- every union joins classes of one shape),
 // node cost from the symbol's shape and attributes
 __device__ uint32_t add_node_sid(Leaf& L, uint32_t sid, int op, uint32_t ar, const uint32_t* k, uint32_t* err,
-                                 bool known_absent) {
+                                 bool known_absent, const uint32_t* pcost) {
     if (!known_absent) {
         const uint32_t e0 = hc_get(L, sid, k, ar);
         if (e0 != NONE) return find(L, L.cid[e0]);
     }
     if (L.n + 1 > L.cap_n || L.K + ar > L.cap_k || L.U + 1 > L.cap_u) { *err = A_CAPACITY; return NONE; }
-    Shape cs[4];   // child class shapes: only the node cost needs them
-    for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, k[j]);
-    Sym s;
-    s.name = 0; s.arity = ar; s.np = 0;
-    s.shape = sym_shape(*L.a, sid);
-    s.ival[0] = INT_NONE;
-    if (op == OP_MAXPOOL) {
-        const uint32_t code = (uint32_t)L.d->sym_par[L.d->sym_poff[sid]];
-        s.ival[0] = code < L.a->n_values ? L.a->val_int[code] : INT_NONE;
+    double cost;
+    if (pcost) {   // priced by the planner warp
+        cost = __hiloint2double((int)pcost[1], (int)pcost[0]);
+    } else {
+        Shape cs[4];   // child class shapes: only the node cost needs them
+        for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, k[j]);
+        Sym s;
+        s.name = 0; s.arity = ar; s.np = 0;
+        s.shape = sym_shape(*L.a, sid);
+        s.ival[0] = INT_NONE;
+        if (op == OP_MAXPOOL) {
+            const uint32_t code = (uint32_t)L.d->sym_par[L.d->sym_poff[sid]];
+            s.ival[0] = code < L.a->n_values ? L.a->val_int[code] : INT_NONE;
+        }
+        cost = node_cost(*L.a, op, s, cs);
     }
     const uint32_t id = L.U++;
     const uint32_t e = L.n++;
@@ -462,7 +470,7 @@ __device__ uint32_t add_node_sid(Leaf& L, uint32_t sid, int op, uint32_t ar, con
         for (uint32_t i = 0; i < ar; i++) L.kids[k0 + i] = k[i];
         L.koff[e + 1] = L.K;
         L.cid[e] = id;
-        L.cost[e] = node_cost(*L.a, op, s, cs);
+        L.cost[e] = cost;
         hc_insert(L, e);
         list_push(L, id, e);
         if (L.usepot) {
@@ -518,14 +526,224 @@ __device__ bool union_classes(Leaf& L, uint32_t a, uint32_t b, uint32_t* qtail) 
     return true;
 }
 
+// One match of the ordered replay (rewrite.py:538-566): per target _target_refs, the cycle test, the
+// shape tests, the instantiation and the union. ``plan``: the match's plan (PS words per target,
+// flags at FL, node costs at PMAX when COST) or nullptr (full path).
+template <uint32_t PS, uint32_t FL, bool COST>
+__device__ __forceinline__ void replay_match(Leaf& L, const Dev& d, const AArgs& a, uint32_t rule, const int32_t* rp,
+                                             int32_t NT, const uint32_t* rec, const uint32_t* plan, uint32_t& st,
+                                             uint32_t& cyc, uint32_t& shp, uint32_t& unions, uint32_t* sh_qtail) {
+    for (int32_t t = 0; t < NT && st == A_OK; t++) {
+        const int32_t* tp = rp + rp[7 + t];
+        const uint32_t ni = (uint32_t)tp[0];
+        if (ni > MAXI) { st = A_PROGRAM; break; }
+        const uint32_t* pl = plan ? plan + t * PS : nullptr;
+        const uint32_t pflags = plan ? pl[FL] : PLAN_SLOW;
+        const bool fast = !(pflags & PLAN_SLOW);
+        const uint32_t matched = find(L, rec[t]);
+        // _target_refs (rewrite.py:463-489): refs set, existing instance class
+        uint32_t cid[MAXI];          // class of instruction i (NONE: not existing)
+        uint32_t vcls[MAXI];         // root of a var instruction's binding
+        uint8_t rmiss[MAXI];         // _target_refs probed instruction i (all children existed) and missed
+        uint32_t rbeg[MAXI], rend[MAXI];
+        uint32_t refs[64];
+        uint32_t nref = 0;
+        bool inst_err = false;
+        for (uint32_t i = 0; i < ni && !inst_err; i++) {
+            const int32_t* ins = tp + 1 + INSTR * i;
+            if (ins[0] == 0) {
+                const uint32_t c = find(L, rec[ins[1]]);
+                cid[i] = c;
+                vcls[i] = c;
+                rbeg[i] = nref;
+                if (nref < 64) refs[nref++] = c;
+                rend[i] = nref;
+                continue;
+            }
+            const uint32_t ar = (uint32_t)ins[3];
+            uint32_t b0 = nref;
+            bool all = true;
+            uint32_t kc[4];
+            for (uint32_t j = 0; j < ar; j++) {
+                const uint32_t ci = (uint32_t)ins[5 + j];
+                for (uint32_t r = rbeg[ci]; r < rend[ci]; r++)
+                    if (nref < 64) refs[nref++] = refs[r];
+                if (cid[ci] == NONE) all = false;
+                else kc[j] = cid[ci];
+            }
+            cid[i] = NONE;
+            rmiss[i] = 0;
+            if (all) {
+                uint32_t sid;
+                if (fast) {
+                    sid = pl[i];
+                    if (sid == PLAN_FAIL) { inst_err = true; break; }
+                } else {
+                    Shape cs[4];
+                    for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, kc[j]);
+                    Sym s;
+                    if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
+                    sid = sym_lookup(d, a, s);
+                }
+                const uint32_t e = sid == NONE ? NONE : hc_get(L, sid, kc, ar);
+                if (e != NONE) {
+                    const uint32_t c = find(L, L.cid[e]);
+                    cid[i] = c;
+                    nref = b0;
+                    refs[nref++] = c;
+                } else {
+                    rmiss[i] = 1;
+                }
+            }
+            rbeg[i] = b0;
+            rend[i] = nref;
+        }
+        if (nref >= 64) { st = A_PROGRAM; break; }
+        if (inst_err) { shp++; continue; }
+        const uint32_t top = ni - 1;
+        if (cid[top] != NONE && cid[top] == matched) continue;
+        bool ovf = false;
+        if (reaches(L, refs + rbeg[top], rend[top] - rbeg[top], matched, &ovf, sh_qtail)) { cyc++; continue; }
+        ovf = __any_sync(0xffffffffu, ovf);
+        if (ovf) { st = A_CAPACITY; break; }
+        // _instance_shape (rewrite.py:508-514) then the matched-class shape test
+        if (fast) {
+            if (pflags & (PLAN_SHAPE_ERR | PLAN_SHAPE_MISMATCH)) { shp++; continue; }
+            uint32_t inst[MAXI];
+            uint32_t err = A_OK;
+            // every inst[] is a root (a var's find from _target_refs -- adds do not move roots --,
+            // a hashcons hit's find, or a new id) and no union happens before the top one
+            // an instruction _target_refs found reuses that class (adds never remove a node and
+            // move no root); one it probed and missed is still missing unless this target
+            // already added a node (two instructions of one target may build the same node)
+            bool added = false;
+            for (uint32_t i = 0; i < ni && err == A_OK; i++) {
+                const int32_t* ins = tp + 1 + INSTR * i;
+                if (ins[0] == 0) { inst[i] = vcls[i]; continue; }
+                if (cid[i] != NONE) { inst[i] = cid[i]; continue; }
+                const uint32_t ar = (uint32_t)ins[3];
+                uint32_t kc[4];
+                for (uint32_t j = 0; j < ar; j++) kc[j] = inst[ins[5 + j]];
+                const uint32_t n0 = L.n;
+                inst[i] = add_node_sid(L, pl[i], ins[2], ar, kc, &err, rmiss[i] && !added, COST ? pl + PMAX + 2 * i : nullptr);
+                added = added || L.n != n0;
+            }
+            if (err != A_OK) { st = err; break; }
+            if (union_classes(L, inst[top], matched, sh_qtail)) unions++;
+            continue;
+        }
+        Shape sh[MAXI];
+        for (uint32_t i = 0; i < ni && !inst_err; i++) {
+            const int32_t* ins = tp + 1 + INSTR * i;
+            if (ins[0] == 0) { sh[i] = class_shape(L, rec[ins[1]]); continue; }
+            const uint32_t ar = (uint32_t)ins[3];
+            Shape cs[4];
+            for (uint32_t j = 0; j < ar; j++) cs[j] = sh[ins[5 + j]];
+            Sym s;
+            if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
+            sh[i] = s.shape;
+        }
+        if (inst_err) { shp++; continue; }
+        const Shape msh = class_shape(L, matched);
+        if (sh[top].nd != NO_SHAPE && msh.nd != NO_SHAPE && !shape_eq(sh[top], msh)) { shp++; continue; }
+        // _instantiate (rewrite.py:517-523) bottom-up, then union with the matched class
+        uint32_t inst[MAXI];
+        uint32_t err = A_OK;
+        for (uint32_t i = 0; i < ni && err == A_OK; i++) {
+            const int32_t* ins = tp + 1 + INSTR * i;
+            if (ins[0] == 0) { inst[i] = find(L, rec[ins[1]]); continue; }
+            const uint32_t ar = (uint32_t)ins[3];
+            uint32_t kc[4];
+            Shape cs[4];
+            for (uint32_t j = 0; j < ar; j++) { kc[j] = inst[ins[5 + j]]; cs[j] = class_shape(L, kc[j]); }
+            Sym s;
+            if (!make_symbol(a, ins, rec, cs, ar, s)) { err = A_PROGRAM; break; }   // checked above
+            for (uint32_t j = 0; j < ar; j++) kc[j] = find(L, kc[j]);
+            inst[i] = add_node(L, s, ins[2], kc, cs, &err);
+            if (err == A_NEED_SYMBOL && L.lane == 0) {   // describe the missing symbol for host interning
+                uint32_t* ms = a.missing + 16 * (uint64_t)L.l;
+                ms[0] = (uint32_t)s.name; ms[1] = s.arity; ms[2] = s.np;
+                for (int p = 0; p < 3; p++) { ms[3 + p] = s.code[p]; ms[6 + p] = (uint32_t)s.ival[p]; }
+                ms[9] = s.shape.nd;
+                for (int p = 0; p < 4; p++) ms[10 + p] = s.shape.d[p];
+                ms[14] = (uint32_t)rule; ms[15] = ((uint32_t)t << 8) | i;   // target, instruction
+            }
+        }
+        if (err != A_OK) { st = err; break; }
+        if (union_classes(L, inst[top], matched, sh_qtail)) unions++;
+    }
+}
+
+__device__ __forceinline__ Shape shape_of(const AArgs& a, uint32_t sid) {
+    Shape sh;
+    sh.nd = NO_SHAPE;
+    return sid == NONE ? sh : sym_shape(a, sid);
+}
+
+// Plan of one match for the two-warp replay (a lane of the planner warp), per target: for every instruction the symbol
+// make_symbol builds and its id (sym_lookup; PLAN_FAIL: make_symbol fails, or not interned with flag
+// PLAN_SLOW) and the node cost of an add; flags PLAN_SHAPE_ERR (_instance_shape fails) and
+// PLAN_SHAPE_MISMATCH (the matched-class shape test). All of it depends only on class shapes, which
+// no union of an apply changes (the shape test admits only same-shape unions; rebuilt classes are
+// shape-homogeneous), so the planner reads only what the replay never writes: the symbol tables and
+// symc, the symbol of every pre-apply class.
+__device__ __noinline__ void plan_match(const Dev& d, const AArgs& a, const int32_t* rp, int32_t NT, const uint32_t* prec,
+                           const uint32_t* symc, uint32_t (*pl)[PW]) {
+    for (int32_t t = 0; t < NT; t++) {
+        const int32_t* tp = rp + rp[7 + t];
+        const uint32_t ni = (uint32_t)tp[0];
+        uint32_t* p = pl[t];
+        uint32_t flags = 0;
+        if (ni > PMAX) { p[3 * PMAX] = PLAN_SLOW; continue; }
+        Shape shs[PMAX];
+        bool bad = false;
+        for (uint32_t i = 0; i < ni; i++) {
+            const int32_t* ins = tp + 1 + INSTR * i;
+            if (ins[0] == 0) { shs[i] = shape_of(a, symc[prec[ins[1]]]); continue; }
+            p[i] = PLAN_FAIL;
+            if (bad) continue;   // _instance_shape stops at its first failure
+            const uint32_t ar = (uint32_t)ins[3];
+            Shape cs[4];
+            for (uint32_t j = 0; j < ar; j++) cs[j] = shs[ins[5 + j]];
+            Sym ps;
+            if (!make_symbol(a, ins, prec, cs, ar, ps)) { bad = true; flags |= PLAN_SHAPE_ERR; continue; }
+            shs[i] = ps.shape;
+            const uint32_t sid = sym_lookup(d, a, ps);
+            if (sid == NONE) flags |= PLAN_SLOW;
+            p[i] = sid == NONE ? PLAN_FAIL : sid;
+            const double c = node_cost(a, ins[2], ps, cs);
+            p[PMAX + 2 * i] = (uint32_t)__double2loint(c);
+            p[PMAX + 2 * i + 1] = (uint32_t)__double2hiint(c);
+        }
+        if (!bad) {
+            const Shape msh = shape_of(a, symc[prec[t]]);
+            if (shs[ni - 1].nd != NO_SHAPE && msh.nd != NO_SHAPE && !shape_eq(shs[ni - 1], msh))
+                flags |= PLAN_SHAPE_MISMATCH;
+        }
+        p[3 * PMAX] = flags;
+    }
+}
+
 }  // namespace
 
-__global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
-    // one warp per leaf: the lanes stage the rebuilt state into the working arrays, build the
-    // class lists and the lookup table; lane 0 then replays the matches in order
-    const uint32_t l = blockIdx.x, lane = threadIdx.x;
+template <int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 1 ? 16 : 1) k_apply(Dev d, AArgs a) {
+    // warp 0 stages the rebuilt state into the working arrays, builds the class lists and the lookup
+    // table, then replays the matches in order. NW = 1: the lanes plan each chunk of matches before
+    // warp 0 replays it; NW = 2 (leaves with many matches): warp 1 plans the next chunk while warp 0
+    // replays the current one. A launch handles the leaves whose match count is in [sel_lo, sel_hi).
+    const uint32_t l = blockIdx.x, lane = threadIdx.x & 31u, warp = NW == 1 ? 0u : threadIdx.x >> 5;
     if (l >= d.L) return;
     const uint32_t rule = a.leaf_rule[l];
+    {
+        uint32_t cnt0 = 0;
+        if (rule != NONE) {
+            const int32_t* rp0 = a.prog + a.rule_off[rule];
+            const uint64_t mi = (uint64_t)rp0[1] * d.L + l;
+            cnt0 = rp0[0] ? a.j_count[mi] : a.m_count[mi];
+        }
+        if (cnt0 < a.sel_lo || cnt0 >= a.sel_hi) return;
+    }
     uint32_t* rep = a.report + 8 * (uint64_t)l;
     const uint64_t b = d.nb[l], k0 = d.kb[l], u0 = d.ub[l], t0 = d.tb[l];
     Leaf L;
@@ -547,6 +765,12 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
     L.tmask = (uint32_t)(d.tb[l + 1] - t0) - 1;
     L.stamp = 0;
     L.changed = false;
+    __shared__ uint32_t sh_qtail;
+    __shared__ uint32_t sh_plan[NW][PLAN_CH][PLAN_T][NW == 1 ? MAXI + 1 : PW];
+    __shared__ uint32_t sh_kahn, sh_stop[2];
+    L.lane = lane;
+    uint32_t* symc = a.s_pend + u0;   // NW = 2: symbol of every pre-apply class (the planner's shapes)
+    if (warp == 0) {
     // the rebuilt state becomes the working state: hashcons entries (canonical keys, classes
     // are roots), union-find, class membership lists, lookup table
     const uint32_t* okoff = d.o_koff + b + l;
@@ -577,12 +801,9 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
             if (atomicCAS(&L.tab[s], NONE, e) == NONE) break;
     }
     __syncwarp();
-    // from here every lane runs the same sequential replay (identical values in registers); state
-    // writes are issued by lane 0 and fenced with __syncwarp, the cycle test uses all lanes
-    __shared__ uint32_t sh_qtail;
-    __shared__ uint32_t sh_plan[PLAN_CH][PLAN_T][MAXI + 1];
-    L.lane = lane;
-    __shared__ uint32_t sh_kahn;
+    // from here every lane of warp 0 runs the same sequential replay (identical values in
+    // registers); state writes are issued by lane 0 and fenced with __syncwarp, the cycle test uses
+    // all lanes
     if (rule != NONE && L.usepot) {
         // cycle-test potentials of the rebuilt state: parent-edge lists (child slots, self-loops left
         // out), then Kahn rounds from the classes without children: pot = height; classes in or
@@ -638,6 +859,13 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
             if (L.head[c] != NONE && pend[c] != 0) L.pot[c] = round + 1;
         __syncwarp();
     }
+    if (NW == 2 && rule != NONE)   // (Kahn is done with pend: it becomes symc)
+        for (uint32_t x = lane; x < L.U; x += 32) {
+            const uint32_t e = L.head[find(L, x)];
+            symc[x] = e == NONE ? NONE : L.sym[e];
+        }
+    }   // warp 0
+    __syncthreads();
     uint32_t st = A_OK, found = 0, cyc = 0, shp = 0;
     const uint32_t n_before = L.n;
     uint32_t unions = 0;
@@ -658,6 +886,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
         // hashcons probes, the cycle test, adds, unions) and the reference's order. A target whose
         // plan hit a symbol the table lacks replays the full path (host interning, below).
         const bool planned = NT <= PLAN_T;
+        if constexpr (NW == 1) {
         for (uint32_t m0 = 0; m0 < cnt && st == A_OK; m0 += PLAN_CH) {
           const uint32_t m1 = min(cnt, m0 + PLAN_CH);
           if (planned) {
@@ -667,7 +896,7 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
                 for (int32_t t = 0; t < NT; t++) {
                     const int32_t* tp = rp + rp[7 + t];
                     const uint32_t ni = (uint32_t)tp[0];
-                    uint32_t* pl = sh_plan[lane][t];
+                    uint32_t* pl = sh_plan[0][lane][t];
                     uint32_t flags = 0;
                     if (ni > MAXI) { pl[MAXI] = PLAN_SLOW; continue; }
                     Shape shs[MAXI];
@@ -698,155 +927,43 @@ __global__ void __launch_bounds__(32) k_apply(Dev d, AArgs a) {
             __syncwarp();
           }
           for (uint32_t m = m0; m < m1 && st == A_OK; m++) {
-            const uint32_t* rec = words + (uint64_t)m * W;
-            for (int32_t t = 0; t < NT && st == A_OK; t++) {
-                const int32_t* tp = rp + rp[7 + t];
-                const uint32_t ni = (uint32_t)tp[0];
-                if (ni > MAXI) { st = A_PROGRAM; break; }
-                const uint32_t* pl = planned ? sh_plan[m - m0][t] : nullptr;
-                const uint32_t pflags = planned ? pl[MAXI] : PLAN_SLOW;
-                const bool fast = !(pflags & PLAN_SLOW);
-                const uint32_t matched = find(L, rec[t]);
-                // _target_refs (rewrite.py:463-489): refs set, existing instance class
-                uint32_t cid[MAXI];          // class of instruction i (NONE: not existing)
-                uint32_t vcls[MAXI];         // root of a var instruction's binding
-                uint8_t rmiss[MAXI];         // _target_refs probed instruction i (all children existed) and missed
-                uint32_t rbeg[MAXI], rend[MAXI];
-                uint32_t refs[64];
-                uint32_t nref = 0;
-                bool inst_err = false;
-                for (uint32_t i = 0; i < ni && !inst_err; i++) {
-                    const int32_t* ins = tp + 1 + INSTR * i;
-                    if (ins[0] == 0) {
-                        const uint32_t c = find(L, rec[ins[1]]);
-                        cid[i] = c;
-                        vcls[i] = c;
-                        rbeg[i] = nref;
-                        if (nref < 64) refs[nref++] = c;
-                        rend[i] = nref;
-                        continue;
-                    }
-                    const uint32_t ar = (uint32_t)ins[3];
-                    uint32_t b0 = nref;
-                    bool all = true;
-                    uint32_t kc[4];
-                    for (uint32_t j = 0; j < ar; j++) {
-                        const uint32_t ci = (uint32_t)ins[5 + j];
-                        for (uint32_t r = rbeg[ci]; r < rend[ci]; r++)
-                            if (nref < 64) refs[nref++] = refs[r];
-                        if (cid[ci] == NONE) all = false;
-                        else kc[j] = cid[ci];
-                    }
-                    cid[i] = NONE;
-                    rmiss[i] = 0;
-                    if (all) {
-                        uint32_t sid;
-                        if (fast) {
-                            sid = pl[i];
-                            if (sid == PLAN_FAIL) { inst_err = true; break; }
-                        } else {
-                            Shape cs[4];
-                            for (uint32_t j = 0; j < ar; j++) cs[j] = class_shape(L, kc[j]);
-                            Sym s;
-                            if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
-                            sid = sym_lookup(d, a, s);
-                        }
-                        const uint32_t e = sid == NONE ? NONE : hc_get(L, sid, kc, ar);
-                        if (e != NONE) {
-                            const uint32_t c = find(L, L.cid[e]);
-                            cid[i] = c;
-                            nref = b0;
-                            refs[nref++] = c;
-                        } else {
-                            rmiss[i] = 1;
-                        }
-                    }
-                    rbeg[i] = b0;
-                    rend[i] = nref;
-                }
-                if (nref >= 64) { st = A_PROGRAM; break; }
-                if (inst_err) { shp++; continue; }
-                const uint32_t top = ni - 1;
-                if (cid[top] != NONE && cid[top] == matched) continue;
-                bool ovf = false;
-                if (reaches(L, refs + rbeg[top], rend[top] - rbeg[top], matched, &ovf, &sh_qtail)) { cyc++; continue; }
-                ovf = __any_sync(0xffffffffu, ovf);
-                if (ovf) { st = A_CAPACITY; break; }
-                // _instance_shape (rewrite.py:508-514) then the matched-class shape test
-                if (fast) {
-                    if (pflags & (PLAN_SHAPE_ERR | PLAN_SHAPE_MISMATCH)) { shp++; continue; }
-                    uint32_t inst[MAXI];
-                    uint32_t err = A_OK;
-                    // every inst[] is a root (a var's find from _target_refs -- adds do not move roots --,
-                    // a hashcons hit's find, or a new id) and no union happens before the top one
-                    // an instruction _target_refs found reuses that class (adds never remove a node and
-                    // move no root); one it probed and missed is still missing unless this target
-                    // already added a node (two instructions of one target may build the same node)
-                    bool added = false;
-                    for (uint32_t i = 0; i < ni && err == A_OK; i++) {
-                        const int32_t* ins = tp + 1 + INSTR * i;
-                        if (ins[0] == 0) { inst[i] = vcls[i]; continue; }
-                        if (cid[i] != NONE) { inst[i] = cid[i]; continue; }
-                        const uint32_t ar = (uint32_t)ins[3];
-                        uint32_t kc[4];
-                        for (uint32_t j = 0; j < ar; j++) kc[j] = inst[ins[5 + j]];
-                        const uint32_t n0 = L.n;
-                        inst[i] = add_node_sid(L, pl[i], ins[2], ar, kc, &err, rmiss[i] && !added);
-                        added = added || L.n != n0;
-                    }
-                    if (err != A_OK) { st = err; break; }
-                    if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
-                    continue;
-                }
-                Shape sh[MAXI];
-                for (uint32_t i = 0; i < ni && !inst_err; i++) {
-                    const int32_t* ins = tp + 1 + INSTR * i;
-                    if (ins[0] == 0) { sh[i] = class_shape(L, rec[ins[1]]); continue; }
-                    const uint32_t ar = (uint32_t)ins[3];
-                    Shape cs[4];
-                    for (uint32_t j = 0; j < ar; j++) cs[j] = sh[ins[5 + j]];
-                    Sym s;
-                    if (!make_symbol(a, ins, rec, cs, ar, s)) { inst_err = true; break; }
-                    sh[i] = s.shape;
-                }
-                if (inst_err) { shp++; continue; }
-                const Shape msh = class_shape(L, matched);
-                if (sh[top].nd != NO_SHAPE && msh.nd != NO_SHAPE && !shape_eq(sh[top], msh)) { shp++; continue; }
-                // _instantiate (rewrite.py:517-523) bottom-up, then union with the matched class
-                uint32_t inst[MAXI];
-                uint32_t err = A_OK;
-                for (uint32_t i = 0; i < ni && err == A_OK; i++) {
-                    const int32_t* ins = tp + 1 + INSTR * i;
-                    if (ins[0] == 0) { inst[i] = find(L, rec[ins[1]]); continue; }
-                    const uint32_t ar = (uint32_t)ins[3];
-                    uint32_t kc[4];
-                    Shape cs[4];
-                    for (uint32_t j = 0; j < ar; j++) { kc[j] = inst[ins[5 + j]]; cs[j] = class_shape(L, kc[j]); }
-                    Sym s;
-                    if (!make_symbol(a, ins, rec, cs, ar, s)) { err = A_PROGRAM; break; }   // checked above
-                    for (uint32_t j = 0; j < ar; j++) kc[j] = find(L, kc[j]);
-                    inst[i] = add_node(L, s, ins[2], kc, cs, &err);
-                    if (err == A_NEED_SYMBOL && lane == 0) {   // describe the missing symbol for host interning
-                        uint32_t* ms = a.missing + 16 * (uint64_t)l;
-                        ms[0] = (uint32_t)s.name; ms[1] = s.arity; ms[2] = s.np;
-                        for (int p = 0; p < 3; p++) { ms[3 + p] = s.code[p]; ms[6 + p] = (uint32_t)s.ival[p]; }
-                        ms[9] = s.shape.nd;
-                        for (int p = 0; p < 4; p++) ms[10 + p] = s.shape.d[p];
-                        ms[14] = (uint32_t)rule; ms[15] = ((uint32_t)t << 8) | i;   // target, instruction
-                    }
-                }
-                if (err != A_OK) { st = err; break; }
-                if (union_classes(L, inst[top], matched, &sh_qtail)) unions++;
-            }
+            replay_match<MAXI + 1, MAXI, false>(L, d, a, rule, rp, NT, words + (uint64_t)m * W,
+                                                planned ? &sh_plan[0][m - m0][0][0] : nullptr, st, cyc, shp, unions,
+                                                &sh_qtail);
           }
         }
+        } else {
+        // NW = 2: warp 1 plans chunk c+1 (plan_match, with node costs) while warp 0 replays chunk c
+        const uint32_t nch = (cnt + PLAN_CH - 1) / PLAN_CH;
+        if (warp == 1 && planned && lane < min(cnt, PLAN_CH))
+            plan_match(d, a, rp, NT, words + (uint64_t)lane * W, symc, sh_plan[0][lane]);
+        __syncthreads();
+        for (uint32_t ch = 0; ch < nch; ch++) {
+            const uint32_t m0 = ch * PLAN_CH, m1 = min(cnt, m0 + PLAN_CH), buf = ch & 1u;
+            if (warp == 1) {
+                if (planned && m1 + lane < min(cnt, m1 + PLAN_CH))
+                    plan_match(d, a, rp, NT, words + (uint64_t)(m1 + lane) * W, symc, sh_plan[buf ^ 1u][lane]);
+            } else {
+                for (uint32_t m = m0; m < m1 && st == A_OK; m++)
+                    replay_match<PW, 3 * PMAX, true>(L, d, a, rule, rp, NT, words + (uint64_t)m * W,
+                                                     planned ? &sh_plan[buf][m - m0][0][0] : nullptr, st, cyc, shp,
+                                                     unions, &sh_qtail);
+                if (lane == 0) sh_stop[buf] = st;
+            }
+            __syncthreads();
+            if (sh_stop[buf] != A_OK) break;
+        }
+        }
     }
-    if (lane != 0) return;
+    if (warp != 0 || lane != 0) return;
     d.n_cnt[l] = L.n;
     d.u_cnt[l] = L.U;
     a.status[l] = st;
     rep[0] = found; rep[1] = L.changed ? 1u : 0u; rep[2] = cyc; rep[3] = shp;
     rep[4] = unions; rep[5] = L.n - n_before; rep[6] = 0; rep[7] = 0;
 }
+
+template __global__ void k_apply<1>(Dev, AArgs);
+template __global__ void k_apply<2>(Dev, AArgs);
 
 }  // namespace esat

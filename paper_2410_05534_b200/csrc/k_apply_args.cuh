@@ -42,9 +42,11 @@ struct AArgs {
     // cycle-test potentials: pot[U], parent-edge lists phead/ptail[U] over child slots pnext/eown[K],
     // Kahn pending counts pend[U]
     uint32_t *s_pot, *s_phead, *s_ptail, *s_pend, *s_pnext, *s_eown;
+    uint32_t sel_lo, sel_hi;   // the launch handles leaves whose rule has a match count in [sel_lo, sel_hi)
     int no_pot;   // 1: plain BFS without potential pruning (env ESAT_APPLY_NO_POT; for measurement)
 };
 
+template <int NW>
 __global__ void k_apply(Dev d, AArgs a);
 
 }  // namespace esat
