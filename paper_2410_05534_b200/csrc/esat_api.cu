@@ -11,6 +11,7 @@
 namespace esat {
 template <int T> __global__ void k_rebuild(Dev);
 template <int T> __global__ void k_extract(Dev, XArgs);
+__global__ void k_extract_order(Dev, uint32_t*);
 }  // namespace esat
 #include "k_ematch_args.cuh"
 #include "k_apply_args.cuh"
@@ -130,6 +131,7 @@ struct esat_batch {
     bool j_relaunch_needed = false, m_sig_matches_join = false, m_sized = false, j_sized = false;
     std::vector<uint32_t> m_sig, j_sig;
     uint32_t* d_lmask = nullptr;   // per-leaf pattern masks of the last esat_ematch_masked call
+    uint32_t* x_order = nullptr;   // k_extract's leaf order (largest first)
     bool lmask_on = false;
     // apply loop: live counts (valid once set by esat_batch_set_counts or an apply) + scratch
     bool counts = false;
@@ -483,6 +485,14 @@ static int launch_extract(esat_batch* b, int method, cudaStream_t s) {
     // SMs (one huge e-graph, config 4) gives each leaf four warps for its wide levels instead
     static const int xt_env = getenv("ESAT_EXTRACT_THREADS") ? atoi(getenv("ESAT_EXTRACT_THREADS")) : 0;
     const int xt = xt_env ? xt_env : (b->L < 148 ? 128 : 32);
+    // more leaves than one wave holds: largest leaves first (k_extract_order)
+    static const int xo_env = getenv("ESAT_EXTRACT_ORDER") ? atoi(getenv("ESAT_EXTRACT_ORDER")) : 1;
+    x.lorder = nullptr;
+    if (xo_env && b->L > 148u * 32u) {
+        if (!b->x_order) OWN(b->x_order, b->L);
+        k_extract_order<<<1, 1024, 0, s>>>(b->d, b->x_order);
+        x.lorder = b->x_order;
+    }
     if (b->L) {
         if (xt == 128) k_extract<128><<<b->L, 128, 0, s>>>(b->d, x);
         else if (xt == 64) k_extract<64><<<b->L, 64, 0, s>>>(b->d, x);

@@ -67,6 +67,7 @@ struct XArgs {
     uint32_t* lhn;               // [node rows] flushed node of each class at its last merge (flush reuse)
     double* lcc;                 // [2 x node rows] its child contributions (cc1, cc2)
     uint64_t slot_stride;
+    const uint32_t* lorder;      // CTA -> leaf (largest leaves first), or null (identity)
 };
 
 enum : uint32_t { X_OK = 0, X_NOT_CONVERGED = 1, X_INFEASIBLE = 2, X_CYCLIC = 3, X_CHILD_NOT_CHOSEN = 4,

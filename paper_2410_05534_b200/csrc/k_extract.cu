@@ -297,7 +297,7 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
 
 template <int T>
 __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // <= 64 regs: 32 resident leaves per SM
-    const uint32_t l = blockIdx.x, tid = threadIdx.x;
+    const uint32_t l = x.lorder ? x.lorder[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
     const uint64_t b = d.nb[l], k0 = d.kb[l];
     const uint32_t C = d.v_C[l];
     const uint32_t* coff = d.cls_off + b + l;
@@ -671,6 +671,29 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
         uint8_t* state = x.reach + b;
         for (uint32_t k = tid; k < C; k += T) state[k] = state[k] == 2 ? 1 : 0;
     }
+}
+
+// Longest-first leaf order for k_extract (one CTA): a leaf's extraction time grows with its class
+// count, and a batch of several waves finishes sooner when the largest leaves start first (the
+// last wave is then made of small leaves). Counting sort of the leaves by descending class count in
+// 256 buckets of 8 classes; order inside a bucket is arbitrary (every leaf's result is independent
+// of the order).
+__global__ void k_extract_order(Dev d, uint32_t* order) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t sh_scan[33];
+    const uint32_t L = d.L;
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < L; l += blockDim.x) atomicAdd(&hist[255 - min(d.v_C[l] >> 3, 255u)], 1u);
+    __syncthreads();
+    uint32_t tot;
+    const uint32_t v = threadIdx.x < 256 ? hist[threadIdx.x] : 0u;
+    const uint32_t p = block_exscan(v, sh_scan, &tot);
+    __syncthreads();
+    if (threadIdx.x < 256) hist[threadIdx.x] = p;
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < L; l += blockDim.x)
+        order[atomicAdd(&hist[255 - min(d.v_C[l] >> 3, 255u)], 1u)] = l;
 }
 
 template __global__ void k_extract<32>(Dev, XArgs);
