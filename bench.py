@@ -585,6 +585,7 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the per_config sweep of the other leaf sets")
     ap.add_argument("--no-mcts", action="store_true", help="skip the MCTS search measurement")
     ap.add_argument("--config-steps", type=int, default=20)
+    ap.add_argument("--quick", action="store_true", help="A/B timing only: skip the fingerprint and apply keys")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ocf-pool", type=float, default=32.0,
                     help="OCF history pool entries per e-node (grown automatically if too small)")
@@ -613,8 +614,8 @@ def main():
     head = measure_config(ctx, stream, dev, args.model, B, K, args.warmup, world, rank, args.e2e_steps, args.ocf_pool,
                           clocks=clk)
     leaves, symarr, name_id, code, ref_ocf, meta, pipe, batch = head.pop("_keep")
-    fp_line = measure_fingerprint(ctx, batch, meta)
-    apply_line = measure_apply(ctx, leaves, min(B, 4096), rank * B, symarr, name_id, code, meta)
+    fp_line = None if args.quick else measure_fingerprint(ctx, batch, meta)
+    apply_line = None if args.quick else measure_apply(ctx, leaves, min(B, 4096), rank * B, symarr, name_id, code, meta)
     per_config = {}
     if not args.no_configs:
         for m in ("bert", "nasrnn", "resnext50", "inception_v3", "nasnet_a"):

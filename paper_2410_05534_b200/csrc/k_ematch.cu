@@ -285,8 +285,14 @@ __device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
 
 }  // namespace
 
+#ifndef ESAT_EMATCH_MINB
+#define ESAT_EMATCH_MINB 1
+#endif
+#ifndef ESAT_JOIN_MINB
+#define ESAT_JOIN_MINB 1
+#endif
 template <int T>
-__global__ void __launch_bounds__(T) k_ematch(Dev d, MArgs a) {
+__global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a) {
     // One CTA per leaf runs every pattern of the call. The leaf's clean view (class ids/offsets,
     // node symbols, child CSR) is staged into shared memory with TMA bulk copies when it fits,
     // so the backtracking matcher's dependent loads hit SMEM instead of L2.
@@ -1057,7 +1063,7 @@ __global__ void __launch_bounds__(T) k_join_big(uint32_t L, JArgs a) {
 }
 
 template <int T>
-__global__ void __launch_bounds__(T) k_join(uint32_t L, JArgs a) {
+__global__ void __launch_bounds__(T, ESAT_JOIN_MINB) k_join(uint32_t L, JArgs a) {
     const uint32_t l = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
     __shared__ uint32_t sh_scan[33];
     __shared__ unsigned long long sh_base;

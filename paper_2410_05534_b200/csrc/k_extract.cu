@@ -40,7 +40,9 @@ namespace esat {
 namespace {
 
 struct Hist {
-    const uint32_t* bits;   // block base; words outside [4*lo4, 4*hi4) are zero (not stored)
+    // block base; words outside [4*lo4, 4*hi4) are zero (not stored). An absent history has
+    // lo4 == hi4 == 0, so the range tests below need no separate presence test.
+    const uint32_t* bits;
     uint32_t lo4, hi4;      // occupied uint4-group range
     bool present;
 };
@@ -52,7 +54,8 @@ struct LeafCtx {
     const double *ncost, *cost, *prev;
     const uint32_t* pk;        // history blocks (leaf base applied)
     const double* pv;          // value pool
-    const uint32_t *hoff[2], *hrng[2];
+    const uint32_t *hoff, *hrng;   // parity p at + p * ss (pointer arithmetic: no local-memory array)
+    uint64_t ss;
 };
 
 __device__ __forceinline__ double child_cost(const LeafCtx& c, uint32_t j) {
@@ -66,8 +69,9 @@ __device__ __forceinline__ Hist child_hist(const LeafCtx& c, uint32_t j) {
     if (j < c.k) par = c.pass & 1;                // flushed earlier in this pass
     else if (c.pass == 0) return h;               // not flushed yet
     else par = (c.pass - 1) & 1;                  // last pass's flush
-    h.bits = c.pk + c.hoff[par][j];
-    const uint32_t rg = c.hrng[par][j];
+    const uint64_t at = (uint64_t)par * c.ss + j;
+    h.bits = c.pk + c.hoff[at];
+    const uint32_t rg = c.hrng[at];
     h.lo4 = rg & 0xFFFFu;
     h.hi4 = rg >> 16;
     h.present = true;
@@ -80,18 +84,15 @@ __device__ __forceinline__ const double* wmax_of(const LeafCtx& c, const Hist& h
 }
 
 __device__ __forceinline__ bool hbit(const Hist& h, uint32_t key) {
-    const uint32_t g = key >> 7;
-    return h.present && g >= h.lo4 && g < h.hi4 && ((h.bits[key >> 5] >> (key & 31)) & 1u);
+    return ((key >> 7) - h.lo4 < h.hi4 - h.lo4) && ((h.bits[key >> 5] >> (key & 31)) & 1u);
 }
 
 __device__ __forceinline__ uint4 hword4(const Hist& h, uint32_t w4) {
-    return (h.present && w4 >= h.lo4 && w4 < h.hi4) ? reinterpret_cast<const uint4*>(h.bits)[w4]
-                                                    : make_uint4(0, 0, 0, 0);
+    return (w4 - h.lo4 < h.hi4 - h.lo4) ? reinterpret_cast<const uint4*>(h.bits)[w4] : make_uint4(0, 0, 0, 0);
 }
 
 __device__ __forceinline__ uint32_t hword(const Hist& h, uint32_t w) {
-    const uint32_t g = w >> 2;
-    return (h.present && g >= h.lo4 && g < h.hi4) ? h.bits[w] : 0u;
+    return ((w >> 2) - h.lo4 < h.hi4 - h.lo4) ? h.bits[w] : 0u;
 }
 
 __device__ __forceinline__ uint32_t bit_of(uint32_t key, uint32_t w) {
@@ -128,6 +129,24 @@ __device__ double overlap_max(const LeafCtx& c, const Hist& hA, uint32_t sA, con
         }
     }
     return m;
+}
+
+// Value of the merged history at the key of ``bit`` (one set bit of word w): sA's, then sB's
+// contribution, then hA's value, then hB's (precedence of Alg. 2's dictionary writes). Branch-free
+// -- lanes of a warp merge different words of different classes, and a per-source branch would
+// serialise them; the load address falls back to the (valid) pool base for sA / sB keys.
+__device__ __forceinline__ double merged_value(uint32_t bit, uint32_t wA, uint32_t wB, const double* va,
+                                               const double* vb, uint32_t sAw, uint32_t sBw, double vA, double vB,
+                                               const double* pool) {
+    const uint32_t below = bit - 1u;
+    const bool inA = wA & bit, inB = wB & bit;
+    const uint32_t ia = __popc(wA & below), ib = __popc(wB & below);
+    const double* base = inA ? va : (inB ? vb : pool);
+    const uint32_t idx = inA ? ia : (inB ? ib : 0u);
+    double v = base[idx];
+    v = (sBw & bit) ? vB : v;
+    v = (sAw & bit) ? vA : v;
+    return v;
 }
 
 // Merged history hA + {sA: vA} + hB + {sB: vB} with precedence sA, sB, hA, hB (first writer of a
@@ -174,7 +193,7 @@ __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, d
     const double* mO = hO.present ? wmax_of(c, hO) : nullptr;
     uint32_t o = base;
     for (uint32_t w = 4 * lo; w < 4 * hi; w++) {
-        const uint32_t wA = hword(hA, w), wB = hword(hB, w), sp = bit_of(sA, w) | bit_of(sB, w);
+        const uint32_t wA = hword(hA, w), wB = hword(hB, w), sAw = bit_of(sA, w), sBw = bit_of(sB, w), sp = sAw | sBw;
         uint32_t ow = wA | wB | sp;
         ob[w] = ow;
         // same keys as the previous flush so far? (then its values are the comparison)
@@ -202,15 +221,10 @@ __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, d
             bool eq = true;
             uint32_t m = ow;
             for (int i = 0; m && eq; i++) {
-                const int bpos = __ffs(m) - 1;
-                const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
-                double val;
-                if (key == sA) val = vA;
-                else if (key == sB) val = vB;
-                else if ((wA >> bpos) & 1u) val = va[__popc(wA & below)];
-                else val = vb[__popc(wB & below)];
+                const uint32_t bit = m & (0u - m);
+                const double val = merged_value(bit, wA, wB, va, vb, sAw, sBw, vA, vB, c.pv);
                 eq = __double_as_longlong(val) == __double_as_longlong(vo[i]);
-                m &= m - 1;
+                m ^= bit;
             }
             if (eq) { optr[w] = pO[w]; omax[w] = mO[w]; continue; }
             dif = true;
@@ -218,16 +232,11 @@ __device__ uint32_t merge_write(const LeafCtx& c, const Hist& hA, uint32_t sA, d
         optr[w] = o;
         double mx = 0.0;
         while (ow) {
-            const int bpos = __ffs(ow) - 1;
-            const uint32_t key = 32 * w + bpos, below = (1u << bpos) - 1u;
-            double val;
-            if (key == sA) val = vA;
-            else if (key == sB) val = vB;
-            else if ((wA >> bpos) & 1u) val = va[__popc(wA & below)];
-            else val = vb[__popc(wB & below)];
+            const uint32_t bit = ow & (0u - ow);
+            const double val = merged_value(bit, wA, wB, va, vb, sAw, sBw, vA, vB, c.pv);
             pv[o++] = val;
             mx = pymax(mx, val);
-            ow &= ow - 1;
+            ow ^= bit;
         }
         omax[w] = mx;
     }
@@ -319,8 +328,9 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     double* lcc = x.lcc + 2 * b;         // its two child contributions then
     const bool ocf = x.method == 1;
     uint64_t capk = 0, capv = 0;
-    uint32_t* hoffw[2] = {nullptr, nullptr};
-    uint32_t* hrngw[2] = {nullptr, nullptr};
+    uint32_t* hoffw = nullptr;   // [parity * ss + class]
+    uint32_t* hrngw = nullptr;
+    const uint64_t ss = x.slot_stride;
     uint32_t* pkw = nullptr;
     double* pvw = nullptr;
     if (ocf) {
@@ -331,11 +341,9 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
         pvw = x.pool_val + pbv;
         c.pk = pkw;
         c.pv = pvw;
-        for (int p = 0; p < 2; p++) {
-            hoffw[p] = x.hoff + p * x.slot_stride + b;
-            hrngw[p] = x.hrng + p * x.slot_stride + b;
-            c.hoff[p] = hoffw[p]; c.hrng[p] = hrngw[p];
-        }
+        hoffw = x.hoff + b;
+        hrngw = x.hrng + b;
+        c.hoff = hoffw; c.hrng = hrngw; c.ss = ss;
     }
 
     __shared__ uint32_t sh_scan[33];
@@ -443,8 +451,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 if (!need) {
                     chg_cur[k] = 0;
                     if (ocf && C > 1) {
-                        hoffw[par][k] = hoffw[ppar][k];
-                        hrngw[par][k] = hrngw[ppar][k];
+                        hoffw[par * ss + k] = hoffw[ppar * ss + k];
+                        hrngw[par * ss + k] = hrngw[ppar * ss + k];
                     }
                     continue;
                 }
@@ -500,8 +508,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                     if (pass < 2) atomicAdd(&dbg[pass][same ? 3 : 2], 1u);
 #endif
                     if (same) {
-                        hoffw[par][k] = hoffw[ppar][k];
-                        hrngw[par][k] = hrngw[ppar][k];
+                        hoffw[par * ss + k] = hoffw[ppar * ss + k];
+                        hrngw[par * ss + k] = hrngw[ppar * ss + k];
                     } else if (C > 1) {
                         lhn[k] = h_gen ? NONE - 1 : hkey;
                         lcc[2 * k] = h_cc1;
@@ -524,8 +532,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                             } else {
                                 Hist hO{nullptr, 0u, 0u, false};
                                 if (pass > 0) {
-                                    const uint32_t r2 = hrngw[ppar][k];
-                                    hO = Hist{pkw + hoffw[ppar][k], r2 & 0xFFFFu, r2 >> 16, true};
+                                    const uint32_t r2 = hrngw[ppar * ss + k];
+                                    hO = Hist{pkw + hoffw[ppar * ss + k], r2 & 0xFFFFu, r2 >> 16, true};
                                 }
                                 rng = merge_write(c, h1, c1, h_cc1, h2, c2, h_cc2, pkw + offk, &sh_topv, capv, pvw,
                                                   &sh_over, hO, &mchg);
@@ -534,12 +542,12 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                             }
                         }   // else: empty history (no node, or a leaf node): the empty range, no block
                         if (!ok) { offk = 0; rng = 0; atomicOr(&sh_over, 4u); }   // status reports it
-                        hoffw[par][k] = offk;
-                        hrngw[par][k] = rng;
+                        hoffw[par * ss + k] = offk;
+                        hrngw[par * ss + k] = rng;
                         hchg = pass == 0;
                         if (merged) hchg = mchg;   // answered by the merge
                         else if (!hchg) {  // did the flushed history change w.r.t. last pass?
-                            const uint32_t ok2 = hoffw[ppar][k], r2 = hrngw[ppar][k];
+                            const uint32_t ok2 = hoffw[ppar * ss + k], r2 = hrngw[ppar * ss + k];
                             const uint32_t la = rng & 0xFFFFu, ha = rng >> 16, lb = r2 & 0xFFFFu, hb2 = r2 >> 16;
                             const uint32_t lo = min(la, lb), hi = max(ha, hb2);
                             const uint32_t* a1 = pkw + offk;

@@ -17,6 +17,8 @@ import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / ("libesat_b200_debug.so" if os.environ.get("ESAT_DEBUG_LIB") else "libesat_b200.so")
+if os.environ.get("ESAT_LIB"):   # measurement A/B: an in-tree variant build (csrc/Makefile `variant`)
+    LIB_PATH = LIB_DIR / os.environ["ESAT_LIB"]
 NONE = 0xFFFFFFFF
 
 OK, E_ARG, E_CUDA, E_CAPACITY, E_STATE = 0, 1, 2, 3, 4

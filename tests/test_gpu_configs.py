@@ -1,7 +1,8 @@
 """The five BASELINE configs' leaf sets (reference-generated MCTS rollout leaves,
 tests/golden/bench_<model>.npz): the device pipeline must reproduce the reference's OCF and
 default-greedy root costs bit-exactly on every leaf, and the CPU oracle's per-rule match counts,
-merge counts and chosen e-nodes."""
+merge counts, every match record
+(in order) and chosen e-nodes."""
 
 import numpy as np
 import pytest
@@ -44,12 +45,22 @@ def test_config_leaves_bit_exact(model):
     ov = O.rebuild(packed, symarr["rank"], threads=8)
     assert np.array_equal(view["merges"], ov["merges"]) and np.array_equal(view["C"], ov["C"])
     for j, r in enumerate(pipe.rules):
+        # every match record, in the reference's order (not just the counts): the device lists
+        # and the oracle's share the [leaf][match][W words] layout
         if r.multi:
-            _, _, cnt, _ = O.joint(packed, ov, symarr, r._programs, r.var_maps, r.pvar_maps, len(r.var_names),
-                                   len(r.pvar_names), threads=8)
+            ow, ooff, cnt, W = O.joint(packed, ov, symarr, r._programs, r.var_maps, r.pvar_maps, len(r.var_names),
+                                       len(r.pvar_names), threads=8)
+            dw, doff, dcnt = b.download_matches(pipe.joins.index(r), from_join=True)
         else:
-            _, _, cnt, _ = O.ematch(packed, ov, symarr, r._programs[0], threads=8)
+            ow, ooff, cnt, W = O.ematch(packed, ov, symarr, r._programs[0], threads=8)
+            dw, doff, dcnt = b.download_matches(r.pattern_ids[0])
         assert np.array_equal(counts[j], cnt), (model, r.rule.id)
+        assert np.array_equal(dcnt, cnt), (model, r.rule.id)
+        for l in range(packed["n_leaves"]):
+            n = int(cnt[l]) * W
+            got = dw[int(doff[l]):int(doff[l]) + n]
+            want = ow[int(ooff[l]):int(ooff[l]) + n]
+            assert np.array_equal(got, want), (model, r.rule.id, l)
     b.close()
     ctx.close()
     del json
