@@ -108,11 +108,14 @@ int esat_batch_upload(esat_batch* b, const uint32_t* hc_sym, const uint32_t* hc_
 /* EGraph.rebuild over every leaf; per-leaf merge counts stay on device (download below) */
 int esat_rebuild(esat_batch* b);
 
-/* e-match patterns[0..n) over every leaf (mode LIST or EXISTS) */
+/* e-match patterns[0..n) over every leaf (mode LIST or EXISTS); n <= ESAT_MAX_CALL_PATTERNS
+ * (one CTA per leaf and 32-pattern chunk) */
+#define ESAT_MAX_CALL_PATTERNS 1024u
 int esat_ematch(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode);
-/* the same, with a per-leaf pattern mask: bit p of leaf_mask[l] selects call-pattern p on leaf l
- * (0: the leaf is not matched, its counts are 0). An MCTS rollout step matches only the sources of
- * the rule each leaf applies; joins of unmatched sources are empty. */
+/* the same, with per-leaf pattern masks: ceil(n/32) words per leaf, chunk-major -- bit p of
+ * leaf_mask[c * n_leaves + l] selects call-pattern 32c+p on leaf l (0: the leaf is not matched, its
+ * counts are 0). An MCTS rollout step matches only the sources of the rule each leaf applies
+ * (SPEC.md:603-611); joins of unmatched sources are empty. */
 int esat_ematch_masked(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode,
                        const uint32_t* leaf_mask);
 /* joint_match of multi-pattern rules over the LIST results of their source patterns.

@@ -130,7 +130,8 @@ struct esat_batch {
     bool m_verified = false, m_pending = false, j_verified = false, j_pending = false;
     bool j_relaunch_needed = false, m_sig_matches_join = false, m_sized = false, j_sized = false;
     std::vector<uint32_t> m_sig, j_sig;
-    uint32_t* d_lmask = nullptr;   // per-leaf pattern masks of the last esat_ematch_masked call
+    uint32_t* d_lmask = nullptr;   // per-leaf pattern masks of the last esat_ematch_masked call ([chunk][leaf])
+    uint32_t raw_chunks = 0, lmask_chunks = 0;   // pattern chunks (32 patterns each) d_raw / d_lmask hold
     uint32_t* x_order = nullptr;   // k_extract's leaf order (largest first)
     bool lmask_on = false;
     // apply loop: live counts (valid once set by esat_batch_set_counts or an apply) + scratch
@@ -685,6 +686,7 @@ static int ematch_launch(esat_batch* b) {
     MArgs a{};
     a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = b->m_mode;
     a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw; a.nzl = b->d_raw + 32ull * (b->N + 1);
+    a.chunk_stride = 64ull * (b->N + 1);
     a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
     Dev d = b->d;
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
@@ -698,7 +700,7 @@ static int ematch_launch(esat_batch* b) {
         c->ematch_attr = cap_bytes;
     }
     tic(c);
-    if (L && P) k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, a);
+    if (L && P) k_ematch<128><<<dim3((unsigned)L, (P + 31) / 32), 128, a.smem_bytes, c->stream>>>(d, a);
     toc(c);
     if ((r = launch_check(c, "k_ematch"))) return r;
     return ESAT_OK;
@@ -756,7 +758,8 @@ int esat_ematch(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode) {
 
 int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int mode, const uint32_t* leaf_mask) {
     if (!b || (P && !pat_ids) || (mode != ESAT_MATCH_LIST && mode != ESAT_MATCH_EXISTS)) return ESAT_E_ARG;
-    if (P > 32) return fail(b->ctx, ESAT_E_ARG, "at most 32 patterns per esat_ematch call (got %u)", P);
+    if (P > ESAT_MAX_CALL_PATTERNS)
+        return fail(b->ctx, ESAT_E_ARG, "at most %u patterns per esat_ematch call (got %u)", ESAT_MAX_CALL_PATTERNS, P);
     esat_ctx* c = b->ctx;
     if (!b->rebuilt) return fail(c, ESAT_E_STATE, "ematch requires a rebuilt e-graph");
     for (uint32_t i = 0; i < P; i++)
@@ -773,14 +776,22 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
     sig.push_back(c->pat_gen);
     sig.push_back(c->sym_gen);
     if (sig != b->m_sig) {
+        const uint32_t nch = (P + 31) / 32;   // k_ematch runs one CTA per (leaf, 32-pattern chunk)
         if (P > b->m_Pcap) {
+            const uint64_t Pc = 32ull * nch;
             afree(b->d_pat_ids, c->stream); afree(b->d_m_count, c->stream); afree(b->d_m_off, c->stream); afree(b->d_m_W, c->stream);
             b->d_pat_ids = nullptr; b->d_m_count = nullptr; b->d_m_off = nullptr; b->d_m_W = nullptr;
-            CK(c, cudaMallocAsync((void**)&b->d_pat_ids, 4ull * 32, c->stream));
-            CK(c, cudaMallocAsync((void**)&b->d_m_count, 4ull * 32 * (L ? L : 1), c->stream));
-            CK(c, cudaMallocAsync((void**)&b->d_m_off, 8ull * 32 * (L ? L : 1), c->stream));
-            CK(c, cudaMallocAsync((void**)&b->d_m_W, 4ull * 32, c->stream));
-            b->m_Pcap = 32;
+            CK(c, cudaMallocAsync((void**)&b->d_pat_ids, 4ull * Pc, c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_count, 4ull * Pc * (L ? L : 1), c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_off, 8ull * Pc * (L ? L : 1), c->stream));
+            CK(c, cudaMallocAsync((void**)&b->d_m_W, 4ull * Pc, c->stream));
+            b->m_Pcap = (uint32_t)Pc;
+        }
+        if (nch > b->raw_chunks) {   // [chunk][leaf][32][C] counts + work lists
+            afree(b->d_raw, c->stream);
+            b->d_raw = nullptr;
+            CK(c, cudaMallocAsync((void**)&b->d_raw, 8ull * (b->N + 1) * 32 * nch + 64, c->stream));
+            b->raw_chunks = nch;
         }
         b->m_W.resize(P);
         for (uint32_t i = 0; i < P; i++) {
@@ -791,7 +802,6 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
         }
         CK(c, cudaMemcpyAsync(b->d_pat_ids, pat_ids, 4ull * P, cudaMemcpyHostToDevice, c->stream));
         CK(c, cudaMemcpyAsync(b->d_m_W, b->m_W.data(), 4ull * P, cudaMemcpyHostToDevice, c->stream));
-        if (!b->d_raw) CK(c, cudaMallocAsync((void**)&b->d_raw, 8ull * (b->N + 1) * 32 + 64, c->stream));   // [leaf][32][C] counts + work list
         if (!b->stage_cap) {
             if ((r = regrow(c, &b->stage, &b->stage_cap, 4 * b->N + 4096))) return r;
             if ((r = regrow(c, &b->m_out, &b->m_cap, 4 * b->N + 4096))) return r;
@@ -810,8 +820,14 @@ int esat_ematch_masked(esat_batch* b, uint32_t P, const uint32_t* pat_ids, int m
         b->m_sized = false;
     }
     if (leaf_mask) {
-        if (!b->d_lmask) CK(c, cudaMallocAsync((void**)&b->d_lmask, 4ull * (L ? L : 1), c->stream));
-        CK(c, cudaMemcpyAsync(b->d_lmask, leaf_mask, 4ull * L, cudaMemcpyHostToDevice, c->stream));
+        const uint32_t nch = (P + 31) / 32;   // mask words per leaf, chunk-major
+        if (nch > b->lmask_chunks) {
+            afree(b->d_lmask, c->stream);
+            b->d_lmask = nullptr;
+            CK(c, cudaMallocAsync((void**)&b->d_lmask, 4ull * nch * (L ? L : 1), c->stream));
+            b->lmask_chunks = nch;
+        }
+        CK(c, cudaMemcpyAsync(b->d_lmask, leaf_mask, 4ull * nch * L, cudaMemcpyHostToDevice, c->stream));
     }
     b->lmask_on = leaf_mask != nullptr;
     b->m_P = P;

@@ -292,8 +292,10 @@ __device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
 #define ESAT_JOIN_MINB 1
 #endif
 template <int T>
-__global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a) {
-    // One CTA per leaf runs every pattern of the call. The leaf's clean view (class ids/offsets,
+__global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a0) {
+    // One CTA per (leaf, chunk of <= 32 call patterns): blockIdx.y selects the chunk, whose
+    // pattern ids, [pattern][leaf] count / offset rows, per-leaf mask words and scratch rows are
+    // this CTA's slices of the call's arrays. The leaf's clean view (class ids/offsets,
     // node symbols, child CSR) is staged into shared memory with TMA bulk copies when it fits,
     // so the backtracking matcher's dependent loads hit SMEM instead of L2.
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -303,12 +305,20 @@ __global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a) 
     __shared__ uint32_t sh_scan[33];
     __shared__ unsigned long long sh_base;
     __shared__ __align__(8) uint64_t bar;
-    constexpr uint32_t MAXP = 32;   // patterns per call (host-checked)
+    constexpr uint32_t MAXP = 32;   // patterns per CTA (a call of P patterns runs ceil(P/32) CTAs per leaf)
     __shared__ uint32_t sh_tot[MAXP];
     __shared__ unsigned long long sh_pbase[MAXP];
-    const uint32_t l = blockIdx.x, tid = threadIdx.x;
+    const uint32_t l = blockIdx.x, tid = threadIdx.x, cy = blockIdx.y;
     if (tid < MAXP) sh_tot[tid] = 0;
     const uint32_t L = d.L;
+    MArgs a = a0;
+    a.pat_ids += MAXP * cy;
+    a.P = min(MAXP, a0.P - MAXP * cy);
+    a.count += (uint64_t)MAXP * cy * L;
+    a.off += (uint64_t)MAXP * cy * L;
+    a.raw += a0.chunk_stride * cy;
+    a.nzl += a0.chunk_stride * cy;
+    if (a.leaf_mask) a.leaf_mask += (uint64_t)cy * L;
     const uint64_t b = d.nb[l];
     const uint32_t C = d.v_C[l];
     const uint32_t* g_cls_id = d.cls_id + b;

@@ -299,13 +299,16 @@ class DeviceBatch:
         self.ctx.check(self.L.esat_extract_async(self.h, C.c_int(METHODS[method])))
 
     def ematch(self, pattern_ids, mode: int = MATCH_LIST, leaf_mask=None):
-        """k_ematch of the call patterns over every leaf; ``leaf_mask[l]`` (bit p = call-pattern p)
-        restricts a leaf to the patterns it needs (esat_ematch_masked)."""
+        """k_ematch of the call patterns over every leaf; ``leaf_mask`` restricts a leaf to the
+        patterns it needs (esat_ematch_masked): shape [L] (bit p = call-pattern p, <= 32 patterns)
+        or [ceil(P/32), L] (bit p of row c = call-pattern 32c+p)."""
         ids = _u32(pattern_ids)
         if leaf_mask is None:
             self.ctx.check(self.L.esat_ematch(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode)))
         else:
-            m = _u32(leaf_mask)
+            m = _u32(leaf_mask).reshape(-1)
+            if m.size != ((len(ids) + 31) // 32) * self.n_leaves:
+                raise ValueError(f"leaf_mask needs ceil(P/32) x {self.n_leaves} words, got {m.size}")
             self.ctx.check(self.L.esat_ematch_masked(self.h, C.c_uint32(len(ids)), _p(ids), C.c_int(mode), _p(m)))
 
     def download_counts(self, n: int, from_join: bool = False) -> np.ndarray:

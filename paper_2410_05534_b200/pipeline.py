@@ -117,9 +117,14 @@ class LeafPipeline:
 
     def rule_masks(self, leaf_rule) -> np.ndarray:
         """Per-leaf pattern masks for applying rule ``leaf_rule[l]`` (0xFFFFFFFF: none): the bits of
-        that rule's source patterns."""
-        bits = [sum(1 << p for p in r.pattern_ids) for r in self.rules]
-        return np.array([0 if int(r) == 0xFFFFFFFF else bits[int(r)] for r in leaf_rule], np.uint32)
+        that rule's source patterns, one 32-pattern chunk per row ([ceil(P/32), L], esat_ematch_masked)."""
+        nch = max(1, (len(self.pattern_ids) + 31) // 32)
+        bits = np.zeros((len(self.rules) + 1, nch), np.uint32)   # last row: no rule
+        for i, r in enumerate(self.rules):
+            for p in r.pattern_ids:
+                bits[i, p // 32] |= np.uint32(1 << (p % 32))
+        sel = np.array([len(self.rules) if int(r) == 0xFFFFFFFF else int(r) for r in leaf_rule], np.int64)
+        return np.ascontiguousarray(bits[sel].T)
 
     def exists(self) -> np.ndarray:
         """is_rule_applicable of every rule on every leaf (rewrite.py:579-589): one EXISTS-mode

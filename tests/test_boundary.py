@@ -88,3 +88,22 @@ def test_cost_model_spec_kats():
     assert operator_cost(CostModelConfig(mode="unit"), "conv2d", (1, 1, "none"), (1, 8, 16, 16),
                          ((1, 8, 16, 16), (8, 8, 3, 3))) == 1.0
     assert operator_cost(CostModelConfig(mode="unit"), "input", ("x",), (1, 8), ()) == 0.0
+
+
+def test_rule_masks_chunk_layout():
+    """LeafPipeline.rule_masks: one 32-pattern chunk per row (esat_ematch_masked's chunk-major
+    [ceil(P/32), L] words), so rules whose sources sit beyond pattern 31 mask the right bits."""
+    from types import SimpleNamespace
+
+    from paper_2410_05534_b200.pipeline import LeafPipeline
+
+    pipe = LeafPipeline.__new__(LeafPipeline)
+    pipe.pattern_ids = list(range(70))
+    pipe.rules = [SimpleNamespace(pattern_ids=[0, 5]), SimpleNamespace(pattern_ids=[33]),
+                  SimpleNamespace(pattern_ids=[31, 64, 69])]
+    m = pipe.rule_masks(np.array([2, 0xFFFFFFFF, 1, 0], np.uint32))
+    assert m.shape == (3, 4) and m.dtype == np.uint32 and m.flags["C_CONTIGUOUS"]
+    assert m[:, 0].tolist() == [1 << 31, 0, (1 << 0) | (1 << 5)]
+    assert m[:, 1].tolist() == [0, 0, 0]
+    assert m[:, 2].tolist() == [0, 1 << 1, 0]
+    assert m[:, 3].tolist() == [(1 << 0) | (1 << 5), 0, 0]
