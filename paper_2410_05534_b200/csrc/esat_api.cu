@@ -298,7 +298,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     b->ub.assign(ub, ub + L + 1);
     b->tb.assign(L + 1, 0);
     for (uint32_t l = 0; l < L; l++) {
-        uint64_t n = nb[l + 1] - nb[l], t = 2;
+        uint64_t n = nb[l + 1] - nb[l], t = 4;   // >= 4 slots: every table 16-B aligned (k_apply clears by uint4)
         while (t < 2 * n) t <<= 1;
         b->tb[l + 1] = b->tb[l] + t;
     }

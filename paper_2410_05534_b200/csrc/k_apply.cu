@@ -789,7 +789,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? 16 : 1) k_apply(Dev d, AArg
         L.head[x] = NONE;
         L.seen[x] = 0;
     }
-    for (uint32_t s = lane; s <= L.tmask; s += 32) L.tab[s] = NONE;
+    {   // tables are >= 4 slots and 16-B aligned (esat_batch_create): clear 4 slots per store
+        uint4* t4 = reinterpret_cast<uint4*>(L.tab);
+        const uint4 none4 = make_uint4(NONE, NONE, NONE, NONE);
+        for (uint32_t s = lane; s < (L.tmask + 1) / 4; s += 32) t4[s] = none4;
+    }
     __syncwarp();
     for (uint32_t e = lane; e < L.n; e += 32) {
         const uint32_t c = L.cid[e];   // rebuilt classes are union-find roots
