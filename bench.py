@@ -366,9 +366,12 @@ def measure_config(ctx, stream, dev, model, B, steps, warmup, world, rank, e2e_s
     pipe = LeafPipeline(ctx, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=ocf_pool)
     packed, src_idx = make_batch(leaves, B, rotate=rank * B)  # contiguous shard of the global leaf sequence
     batch = pipe.load(packed)
+    ctx.reset_extract_lanes()    # a new leaf set: k_extract's lane groups are re-tuned on it
     for _ in range(max(warmup, 3)):
         pipe.step()
     torch.cuda.synchronize()
+    ext = batch.download_extract()   # tunes the lane-group width (native.Context.tune_extract_lanes)
+    pipe.step()                      # the parity-checked step runs with the tuned width
     ext = batch.download_extract()
     while pipe.grow_pool(ext):   # size the OCF history pools once, outside timing
         pipe.step()
@@ -502,6 +505,7 @@ def measure_config(ctx, stream, dev, model, B, steps, warmup, world, rank, e2e_s
             "roofline_frac": {k: abytes[k] / (kernel_ms[k] / 1e3) / 1e9 / peak for k in abytes},
             "algorithmic_bytes": abytes,
             "parity_vs_reference": parity_ok,
+            "extract_lanes": ctx.extract_lanes, "extract_level_width": ctx.extract_width,
             "parity_detail": {"status_nonzero": int(np.sum(ext["status"] != 0)),
                               "cost_mismatch": int(np.sum(ext["root_cost"].view(np.uint64) != exp.view(np.uint64))),
                               "ocf_pool_entries_per_node": pipe.pool, "ocf_pool_bitsets_per_node": pipe.pool_bitsets},
@@ -675,7 +679,9 @@ def main():
                                    "traffic": trd.get(args.model, {}).get(k)
                                    if isinstance(trd.get(args.model), dict) else None}
                                for k in abytes},
+        "extract_lanes": head["extract_lanes"], "extract_level_width": head["extract_level_width"],
         "per_config": {m: {k: r[k] for k in ("value", "ms_per_step", "e2e", "kernel_ms", "roofline_frac",
+                                              "extract_lanes", "extract_level_width",
                                               "matches_per_s", "ematch_matches_per_s", "nodes_per_leaf_mean",
                                               "leaves_per_rank", "parity_vs_reference")}
                        for m, r in per_config.items()},

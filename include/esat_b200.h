@@ -109,7 +109,7 @@ int esat_batch_upload(esat_batch* b, const uint32_t* hc_sym, const uint32_t* hc_
 int esat_rebuild(esat_batch* b);
 
 /* e-match patterns[0..n) over every leaf (mode LIST or EXISTS); n <= ESAT_MAX_CALL_PATTERNS
- * (one CTA per leaf and 32-pattern chunk) */
+ * (one k_ematch launch per 32-pattern chunk) */
 #define ESAT_MAX_CALL_PATTERNS 1024u
 int esat_ematch(esat_batch* b, uint32_t n_patterns, const uint32_t* pattern_ids, int mode);
 /* the same, with per-leaf pattern masks: ceil(n/32) words per leaf, chunk-major -- bit p of
@@ -155,6 +155,13 @@ int esat_download_matches(esat_batch* b, int from_join, uint32_t index, uint32_t
 int esat_download_counts(esat_batch* b, int from_join, uint32_t* counts);
 int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, double* root_cost,
                           double* class_cost, uint32_t* choice, uint8_t* reachable, uint32_t* passes);
+/* shape of the last extraction: total e-classes and total Gauss-Seidel levels over the batch's
+ * leaves (mean level width = classes / levels; the host picks the lane-group width from it) */
+int esat_extract_shape(esat_batch* b, uint64_t* classes, uint64_t* levels);
+/* k_extract lanes per leaf in one-warp CTAs for every later extraction on this context: 32 (one
+ * leaf per warp), 16 or 8 (two / four leaves share a warp: narrow levels); 0 = 32. Results are
+ * identical for every width. */
+int esat_set_extract_lanes(esat_ctx* ctx, uint32_t lanes);
 
 /* run all work of this context on a caller-owned CUDA stream (e.g. torch's current stream) */
 int esat_ctx_set_stream(esat_ctx* ctx, void* cuda_stream);

@@ -10,7 +10,7 @@
 
 namespace esat {
 template <int T> __global__ void k_rebuild(Dev);
-template <int T> __global__ void k_extract(Dev, XArgs);
+template <int T, int G> __global__ void k_extract(Dev, XArgs);
 __global__ void k_extract_order(Dev, uint32_t*);
 }  // namespace esat
 #include "k_ematch_args.cuh"
@@ -32,6 +32,7 @@ struct esat_ctx {
     bool timed = false;
     // max-dynamic-SMEM attributes are per device: tracked per context (one context per device)
     uint32_t ematch_attr = 0;
+    uint32_t extract_lanes = 32;   // k_extract lanes per leaf in one-warp CTAs (esat_set_extract_lanes)
     bool join_attr = false;
     char err[512] = {0};
     // symbol table
@@ -333,7 +334,7 @@ int esat_batch_create(esat_ctx* c, uint32_t L, const uint64_t* nb, const uint64_
     OWN(d.s_tc, T); OWN(d.s_ts, T);
     // extraction buffers
     XArgs& x = b->x;
-    OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.root_cost, L);
+    OWN(x.status, L); OWN(x.err_class, L); OWN(x.passes, L); OWN(x.levels, L); OWN(x.root_cost, L);
     OWN(x.class_cost, N); OWN(x.prev, N); OWN(x.choice, N); OWN(x.level, N); OWN(x.order, N); OWN(x.lvcnt, NL);
     OWN(x.stk, N); OWN(x.stki, N); OWN(x.reach, N);
     OWN(x.hoff, 2 * N); OWN(x.hrng, 2 * N); OWN(x.chg, 2 * N); OWN(x.lhn, N); OWN(x.lcc, 2 * N);
@@ -494,10 +495,16 @@ static int launch_extract(esat_batch* b, int method, cudaStream_t s) {
         k_extract_order<<<1, 1024, 0, s>>>(b->d, b->x_order);
         x.lorder = b->x_order;
     }
+    // lanes per leaf in the one-warp CTAs (32: one leaf per warp; 16 / 8: two / four leaves share a
+    // warp); ESAT_EXTRACT_LANES overrides the context's setting
+    static const int xg_force = getenv("ESAT_EXTRACT_LANES") ? atoi(getenv("ESAT_EXTRACT_LANES")) : 0;
+    const int xg_env = xg_force ? xg_force : (int)c->extract_lanes;
     if (b->L) {
-        if (xt == 128) k_extract<128><<<b->L, 128, 0, s>>>(b->d, x);
-        else if (xt == 64) k_extract<64><<<b->L, 64, 0, s>>>(b->d, x);
-        else k_extract<32><<<b->L, 32, 0, s>>>(b->d, x);
+        if (xt == 128) k_extract<128, 128><<<b->L, 128, 0, s>>>(b->d, x);
+        else if (xt == 64) k_extract<64, 64><<<b->L, 64, 0, s>>>(b->d, x);
+        else if (xg_env == 16) k_extract<32, 16><<<(unsigned)((b->L + 1) / 2), 32, 0, s>>>(b->d, x);
+        else if (xg_env == 8) k_extract<32, 8><<<(unsigned)((b->L + 3) / 4), 32, 0, s>>>(b->d, x);
+        else k_extract<32, 32><<<b->L, 32, 0, s>>>(b->d, x);
     }
     return launch_check(c, "k_extract");
 }
@@ -617,6 +624,30 @@ int esat_download_extract(esat_batch* b, uint32_t* status, uint32_t* err_class, 
     return ESAT_OK;
 }
 
+int esat_extract_shape(esat_batch* b, uint64_t* classes, uint64_t* levels) {
+    if (!b || !classes || !levels) return ESAT_E_ARG;
+    esat_ctx* c = b->ctx;
+    esat_wait_async(c);
+    cudaSetDevice(c->device);
+    std::vector<uint32_t> C(b->L), lv(b->L);
+    if (b->L) {
+        CK(c, cudaMemcpyAsync(C.data(), b->d.v_C, 4 * b->L, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaMemcpyAsync(lv.data(), b->x.levels, 4 * b->L, cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
+    uint64_t sc = 0, sl = 0;
+    for (uint64_t l = 0; l < b->L; l++) { sc += C[l]; sl += lv[l]; }
+    *classes = sc;
+    *levels = sl;
+    return ESAT_OK;
+}
+
+int esat_set_extract_lanes(esat_ctx* c, uint32_t lanes) {
+    if (!c || (lanes != 0 && lanes != 8 && lanes != 16 && lanes != 32)) return ESAT_E_ARG;
+    c->extract_lanes = lanes ? lanes : 32;
+    return ESAT_OK;
+}
+
 int esat_ctx_set_stream(esat_ctx* c, void* stream) {
     if (!c) return ESAT_E_ARG;
     if (c->own_stream && c->stream) {
@@ -686,7 +717,6 @@ static int ematch_launch(esat_batch* b) {
     MArgs a{};
     a.prog = c->d_pat; a.prog_off = c->d_pat_off; a.pat_ids = b->d_pat_ids; a.P = P; a.mode = b->m_mode;
     a.stage = b->stage; a.stage_cap = b->stage_cap; a.tops = b->d_tops; a.raw = b->d_raw; a.nzl = b->d_raw + 32ull * (b->N + 1);
-    a.chunk_stride = 64ull * (b->N + 1);
     a.out = b->m_out; a.out_cap = b->m_cap; a.count = b->d_m_count; a.off = b->d_m_off; a.overflow = b->d_over;
     Dev d = b->d;
     d.sym_name = c->sym_name; d.sym_arity = c->sym_arity; d.sym_rank = c->sym_rank; d.sym_poff = c->sym_poff;
@@ -700,7 +730,19 @@ static int ematch_launch(esat_batch* b) {
         c->ematch_attr = cap_bytes;
     }
     tic(c);
-    if (L && P) k_ematch<128><<<dim3((unsigned)L, (P + 31) / 32), 128, a.smem_bytes, c->stream>>>(d, a);
+    // one launch per 32-pattern chunk: the chunk's slices of the call's ids, rows, masks and scratch
+    for (uint32_t p0 = 0; L && p0 < P; p0 += 32) {
+        const uint32_t ch = p0 / 32;
+        MArgs ac = a;
+        ac.pat_ids = a.pat_ids + p0;
+        ac.P = P - p0 < 32 ? P - p0 : 32;
+        ac.count = a.count + (uint64_t)p0 * L;
+        ac.off = a.off + (uint64_t)p0 * L;
+        ac.raw = a.raw + 64ull * (b->N + 1) * ch;
+        ac.nzl = a.nzl + 64ull * (b->N + 1) * ch;
+        if (a.leaf_mask) ac.leaf_mask = a.leaf_mask + (uint64_t)ch * L;
+        k_ematch<128><<<(unsigned)L, 128, a.smem_bytes, c->stream>>>(d, ac);
+    }
     toc(c);
     if ((r = launch_check(c, "k_ematch"))) return r;
     return ESAT_OK;

@@ -52,6 +52,7 @@ struct Dev {
 struct XArgs {
     int method;                 // 0 default, 1 OCF
     uint32_t *status, *err_class, *passes;
+    uint32_t* levels;           // [L] Gauss-Seidel levels of each leaf (lane-group choice, esat_extract_shape)
     double *root_cost, *class_cost, *prev;
     uint32_t *choice, *level, *order, *lvcnt, *stk, *stki;
     uint8_t *reach;

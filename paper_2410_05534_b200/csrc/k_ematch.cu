@@ -285,17 +285,23 @@ __device__ uint32_t sort_unique(uint32_t* base, uint32_t n, uint32_t W) {
 
 }  // namespace
 
-#ifndef ESAT_EMATCH_MINB
-#define ESAT_EMATCH_MINB 1
+// optional minimum-CTAs-per-SM bounds for occupancy experiments (an explicit 1 is NOT the default:
+// it lets ptxas take 120 registers for k_ematch instead of 80)
+#ifdef ESAT_EMATCH_MINB
+#define ESAT_EMATCH_LB(T) __launch_bounds__(T, ESAT_EMATCH_MINB)
+#else
+#define ESAT_EMATCH_LB(T) __launch_bounds__(T)
 #endif
-#ifndef ESAT_JOIN_MINB
-#define ESAT_JOIN_MINB 1
+#ifdef ESAT_JOIN_MINB
+#define ESAT_JOIN_LB(T) __launch_bounds__(T, ESAT_JOIN_MINB)
+#else
+#define ESAT_JOIN_LB(T) __launch_bounds__(T)
 #endif
 template <int T>
-__global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a0) {
-    // One CTA per (leaf, chunk of <= 32 call patterns): blockIdx.y selects the chunk, whose
-    // pattern ids, [pattern][leaf] count / offset rows, per-leaf mask words and scratch rows are
-    // this CTA's slices of the call's arrays. The leaf's clean view (class ids/offsets,
+__global__ void ESAT_EMATCH_LB(T) k_ematch(Dev d, MArgs a) {
+    // One CTA per leaf runs every pattern of a chunk of <= 32 call patterns (a call with more runs
+    // one launch per chunk; the host passes the chunk's slices of the pattern ids, [pattern][leaf]
+    // count / offset rows, per-leaf mask words and scratch). The leaf's clean view (class ids/offsets,
     // node symbols, child CSR) is staged into shared memory with TMA bulk copies when it fits,
     // so the backtracking matcher's dependent loads hit SMEM instead of L2.
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -305,20 +311,12 @@ __global__ void __launch_bounds__(T, ESAT_EMATCH_MINB) k_ematch(Dev d, MArgs a0)
     __shared__ uint32_t sh_scan[33];
     __shared__ unsigned long long sh_base;
     __shared__ __align__(8) uint64_t bar;
-    constexpr uint32_t MAXP = 32;   // patterns per CTA (a call of P patterns runs ceil(P/32) CTAs per leaf)
+    constexpr uint32_t MAXP = 32;   // patterns per launch (a call of P patterns runs ceil(P/32) launches)
     __shared__ uint32_t sh_tot[MAXP];
     __shared__ unsigned long long sh_pbase[MAXP];
-    const uint32_t l = blockIdx.x, tid = threadIdx.x, cy = blockIdx.y;
+    const uint32_t l = blockIdx.x, tid = threadIdx.x;
     if (tid < MAXP) sh_tot[tid] = 0;
     const uint32_t L = d.L;
-    MArgs a = a0;
-    a.pat_ids += MAXP * cy;
-    a.P = min(MAXP, a0.P - MAXP * cy);
-    a.count += (uint64_t)MAXP * cy * L;
-    a.off += (uint64_t)MAXP * cy * L;
-    a.raw += a0.chunk_stride * cy;
-    a.nzl += a0.chunk_stride * cy;
-    if (a.leaf_mask) a.leaf_mask += (uint64_t)cy * L;
     const uint64_t b = d.nb[l];
     const uint32_t C = d.v_C[l];
     const uint32_t* g_cls_id = d.cls_id + b;
@@ -1073,7 +1071,7 @@ __global__ void __launch_bounds__(T) k_join_big(uint32_t L, JArgs a) {
 }
 
 template <int T>
-__global__ void __launch_bounds__(T, ESAT_JOIN_MINB) k_join(uint32_t L, JArgs a) {
+__global__ void ESAT_JOIN_LB(T) k_join(uint32_t L, JArgs a) {
     const uint32_t l = blockIdx.x, r = blockIdx.y, tid = threadIdx.x;
     __shared__ uint32_t sh_scan[33];
     __shared__ unsigned long long sh_base;

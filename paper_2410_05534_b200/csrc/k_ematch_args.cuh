@@ -20,15 +20,14 @@ struct MArgs {
     unsigned long long* tops;   // [0] stage top, [1] out top (words)
     uint32_t* out;
     uint64_t out_cap;
-    uint32_t* count;            // [P][L] (P = every pattern of the call)
+    uint32_t* count;            // [P][L] (this launch's chunk of the call's rows)
     uint64_t* off;              // [P][L] word offsets into out
     uint32_t* overflow;
     uint32_t smem_bytes;        // dynamic shared memory for staging one leaf's view
     uint32_t* raw;              // [L][32][T] per-thread raw match counts (count -> fill placement)
     uint32_t* nzl;              // [L][32][C] (pattern, class) pairs with matches (pass-2 work list)
     int no_flat;                // 1: always use the generic backtracking matcher
-    const uint32_t* leaf_mask;  // [ceil(P/32)][L] bit p of word [c][l]: match call-pattern 32c+p on leaf l (nullptr: all)
-    uint64_t chunk_stride;      // words between the raw / nzl scratch of consecutive pattern chunks
+    const uint32_t* leaf_mask;  // [L] bit p: match chunk-pattern p on this leaf (nullptr: all)
 };
 
 struct JArgs {

@@ -304,9 +304,47 @@ __device__ double ocf_generic(const LeafCtx& c, uint32_t nd, uint32_t* topk, uin
 
 }  // namespace
 
-template <int T>
-__global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // <= 64 regs: 32 resident leaves per SM
-    const uint32_t l = x.lorder ? x.lorder[blockIdx.x] : blockIdx.x, tid = threadIdx.x;
+// Barrier of one leaf's threads: the CTA when it holds one leaf, else the lane group.
+template <int G, int T>
+__device__ __forceinline__ void gbar(uint32_t gmask) {
+    if (G == T) __syncthreads();
+    else __syncwarp(gmask);
+}
+
+// Exclusive scan over one leaf's threads (G == T: block_exscan; G < 32: shuffles inside the group).
+template <int G>
+__device__ __forceinline__ uint32_t group_exscan(uint32_t v, uint32_t* smem, uint32_t* total, uint32_t gmask) {
+    if (G >= 32) return block_exscan(v, smem, total);
+    const uint32_t gl = threadIdx.x % G;
+    uint32_t xs = v;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(gmask, xs, o, G);
+        if (gl >= (uint32_t)o) xs += y;
+    }
+    *total = __shfl_sync(gmask, xs, G - 1, G);
+    return xs - v;
+}
+
+#ifndef ESAT_XG_MINB
+#define ESAT_XG_MINB 24
+#endif
+// G == T: <= 64 registers, 32 resident leaves (warps) per SM. G < 32: the lane groups need more
+// registers (<= 80 at 24 CTAs per SM: 48 or 96 resident leaves).
+template <int T, int G>
+__global__ void __launch_bounds__(T, G == T ? 1024 / T : ESAT_XG_MINB) k_extract(Dev d, XArgs x) {
+    // G lanes per leaf: G == T is one leaf per CTA (T = 32, 64, 128); G < 32 packs 32/G leaves into
+    // one single-warp CTA, each lane group running its leaf independently (its own barriers via
+    // __syncwarp(gmask), its own shared flags): the narrow Gauss-Seidel levels of small leaves leave
+    // most of a warp idle, so two or four leaves share one warp's issue slots.
+    static_assert(G == T || (T == 32 && G < 32 && (32 % G) == 0), "lane groups only inside one warp");
+    constexpr uint32_t LPW = T / G;                 // leaves per CTA
+    const uint32_t g = G == T ? 0u : threadIdx.x / G;
+    const uint32_t tid = G == T ? threadIdx.x : threadIdx.x % G;   // lane within the leaf's group
+    const uint32_t gmask = G >= 32 ? 0xffffffffu : (((1u << G) - 1u) << (g * G));
+    const uint32_t li = blockIdx.x * LPW + g;
+    if (li >= d.L) return;                         // whole group exits together (no CTA-wide barrier below)
+    const uint32_t l = x.lorder ? x.lorder[li] : li;
     const uint64_t b = d.nb[l], k0 = d.kb[l];
     const uint32_t C = d.v_C[l];
     const uint32_t* coff = d.cls_off + b + l;
@@ -347,13 +385,15 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     }
 
     __shared__ uint32_t sh_scan[33];
-    __shared__ uint32_t sh_flag, sh_maxlv, sh_topk, sh_topv, sh_over;
+    __shared__ uint32_t sh_grp[LPW][8];   // per leaf: flag, max level, bitset top, value top, overflow
+    uint32_t* const gv = sh_grp[g];       // one base register; the five scalars are constant offsets
+    uint32_t &sh_flag = gv[0], &sh_maxlv = gv[1], &sh_topk = gv[2], &sh_topv = gv[3], &sh_over = gv[4];
 #ifdef ESAT_DEBUG
     __shared__ unsigned dbg[2][8];   // per pass: evaluated classes, their nodes, merges, flush reuses, unchanged
     if (tid < 16) dbg[tid / 8][tid % 8] = 0;
 #endif
 
-    for (uint32_t k = tid; k < C; k += T) {
+    for (uint32_t k = tid; k < C; k += G) {
         cost[k] = __longlong_as_double(0x7ff0000000000000ll);
         prev[k] = cost[k];
         ch[k] = NONE;
@@ -365,15 +405,16 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     long long t_start = clock64(), t_lv = 0, t_sort = 0;
     long long t_pass[8] = {0};
 #endif
-    __syncthreads();
+    gbar<G, T>(gmask);
     // ---- K7: wavefront levels over lower-position children ----
     // level[k] = 1 + max level of k's lower-position children. Warp 0 walks the classes in
     // position order 32 at a time: children below the chunk are final (read from memory); a child
     // inside the chunk is always at a lower lane, so one in-register sweep over the lanes in order
     // (shuffle-broadcast of each lane's finished level) resolves every in-chunk chain exactly.
-    if (tid < 32) {
+    constexpr uint32_t CW = G < 32 ? G : 32;       // chunk width of the two in-register sweeps
+    if (tid < CW) {
         uint32_t mx = 0;
-        for (uint32_t kb0 = 0; kb0 < C; kb0 += 32) {
+        for (uint32_t kb0 = 0; kb0 < C; kb0 += CW) {
             const uint32_t k = kb0 + tid;
             uint32_t lv = 0, dep = 0;   // dep: in-chunk children as a lane mask
             if (k < C)
@@ -384,38 +425,38 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                         else if (j < k) dep |= 1u << (j - kb0);
                     }
 #pragma unroll 4
-            for (uint32_t i = 0; i < 31; i++) {
-                const uint32_t li = __shfl_sync(0xffffffffu, lv, i);
-                if ((dep >> i) & 1u) lv = li + 1 > lv ? li + 1 : lv;
+            for (uint32_t i = 0; i < CW - 1; i++) {
+                const uint32_t lvi = __shfl_sync(gmask, lv, i, CW);
+                if ((dep >> i) & 1u) lv = lvi + 1 > lv ? lvi + 1 : lv;
             }
             if (k < C) level[k] = lv;
-            mx = max(mx, __reduce_max_sync(0xffffffffu, k < C ? lv : 0u));
-            __syncwarp();
+            mx = max(mx, __reduce_max_sync(gmask, k < C ? lv : 0u));
+            __syncwarp(gmask);
         }
         if (tid == 0) sh_maxlv = mx;
     }
-    __syncthreads();
+    gbar<G, T>(gmask);
 #ifdef ESAT_DEBUG
     t_lv = clock64();
 #endif
     // counting sort of classes by level
-    for (uint32_t k = tid; k <= C; k += T) lvcnt[k] = 0;
-    __syncthreads();
-    for (uint32_t k = tid; k < C; k += T) atomicAdd(&lvcnt[level[k]], 1u);
-    __syncthreads();
+    for (uint32_t k = tid; k <= C; k += G) lvcnt[k] = 0;
+    gbar<G, T>(gmask);
+    for (uint32_t k = tid; k < C; k += G) atomicAdd(&lvcnt[level[k]], 1u);
+    gbar<G, T>(gmask);
     const uint32_t nlv = C ? sh_maxlv + 1 : 0;
     uint32_t base = 0;
-    for (uint32_t c0 = 0; c0 <= nlv; c0 += T) {
+    for (uint32_t c0 = 0; c0 <= nlv; c0 += G) {
         const uint32_t i = c0 + tid;
         const uint32_t v = i < nlv ? lvcnt[i] : 0u;
         uint32_t tot;
-        const uint32_t p = block_exscan(v, sh_scan, &tot);
+        const uint32_t p = group_exscan<G>(v, sh_scan, &tot, gmask);
         if (i <= nlv) lvcnt[i] = base + p;   // exclusive offsets; lvcnt[nlv] = C
         base += tot;
     }
-    __syncthreads();
-    for (uint32_t k = tid; k < C; k += T) order[atomicAdd(&lvcnt[level[k]], 1u)] = k;
-    __syncthreads();
+    gbar<G, T>(gmask);
+    for (uint32_t k = tid; k < C; k += G) order[atomicAdd(&lvcnt[level[k]], 1u)] = k;
+    gbar<G, T>(gmask);
     // lvcnt[lv] now holds the END of level lv; level lv spans [lv ? lvcnt[lv-1] : 0, lvcnt[lv])
 
 #ifdef ESAT_DEBUG
@@ -428,15 +469,15 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     for (uint64_t it = 0; it < cap; it++) {
         const int pass = (int)it;
         c.pass = pass;
-        for (uint32_t k = tid; k < C; k += T) prev[k] = cost[k];
+        for (uint32_t k = tid; k < C; k += G) prev[k] = cost[k];
         if (tid == 0) sh_flag = 0;
-        __syncthreads();
+        gbar<G, T>(gmask);
         const int par = pass & 1, ppar = par ^ 1;
         uint8_t* chg_cur = x.chg + par * x.slot_stride + b;
         const uint8_t* chg_prv = x.chg + ppar * x.slot_stride + b;
         for (uint32_t lv = 0; lv < nlv; lv++) {
             const uint32_t lo = lv ? lvcnt[lv - 1] : 0u, hi = lvcnt[lv];
-            for (uint32_t idx = lo + tid; idx < hi; idx += T) {
+            for (uint32_t idx = lo + tid; idx < hi; idx += G) {
                 const uint32_t k = order[idx];
                 c.k = k;
                 // Dirty skip (exact): the class's inputs are its children's (cost, history) as read
@@ -574,14 +615,14 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 if (pass < 2 && !hchg && !changed) atomicAdd(&dbg[pass][4], 1u);
 #endif
             }
-            __syncthreads();
+            gbar<G, T>(gmask);
         }
         passes++;
 #ifdef ESAT_DEBUG
         if (passes <= 8) t_pass[passes - 1] = clock64();
 #endif
         const bool any_change = sh_flag != 0;
-        __syncthreads();   // everyone has read the flag before thread 0 resets it for the next pass
+        gbar<G, T>(gmask);   // everyone has read the flag before thread 0 resets it for the next pass
         if (!any_change) { st = X_OK; break; }
     }
     if (sh_over) st = X_CAPACITY;
@@ -598,11 +639,11 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
     if (st == X_OK && !(cost[root] < __longlong_as_double(0x7ff0000000000000ll))) st = X_INFEASIBLE;
     uint8_t* state = x.reach + b;   // 0 unvisited, 1 on stack, 2 done
     bool fast = false;
-    if (st == X_OK && tid < 32) {
+    if (st == X_OK && tid < CW) {
         if (tid == 0) state[root] = 2;
-        __syncwarp();
+        __syncwarp(gmask);
         bool bad = false;
-        for (int kb0 = (int)((C - 1) & ~31u); kb0 >= 0; kb0 -= 32) {
+        for (int kb0 = (int)((C - 1) & ~(CW - 1)); kb0 >= 0; kb0 -= CW) {
             const uint32_t k = (uint32_t)kb0 + tid;
             uint32_t r = k < C ? state[k] : 0u, cmask = 0;
             bool up = false;
@@ -616,8 +657,8 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 if (j >= k) up = true;
                 else if (j >= (uint32_t)kb0) cmask |= 1u << (j - kb0);
             }
-            for (int i = 31; i >= 0; i--) {
-                const uint32_t ri = __shfl_sync(0xffffffffu, r, i), mi = __shfl_sync(0xffffffffu, cmask, i);
+            for (int i = CW - 1; i >= 0; i--) {
+                const uint32_t ri = __shfl_sync(gmask, r, i, CW), mi = __shfl_sync(gmask, cmask, i, CW);
                 if (ri && ((mi >> tid) & 1u)) r = 2;
             }
             if (r) {
@@ -629,12 +670,12 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
                 }
                 state[k] = 2;
             }
-            __syncwarp();
+            __syncwarp(gmask);
         }
-        fast = !__any_sync(0xffffffffu, bad);
+        fast = !__any_sync(gmask, bad);
         if (!fast) {
-            for (uint32_t k = tid; k < C; k += 32) state[k] = 0;
-            __syncwarp();
+            for (uint32_t k = tid; k < C; k += CW) state[k] = 0;
+            __syncwarp(gmask);
         }
     }
     if (tid == 0) {
@@ -672,12 +713,13 @@ __global__ void __launch_bounds__(T, 1024 / T) k_extract(Dev d, XArgs x) {   // 
         x.err_class[l] = err;
         x.root_cost[l] = rc;
         x.passes[l] = passes;
+        x.levels[l] = nlv;
         sh_flag = st;
     }
-    __syncthreads();
+    gbar<G, T>(gmask);
     if (sh_flag == X_OK) {   // DFS states (2 = visited) -> reachable flags
         uint8_t* state = x.reach + b;
-        for (uint32_t k = tid; k < C; k += T) state[k] = state[k] == 2 ? 1 : 0;
+        for (uint32_t k = tid; k < C; k += G) state[k] = state[k] == 2 ? 1 : 0;
     }
 }
 
@@ -704,8 +746,10 @@ __global__ void k_extract_order(Dev d, uint32_t* order) {
         order[atomicAdd(&hist[255 - min(d.v_C[l] >> 3, 255u)], 1u)] = l;
 }
 
-template __global__ void k_extract<32>(Dev, XArgs);
-template __global__ void k_extract<64>(Dev, XArgs);
-template __global__ void k_extract<128>(Dev, XArgs);
+template __global__ void k_extract<32, 32>(Dev, XArgs);
+template __global__ void k_extract<32, 16>(Dev, XArgs);
+template __global__ void k_extract<32, 8>(Dev, XArgs);
+template __global__ void k_extract<64, 64>(Dev, XArgs);
+template __global__ void k_extract<128, 128>(Dev, XArgs);
 
 }  // namespace esat

@@ -70,7 +70,8 @@ def lib():
                      "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
                      "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts",
                      "esat_store_create", "esat_store_destroy", "esat_store_truncate", "esat_store_save",
-                     "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots"):
+                     "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots",
+                     "esat_extract_shape", "esat_set_extract_lanes"):
             getattr(L, name).restype = C.c_int
         u32 = C.c_uint32
         L.esat_store_size.restype = u32
@@ -85,6 +86,8 @@ def lib():
                                        C.c_uint32, vp, C.c_uint32, vp, vp]
         L.esat_batch_set_pool.argtypes = [vp, C.c_double]
         L.esat_batch_set_pool2.argtypes = [vp, C.c_double, C.c_double]
+        L.esat_extract_shape.argtypes = [vp, vp, vp]
+        L.esat_set_extract_lanes.argtypes = [vp, u32]
         _lib = L
     return _lib
 
@@ -99,7 +102,13 @@ EXPORTED = ("esat_ctx_create", "esat_ctx_destroy", "esat_last_error", "esat_ctx_
             "esat_download_apply", "esat_download_state", "esat_fingerprint_setup", "esat_fingerprint",
             "esat_download_fingerprint", "esat_ematch_masked", "esat_download_counts",
             "esat_store_create", "esat_store_destroy", "esat_store_size", "esat_store_truncate", "esat_store_save",
-            "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots")
+            "esat_store_put", "esat_store_info", "esat_store_download", "esat_batch_load_slots",
+            "esat_extract_shape", "esat_set_extract_lanes")
+
+# k_extract lane groups: leaves whose Gauss-Seidel levels average at most this many classes run two
+# to a warp (16 lanes each); wider levels keep a warp per leaf (bench.py `extract_shape`)
+LANES16_MAX_WIDTH = 6.0
+TUNE_MIN_LEAVES = 1024
 
 A_OK, A_NODE_LIMIT, A_NEED_SYMBOL, A_CAPACITY, A_PROGRAM = range(5)
 
@@ -124,6 +133,8 @@ class Context:
         self.device = device
         self.symtab_version = None
         self._children = weakref.WeakSet()   # batches / stores: released before the context
+        self.extract_lanes = None            # k_extract lanes per leaf: None until tuned (then 32 / 16)
+        self.extract_width = None            # mean level width it was tuned on
 
     def check(self, rc: int):
         if rc != OK:
@@ -144,6 +155,27 @@ class Context:
 
     def sync(self):
         self.check(self.L.esat_ctx_sync(self.h))
+
+    def set_extract_lanes(self, lanes: int):
+        """k_extract lanes per leaf for later extractions (32, 16 or 8; results are identical)."""
+        self.check(self.L.esat_set_extract_lanes(self.h, C.c_uint32(lanes)))
+        self.extract_lanes = lanes
+
+    def reset_extract_lanes(self):
+        """Forget the tuned width (a new workload): one leaf per warp until the next tuning."""
+        self.check(self.L.esat_set_extract_lanes(self.h, C.c_uint32(32)))
+        self.extract_lanes = None
+        self.extract_width = None
+
+    def tune_extract_lanes(self, batch) -> int | None:
+        """Once per context, after an extraction of a batch of >= TUNE_MIN_LEAVES leaves: two leaves
+        share a warp when the mean Gauss-Seidel level width is at most LANES16_MAX_WIDTH classes."""
+        if self.extract_lanes is not None or batch.n_leaves < TUNE_MIN_LEAVES:
+            return self.extract_lanes
+        classes, levels = batch.extract_shape()
+        self.extract_width = classes / max(levels, 1)
+        self.set_extract_lanes(16 if self.extract_width <= LANES16_MAX_WIDTH else 32)
+        return self.extract_lanes
 
     def set_stream(self, cuda_stream_handle: int):
         """Issue all work on a caller-owned stream (torch.cuda.current_stream().cuda_stream)."""
@@ -372,7 +404,14 @@ class DeviceBatch:
              "choice": np.zeros(N, np.uint32), "reachable": np.zeros(N, np.uint8), "passes": np.zeros(L, np.uint32)}
         self.ctx.check(self.L.esat_download_extract(self.h, *[_p(o[k]) for k in (
             "status", "err_class", "root_cost", "class_cost", "choice", "reachable", "passes")]))
+        self.ctx.tune_extract_lanes(self)
         return o
+
+    def extract_shape(self) -> tuple:
+        """(total e-classes, total Gauss-Seidel levels) of the last extraction over the batch."""
+        c, lv = C.c_uint64(), C.c_uint64()
+        self.ctx.check(self.L.esat_extract_shape(self.h, C.byref(c), C.byref(lv)))
+        return int(c.value), int(lv.value)
 
     def download_extract_light(self) -> dict:
         """Per-leaf status, error class / overflow mask and root cost only."""
@@ -380,6 +419,7 @@ class DeviceBatch:
         o = {"status": np.zeros(L, np.uint32), "err_class": np.zeros(L, np.uint32), "root_cost": np.zeros(L)}
         self.ctx.check(self.L.esat_download_extract(self.h, _p(o["status"]), _p(o["err_class"]), _p(o["root_cost"]),
                                                     None, None, None, None))
+        self.ctx.tune_extract_lanes(self)
         return o
 
     def download_extract_small(self, root_cost: np.ndarray, status: np.ndarray):

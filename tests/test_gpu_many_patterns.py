@@ -1,4 +1,4 @@
-"""e-match calls with more than 32 patterns (k_ematch runs one CTA per leaf and 32-pattern chunk):
+"""e-match calls with more than 32 patterns (one k_ematch launch per 32-pattern chunk):
 every call-pattern's match records, EXISTS answers, per-leaf masks and joins over sources in later
 chunks must equal those of the same patterns matched in one <= 32-pattern call, which
 test_gpu_parity pins to the reference."""
