@@ -3,9 +3,9 @@
 # Usage: bash tools/ab_extract.sh TAG "libA.so libB.so ..."
 OUT=gpurun_out/${1:-ab}; mkdir -p $OUT
 LIBS="$2"; SETS="${3:-resnext50:16384 resnext50:4096 nasrnn:4096 bert:4096}"
-[ -n "$NOPARITY" ] || timeout 900 python -m pytest -q -x --timeout 600 -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_scale.py tests/test_gpu_c4.py > $OUT/pytest_xt.log 2>&1
+[ -n "$NOPARITY" ] || timeout 900 python -m pytest -q -x --timeout 600 -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_scale.py tests/test_gpu_c4.py tests/test_gpu_many_patterns.py > $OUT/pytest_xt.log 2>&1
 echo "parity: $(tail -1 $OUT/pytest_xt.log)"
-for rep in 1 2; do
+for rep in ${REPS:-1}; do
 for V in $LIBS; do
   for mb in $SETS; do
     M=${mb%%:*}; B=${mb##*:}
