@@ -375,12 +375,9 @@ __global__ void ESAT_EMATCH_LB(T) k_ematch(Dev d, MArgs a) {
     __syncthreads();
     const uint32_t pwords = sp_so[MAXP];
     const bool progs_smem = pwords <= PROG_WORDS;
-    if (progs_smem)
-        for (uint32_t w = tid; w < pwords; w += T) {
-            uint32_t pi = 0;
-            while (pi + 1 < a.P && sp_so[pi + 1] <= w) pi++;
-            sprog[w] = a.prog[sp_po[pi] + (w - sp_so[pi])];
-        }
+    if (progs_smem)   // a warp per pattern, its lanes over the program's words
+        for (uint32_t pi = tid >> 5; pi < a.P; pi += T / 32)
+            for (uint32_t w = tid & 31u; w < sp_pn[pi]; w += 32) sprog[sp_so[pi] + w] = a.prog[sp_po[pi] + w];
     __syncthreads();
     if (need <= a.smem_bytes) mbar_wait(&bar, 0);
 
@@ -462,6 +459,14 @@ __global__ void ESAT_EMATCH_LB(T) k_ematch(Dev d, MArgs a) {
     __syncthreads();
     auto prog_ptr = [&](uint32_t pi) -> const int32_t* { return (progs_smem ? sprog : a.prog) + sp_off[pi]; };
     const uint32_t PC = P * C;
+    const float invC = C ? 1.0f / (float)C : 0.0f;
+    // i / C for i < P * C (quotient < 32): a float estimate, exact after one correction step
+    auto div_c = [&](uint32_t i) -> uint32_t {
+        uint32_t q = (uint32_t)((float)i * invC);
+        if (q * C > i) q--;
+        else if ((q + 1) * C <= i) q++;
+        return q;
+    };
     uint32_t* pc = a.raw + d.nb[l] * MAXP;   // [P][C] counts -> offsets (C <= n, P <= 32)
     uint32_t* nzl = a.nzl + d.nb[l] * MAXP;  // (pattern, class) pairs with matches (any order)
     __shared__ uint32_t sh_nz, sh_next, sh_next2;
@@ -470,7 +475,7 @@ __global__ void ESAT_EMATCH_LB(T) k_ematch(Dev d, MArgs a) {
     // (pattern, class) pairs are handed out dynamically: a thread that drew a heavy pair does not
     // also own a fixed share of the rest
     for (uint32_t i = tid; i < PC; i = atomicAdd(&sh_next, 1u)) {
-        const uint32_t pi = i / C, r = i - pi * C;
+        const uint32_t pi = div_c(i), r = i - pi * C;
         uint32_t n = 0;
         const uint32_t rb = sp_rbit[pi];
         if (((lmask >> pi) & 1u) && (!rb || (cmask[r] & rb))) {
@@ -555,7 +560,7 @@ __global__ void ESAT_EMATCH_LB(T) k_ematch(Dev d, MArgs a) {
             const uint32_t i = nzl[j];
             const uint32_t beg = pc[i], end = (i + 1 < PC) ? pc[i + 1] : grand;
             if (beg == end) continue;
-            const uint32_t pi = i / C, r = i - pi * C, W = sp_W[pi];
+            const uint32_t pi = div_c(i), r = i - pi * C, W = sp_W[pi];
             set_prog(prog_ptr(pi));
             uint32_t* o0 = a.out + sp_wbase[pi] + (uint64_t)(beg - sp_rbase[pi]) * W;
             uint32_t cur = 0;
