@@ -327,10 +327,10 @@ __device__ __forceinline__ uint32_t group_exscan(uint32_t v, uint32_t* smem, uin
 }
 
 #ifndef ESAT_XG_MINB
-#define ESAT_XG_MINB 24
+#define ESAT_XG_MINB 28
 #endif
 // G == T: <= 64 registers, 32 resident leaves (warps) per SM. G < 32: the lane groups need more
-// registers (<= 80 at 24 CTAs per SM: 48 or 96 resident leaves).
+// registers (<= 72 at 28 CTAs per SM: 56 resident leaves; 80 at 24 measured 1 % slower, 64 at 32 3 %).
 template <int T, int G>
 __global__ void __launch_bounds__(T, G == T ? 1024 / T : ESAT_XG_MINB) k_extract(Dev d, XArgs x) {
     // G lanes per leaf: G == T is one leaf per CTA (T = 32, 64, 128); G < 32 packs 32/G leaves into
