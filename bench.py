@@ -467,6 +467,8 @@ def measure_config(ctx, stream, dev, model, B, steps, warmup, world, rank, e2e_s
     # two device batches alternate so step i+1's H2D upload (copy engine) overlaps step i's
     # kernels; every step still uploads its own inputs and reads back its own results
     ctx2 = native.Context(ctx.device)   # its own stream: the two batches' steps overlap
+    if ctx.extract_lanes:                # the same extraction lane width as the tuned context
+        ctx2.set_extract_lanes(ctx.extract_lanes)
     pipe2 = LeafPipeline(ctx2, symarr, rules(), name_id, code, method="ocf", pool_entries_per_node=pipe.pool,
                          pool_bitsets_per_node=pipe.pool_bitsets)
     batch2 = pipe2.load(packed)
