@@ -55,7 +55,10 @@ struct JArgs {
     unsigned long long* big;    // [R][L][2] long-list pairs: scratch offsets of (index, record table); ~0 = none
 };
 
-constexpr uint32_t JOIN_SMEM_S1 = 4096;   // SMEM words for staged source-1 join fields
+#ifndef ESAT_JOIN_S1
+#define ESAT_JOIN_S1 2048
+#endif
+constexpr uint32_t JOIN_SMEM_S1 = ESAT_JOIN_S1;   // SMEM words for staged source-1 join fields (2048: 7 CTAs per SM; 4096 measured 11-15 % slower joins, 1024 unstages NasRNN)
 constexpr uint32_t JOIN_GSORT_WORDS = 1024; // per-warp words for merging a root group's product runs
 
 template <int T> __global__ void k_ematch(Dev, MArgs);
